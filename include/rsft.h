@@ -1,0 +1,177 @@
+/*
+ * rsft.h — C ABI of the B200-native (sm_100a) Realistic Sparse Fourier Transform hot path.
+ *
+ * Method: Wang, Patel, Petropulu, arXiv 1610.01050, Algorithm 1.
+ * Citations "P:<line>" refer to /root/reference/PAPER.md; "Lnn" to the readings in DESIGN.md.
+ *
+ * Pipeline per frame x in C^{N_0 x ... x N_{D-1}} (row-major, last dim contiguous), per loop l:
+ *   y = W x            pre-permutation window            (Alg. 1 l.5,  P:220)
+ *   p = P_{sigma,tau} y  per-dimension permutation       (Def. 1; l.6 P:221)
+ *   z = Wbar p         flat window                        (l.7 P:222)
+ *   f = Aliasing(z)    fold into B_0 x ... buckets        (Def. 2; l.8 P:223)
+ *   fhat = NDFFT_B(f)  forward, unnormalised              (l.9 P:224; L7)
+ *   c_l = |fhat|^2 > gamma_l                              (l.10 P:225; Eq. tpd; L8)
+ *   abar = sum_l Reverse(c_l)                             (l.11-12 P:226-227; Def. 4; Eq. a_i)
+ *   o = {i : abar_i >= mu}                                (l.14 P:229; L10)
+ *
+ * Conventions (all entry points):
+ *  - Every call returns rsft_status; RSFT_OK == 0.  No exceptions, no abort().
+ *  - The plan is host memory owned by the library (rsft_plan_destroy frees it).
+ *  - EVERY device buffer is caller-owned (input, outputs, workspace).  The library never
+ *    allocates device memory.  It never synchronises, except in the one-time rsft_bind
+ *    and in rsft_run_host (both documented below).
+ *  - Device work is issued only on the `stream` argument (a cudaStream_t passed as void*;
+ *    NULL = the legacy default stream).  Results are valid after the caller syncs it.
+ *  - Argument / shape errors are returned before any launch.  Launch failures return
+ *    RSFT_E_CUDA; the CUDA error string is kept in rsft_last_error().
+ *  - One host thread per plan at a time; distinct plans are independent.
+ *  - Data types: input frames are complex64 (interleaved float32 re, im).  Bitmaps are
+ *    uint32 words, bit k of word w <-> flat index 32 w + k (row-major flattening).
+ */
+#ifndef RSFT_H
+#define RSFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rsft_plan_s* rsft_plan_t;
+
+typedef enum {
+  RSFT_OK = 0,
+  RSFT_E_ARG = 1,          /* null pointer, bad range, mu/loops/p_fa out of range     */
+  RSFT_E_SHAPE = 2,        /* N_d or B_d not a power of two, B_d > N_d, support rule (L2)      */
+  RSFT_E_SIGMA = 3,        /* even sigma in rsft_set_schedule (Eq. mod_inv)     */
+  RSFT_E_UNSUPPORTED = 4,  /* D > 3, B_d > 64, L > 32, N_last < 32, or tables beyond smem     */
+  RSFT_E_WORKSPACE = 5,    /* workspace missing, too small or misaligned (256 B)              */
+  RSFT_E_CUDA = 6,         /* a CUDA runtime call or launch failed (see rsft_last_error)      */
+  RSFT_E_STATE = 7         /* plan not bound (rsft_bind) before a device call                 */
+} rsft_status;
+
+typedef enum {
+  RSFT_WIN_RECT = 0,       /* w = 1                                                           */
+  RSFT_WIN_HANN = 1,       /* periodic Hann w[n] = sin^2(pi n / N)  (BASELINE; L3)            */
+  RSFT_WIN_CHEB = 2        /* periodic Dolph-Chebyshev, prewin_param dB        */
+} rsft_win;
+
+typedef enum {
+  RSFT_MODE_AUTO = 0,      /* library picks                                                   */
+  RSFT_MODE_FUSED = 1,     /* one CTA per frame: fold + FFT + threshold fused (D <= 2)        */
+  RSFT_MODE_SPLIT = 2      /* CTA per (frame, outer residue class) + outer-FFT kernel (D >= 2) */
+} rsft_mode;
+
+typedef struct {
+  int32_t ndim;            /* D in 1..3 ("any fixed dimension")                          */
+  int64_t n[3];            /* N_d, powers of two                                       */
+  int64_t b[3];            /* B_d, powers of two, 1 <= B_d <= min(N_d, 64) (Def. 2)       */
+  int64_t support[3];      /* flat-window support W_d; 0 => N_d; need 2 B_d | W_d <= N_d */
+  int32_t loops;           /* L (the paper's T iterations, Alg. 1 l.4 P:219), 1..32           */
+  int32_t prewin;          /* rsft_win of the pre-permutation window               */
+  double prewin_param;     /* Chebyshev attenuation dB when prewin == RSFT_WIN_CHEB           */
+  double flat_atten_db;    /* Dolph-Chebyshev taper of the flat window, default 60 (L2)       */
+  double p_fa;             /* first-stage per-bucket false-alarm probability, (0,1) (L8)      */
+  double noise_var;        /* sigma_n^2 > 0 (L11)                                      */
+  double gamma_override;   /* > 0: gamma_l = gamma_override for every loop       */
+  int32_t mu;              /* second-stage vote threshold 1..L (L9)                    */
+  int32_t random_tau;      /* 0: tau = 0; 1: seeded tau (L4)                          */
+  uint64_t seed;           /* sigma/tau schedule seed (L5)                                    */
+  int64_t max_batch;       /* largest batch passed to execute/detect (sizes the workspace)    */
+  int32_t mode;            /* rsft_mode                                                       */
+} rsft_params;
+
+/* Fill defaults: D=1, loops=1, Hann, 60 dB flat taper, p_fa=1e-6, noise_var=1, mu=loops,
+ * tau=0, max_batch=1, mode auto. */
+void rsft_default_params(rsft_params* p);
+
+/* Validate params and build the host plan (windows, sigma/sigma^{-1}/tau schedule, per-loop
+ * weight tables, beta_l, gamma_l).  Host only: no CUDA call.  Errors: E_ARG, E_SHAPE,
+ * E_UNSUPPORTED.  *out is set to NULL on error. */
+rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out);
+void rsft_plan_destroy(rsft_plan_t plan);
+
+/* Replace the seeded schedule.  sigma: [L][D] odd values in [N_d] (Def. 1: sigma invertible
+ * mod N_d); tau: [L][D] in [N_d] or NULL (=> 0).  Recomputes tables, beta, gamma and
+ * marks the plan unbound.  Errors: E_SIGMA (even sigma), E_ARG. */
+rsft_status rsft_set_schedule(rsft_plan_t plan, const int64_t* sigma, const int64_t* tau);
+
+/* Read back the schedule ([L][D] each; any pointer may be NULL). */
+rsft_status rsft_get_schedule(rsft_plan_t plan, int64_t* sigma, int64_t* sigma_inv, int64_t* tau);
+
+/* beta_l = ||Wbar P_sigma_l w||^2 (Eq. alpha_beta) and gamma_l (Eq. tpd),
+ * fp64, [L] each; either pointer may be NULL. */
+rsft_status rsft_get_thresholds(rsft_plan_t plan, double* beta, double* gamma);
+
+/* Plan-time windows for dimension d, fp64 [N_d]: which = 0 -> pre-window w_d;
+ * which = 1 -> real flat prototype g_d (gbar_d = g_d e^{-j pi t/B_d}, L1-L2);
+ * which = 2 -> fp32 per-loop weight table h_{l,d}[s] widened to fp64, [L][N_d] (I3). */
+rsft_status rsft_get_window(rsft_plan_t plan, int32_t d, int32_t which, double* out);
+
+/* Derived sizes. */
+typedef struct {
+  int64_t ntot, btot;          /* prod N_d, prod B_d                                        */
+  int64_t bitmap_words;        /* words per loop per frame = ceil(B_tot / 32)                */
+  int64_t detect_words;        /* words per frame of the detection bitmap = ceil(N_tot / 32) */
+  int32_t mode;                /* resolved rsft_mode for batch = max_batch                   */
+  int32_t lpad;                /* compile-time loop count used by the fold kernels          */
+  size_t workspace_bytes;
+} rsft_info;
+rsft_status rsft_get_info(rsft_plan_t plan, rsft_info* info);
+size_t rsft_workspace_bytes(rsft_plan_t plan);
+
+/* Upload the plan tables into the caller-owned device workspace (>= rsft_workspace_bytes,
+ * 256-byte aligned) on `stream`, on the current CUDA device, and synchronise `stream`.  The workspace must stay alive
+ * and untouched while the plan is used.  Errors: E_WORKSPACE, E_CUDA. */
+rsft_status rsft_bind(rsft_plan_t plan, void* d_workspace, size_t bytes, void* stream);
+
+/* First stage for loops [loop_begin, loop_end) of `batch` frames (Alg. 1 l.5-10):
+ *   d_x        device, complex64 [batch][N_0]...[N_{D-1}], 16-byte aligned, read once.
+ *   d_bitmaps  device, uint32 [batch][loop_end-loop_begin][bitmap_words]: bit k set iff
+ *              |fhat_l[k]|^2 > gamma_l (flat bucket index k, row-major over B_d).
+ *   d_spectra  NULL, or device complex64 [batch][loop_end-loop_begin][B_tot]: fhat (parity).
+ * Errors: E_ARG (range, batch > max_batch, null), E_STATE, E_CUDA. */
+rsft_status rsft_execute(rsft_plan_t plan, const void* d_x, int64_t batch, int32_t loop_begin,
+                         int32_t loop_end, uint32_t* d_bitmaps, void* d_spectra, void* stream);
+
+/* Reverse mapping + accumulation + second-stage test (Alg. 1 l.11-14) for locations whose
+ * dim-0 index lies in [dim0_begin, dim0_end) (sharded voting; full range = [0, N_0)):
+ *   d_bitmaps  device uint32 [batch][L][bitmap_words] — ALL loops of the plan.
+ *   d_detect   device uint32 [batch][ceil((dim0_end-dim0_begin) * N_tot/N_0 / 32)]:
+ *              bit i set iff abar_i >= mu (location index relative to the slab start).
+ *   d_counts   NULL, or device uint8 [batch][(dim0_end-dim0_begin) * N_tot/N_0]: abar.
+ * D == 1 requires the full range.  The slab size times N_tot/N_0 must be a multiple of 32.
+ * Errors: E_ARG, E_STATE, E_CUDA. */
+rsft_status rsft_detect(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t batch,
+                        int64_t dim0_begin, int64_t dim0_end, uint32_t* d_detect,
+                        uint8_t* d_counts, void* stream);
+
+/* Detection bitmap (full range, [batch][detect_words]) -> ascending flat indices
+ * frame * N_tot + i of the set bits, written to d_idx[0 .. min(count, capacity)).
+ * *d_count (device int64) receives the true count; count > capacity means truncated
+ * (no sync is performed, so overflow is reported in *d_count, not in the return value).
+ * Uses the workspace's compaction scratch.  Errors: E_ARG, E_STATE, E_CUDA. */
+rsft_status rsft_compact(rsft_plan_t plan, const uint32_t* d_detect, int64_t batch,
+                         int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);
+
+/* End-to-end convenience call on HOST buffers (blocking: synchronises `stream`):
+ * copies h_x (complex64 [batch][N...], pinned recommended) into d_scratch, runs execute,
+ * detect and compact, and copies the count and min(count, capacity) indices back.
+ * d_scratch: device buffer of >= rsft_host_scratch_bytes(plan, batch, capacity) bytes.
+ * Returns the true count in *h_count.  Errors: as above. */
+size_t rsft_host_scratch_bytes(rsft_plan_t plan, int64_t batch, int64_t capacity);
+rsft_status rsft_run_host(rsft_plan_t plan, const void* h_x, int64_t batch, int64_t* h_idx,
+                          int64_t capacity, int64_t* h_count, void* d_scratch,
+                          size_t scratch_bytes, void* stream);
+
+/* Number of kernels the last execute/detect/compact/run_host call launched. */
+int32_t rsft_last_launch_count(rsft_plan_t plan);
+
+const char* rsft_status_string(rsft_status s);
+const char* rsft_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSFT_H */

@@ -1,0 +1,172 @@
+// C ABI entry points that touch the device: bind, execute, detect, compact, run_host.
+// See include/rsft.h for the contract of every call.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "rsft_internal.h"
+
+namespace rsft {
+rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                           void* spectra, cudaStream_t st);
+rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                          uint32_t* det, uint8_t* counts, cudaStream_t st);
+rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
+                           int64_t capacity, int64_t* d_count, cudaStream_t st);
+rsft_status upload_twiddles(cudaStream_t st);
+
+static rsft_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RSFT_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return RSFT_E_CUDA;
+}
+static int ilog2i(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+}  // namespace rsft
+
+using namespace rsft;
+
+extern "C" {
+
+rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
+  if (!p) return RSFT_E_ARG;
+  if (!d_ws || bytes < p->ws.total || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return RSFT_E_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rsft_status s;
+  int dev = 0;
+  if ((s = cuda_check(cudaGetDevice(&dev), "cudaGetDevice"))) return s;
+  int sms = 0;
+  if ((s = cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count"))) return s;
+  p->device = dev;
+  p->num_sms = sms;
+  char* base = reinterpret_cast<char*>(d_ws);
+  static thread_local std::vector<LoopDev> loops;
+  loops.assign(p->L, LoopDev{});
+  for (int l = 0; l < p->L; ++l) {
+    for (int d = 0; d < 3; ++d) {
+      loops[l].sig[d] = d < p->D ? (int32_t)p->sigma[l * p->D + d] : 1;
+      loops[l].sinv[d] = d < p->D ? (int32_t)p->sinv[l * p->D + d] : 1;
+      loops[l].tau[d] = d < p->D ? (int32_t)p->tau[l * p->D + d] : 0;
+    }
+    loops[l].gamma = (float)p->gamma[l];
+  }
+  if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.loops_off, loops.data(), sizeof(LoopDev) * p->L,
+                                      cudaMemcpyHostToDevice, st), "upload loops"))) return s;
+  for (int d = 0; d < p->D; ++d)
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.h_off[d], p->hf[d].data(), sizeof(float) * p->hf[d].size(),
+                                        cudaMemcpyHostToDevice, st), "upload weights"))) return s;
+  if ((s = upload_twiddles(st))) return s;
+  if ((s = cuda_check(cudaStreamSynchronize(st), "bind sync"))) return s;   // tables are host temporaries
+
+  PlanDev& pd = p->dev;
+  pd = PlanDev{};
+  pd.D = p->D;
+  pd.L = p->L;
+  pd.mu = p->mu;
+  pd.nplanes = 6;
+  for (int d = 0; d < 3; ++d) {
+    int64_t n = d < p->D ? p->n[d] : 1, b = d < p->D ? p->b[d] : 1;
+    pd.n[d] = (int32_t)n; pd.b[d] = (int32_t)b; pd.a[d] = (int32_t)(n / b);
+    pd.lgn[d] = ilog2i(n); pd.lgb[d] = ilog2i(b); pd.lga[d] = ilog2i(n / b);
+    pd.shift[d] = (d < p->D && b < n) ? 1 : 0;
+    pd.h[d] = d < p->D ? reinterpret_cast<const float*>(base + p->ws.h_off[d]) : nullptr;
+  }
+  pd.ntot = p->ntot;
+  pd.btot = p->btot;
+  pd.wpl = (int32_t)((p->btot + 31) / 32);
+  pd.nlast = (int32_t)p->n[p->D - 1];
+  pd.blast = (int32_t)p->b[p->D - 1];
+  pd.rows = p->ntot / p->n[p->D - 1];
+  pd.bouter = (int32_t)(p->btot / p->b[p->D - 1]);
+  int64_t aouter = 1;
+  for (int d = 0; d + 1 < p->D; ++d) aouter *= p->a[d];
+  pd.aouter = (int32_t)aouter;
+  pd.loops = reinterpret_cast<const LoopDev*>(base + p->ws.loops_off);
+  pd.fbuf = reinterpret_cast<float2*>(base + p->ws.fbuf_off);
+  pd.chunk_counts = reinterpret_cast<long long*>(base + p->ws.chunk_off);
+  pd.chunk_capacity = p->ws.chunk_capacity;
+  p->d_ws = d_ws;
+  p->bound = true;
+  return RSFT_OK;
+}
+
+rsft_status rsft_execute(rsft_plan_t p, const void* d_x, int64_t batch, int32_t loop_begin, int32_t loop_end,
+                         uint32_t* d_bitmaps, void* d_spectra, void* stream) {
+  if (!p || !d_x || !d_bitmaps) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
+  if (loop_begin < 0 || loop_end > p->L || loop_begin >= loop_end) return RSFT_E_ARG;
+  if (reinterpret_cast<uintptr_t>(d_x) & 15) return RSFT_E_ARG;
+  p->last_launches = 0;
+  if (batch == 0) return RSFT_OK;
+  return launch_execute(p, d_x, batch, loop_begin, loop_end - loop_begin, d_bitmaps, d_spectra,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+rsft_status rsft_detect(rsft_plan_t p, const uint32_t* d_bitmaps, int64_t batch, int64_t d0b, int64_t d0e,
+                        uint32_t* d_detect, uint8_t* d_counts, void* stream) {
+  if (!p || !d_bitmaps || !d_detect) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
+  if (d0b < 0 || d0e > p->n[0] || d0b >= d0e) return RSFT_E_ARG;
+  if (p->D == 1 && (d0b != 0 || d0e != p->n[0])) return RSFT_E_ARG;
+  if (((d0e - d0b) * (p->ntot / p->n[0])) % 32) return RSFT_E_ARG;
+  p->last_launches = 0;
+  if (batch == 0) return RSFT_OK;
+  return launch_detect(p, d_bitmaps, batch, d0b, d0e, d_detect, d_counts, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rsft_status rsft_compact(rsft_plan_t p, const uint32_t* d_detect, int64_t batch, int64_t* d_idx,
+                         int64_t capacity, int64_t* d_count, void* stream) {
+  if (!p || !d_detect || !d_count || (capacity > 0 && !d_idx) || capacity < 0) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
+  p->last_launches = 0;
+  return launch_compact(p, d_detect, batch, d_idx, capacity, d_count, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t rsft_host_scratch_bytes(rsft_plan_t p, int64_t batch, int64_t capacity) {
+  if (!p || batch < 1) return 0;
+  size_t x = align256((size_t)batch * p->ntot * 8);
+  size_t bm = align256((size_t)batch * p->L * ((p->btot + 31) / 32) * 4);
+  size_t det = align256((size_t)batch * ((p->ntot + 31) / 32) * 4);
+  size_t idx = align256((size_t)(capacity > 0 ? capacity : 1) * 8);
+  return x + bm + det + idx + 256;
+}
+
+rsft_status rsft_run_host(rsft_plan_t p, const void* h_x, int64_t batch, int64_t* h_idx, int64_t capacity,
+                          int64_t* h_count, void* d_scratch, size_t scratch_bytes, void* stream) {
+  if (!p || !h_x || !h_count || (capacity > 0 && !h_idx) || capacity < 0) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
+  if (!d_scratch || scratch_bytes < rsft_host_scratch_bytes(p, batch, capacity) ||
+      (reinterpret_cast<uintptr_t>(d_scratch) & 255)) return RSFT_E_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* base = reinterpret_cast<char*>(d_scratch);
+  size_t off = 0;
+  void* dx = base + off; off += align256((size_t)batch * p->ntot * 8);
+  uint32_t* dbm = reinterpret_cast<uint32_t*>(base + off); off += align256((size_t)batch * p->L * ((p->btot + 31) / 32) * 4);
+  uint32_t* ddet = reinterpret_cast<uint32_t*>(base + off); off += align256((size_t)batch * ((p->ntot + 31) / 32) * 4);
+  int64_t* didx = reinterpret_cast<int64_t*>(base + off); off += align256((size_t)(capacity > 0 ? capacity : 1) * 8);
+  int64_t* dcount = reinterpret_cast<int64_t*>(base + off);
+  rsft_status s;
+  int32_t launches = 0;
+  if ((s = cuda_check(cudaMemcpyAsync(dx, h_x, (size_t)batch * p->ntot * 8, cudaMemcpyHostToDevice, st), "H2D x"))) return s;
+  if ((s = rsft_execute(p, dx, batch, 0, p->L, dbm, nullptr, stream))) return s;
+  launches += p->last_launches;
+  if ((s = rsft_detect(p, dbm, batch, 0, p->n[0], ddet, nullptr, stream))) return s;
+  launches += p->last_launches;
+  if ((s = rsft_compact(p, ddet, batch, didx, capacity, dcount, stream))) return s;
+  launches += p->last_launches;
+  if ((s = cuda_check(cudaMemcpyAsync(h_count, dcount, 8, cudaMemcpyDeviceToHost, st), "D2H count"))) return s;
+  if ((s = cuda_check(cudaStreamSynchronize(st), "sync"))) return s;
+  int64_t n = *h_count < capacity ? *h_count : capacity;
+  if (n > 0) {
+    if ((s = cuda_check(cudaMemcpyAsync(h_idx, didx, (size_t)n * 8, cudaMemcpyDeviceToHost, st), "D2H idx"))) return s;
+    if ((s = cuda_check(cudaStreamSynchronize(st), "sync"))) return s;
+  }
+  p->last_launches = launches;
+  return RSFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,765 @@
+// RSFT hot-path kernels for sm_100a (B200).  Hand-written CUDA; no cuFFT, no libraries.
+//
+//   K1 fold   : pre-window + permutation + flat window + aliasing, all L loops in ONE coalesced
+//               pass over x (factored form I3): per element and loop one
+//               complex x real FMA; permutation costs no data movement (identity I2).
+//               Alg. 1 l.5-8; Defs. 1-2; Eqs. z, l.
+//   K2 FFT    : half-bucket twiddle + B-point N-D FFT in registers + |.|^2 + NP threshold +
+//               warp ballot -> bitmaps.  Alg. 1 l.9-10; Eq. tpd.
+//   K3 vote   : reverse mapping + accumulation + second stage, word-parallel (32 locations
+//               per lane-op) with bit-sliced counters.  Alg. 1 l.11-14; Def. 4;
+//               Eq. a_i; identity I1 (Props. 3-4).
+//   K4 compact: detection bitmap -> sorted flat index list (popc + scans).
+//
+// Fused mode (D <= 2, many frames): K1 + K2 in one persistent kernel, one CTA per frame;
+// the [L][B] buckets never leave shared memory.  Split mode (D >= 2, big frames): K1 per
+// (frame, outer residue class) + an outer-dimension FFT kernel.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "rsft_internal.h"
+
+namespace rsft {
+
+__constant__ float2 c_tw128[128];   // e^{-j 2 pi k / 128}, k < 128 (fp64-rounded at bind)
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+// Streaming 16-byte load: x is read exactly once, keep it out of L1.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int brev(int v, int lg) { return lg ? (int)(__brev((unsigned)v) >> (32 - lg)) : 0; }
+
+// Multi-axis view of a shared-memory array: element (i_0, ..., i_{k-1}) lives at
+// sum_a i_a * st[a].  Axis 0 (loops) may have any size; axes >= 1 are powers of two.
+struct View {
+  int k;
+  int n[4], lg[4], st[4];
+};
+
+// In-place radix-2 DIT FFT along axis a (forward e^{-j...}, unnormalised; reading L7) of a
+// View whose axis-a data is in bit-reversed order; output natural order.  Stage-parallel:
+// every thread of the CTA takes butterflies of every line, one __syncthreads per stage.
+// tw = shared copy of e^{-j 2 pi k / 128}.
+__device__ __noinline__ void fft_axis(float2* A, const View v, int a, const float2* __restrict__ tw) {
+  const int lgn = v.lg[a];
+  if (lgn == 0) return;
+  int lines = 1;
+  for (int i = 0; i < v.k; ++i) if (i != a) lines *= v.n[i];
+  const int nbf = lines << (lgn - 1);
+  const int sa = v.st[a];
+  for (int s = 1; s <= lgn; ++s) {
+    const int half = 1 << (s - 1);
+    for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
+      int j = bf & (half - 1);
+      int g = (bf >> (s - 1)) & ((1 << (lgn - s)) - 1);
+      int rest = bf >> (lgn - 1);
+      int off = 0;
+      for (int i = v.k - 1; i >= 1; --i) {
+        if (i == a) continue;
+        off += (rest & (v.n[i] - 1)) * v.st[i];
+        rest >>= v.lg[i];
+      }
+      off += rest * v.st[0];
+      float2* e0 = A + off + ((g << s) + j) * sa;
+      float2* e1 = e0 + half * sa;
+      float2 u = *e0;
+      float2 t = cmul(tw[j << (7 - s)], *e1);
+      *e0 = cadd(u, t);
+      *e1 = csub(u, t);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void load_twiddles(float2* tw) {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
+}
+
+// acc += w * v for a complex pair v: one complex x real MAC as a single packed
+// fma.rn.f32x2 (SASS: FFMA2 R, R.F32, R.F32x2, R.F32x2 on sm_100a).
+__device__ __forceinline__ void mac(float2& acc, float w, float vx, float vy) {
+  asm("{\n\t.reg .b64 a, ww, v;\n\tmov.b64 a, {%0,%1};\n\tmov.b64 ww, {%2,%2};\n\t"
+      "mov.b64 v, {%3,%4};\n\tfma.rn.f32x2 a, ww, v, a;\n\tmov.b64 {%0,%1}, a;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y) : "f"(w), "f"(vx), "f"(vy));
+}
+
+// Column weights + lane fold.  Lane owns columns c = base + 2*lane_col + e (e = 0,1); its
+// residues (2*lane + e) mod B_last (B_last <= 64 divides 64).  Lanes whose index agrees
+// mod B_last/2 share residues and are summed with xor shuffles.  After the call lanes
+// < max(B_last/2,1) hold residue sums for residues 2*lane + e (e < min(B_last,2)).
+template <int LP>
+__device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float* __restrict__ hlast,
+                                               int l0, int nl, int nlast, int col, int blast) {
+#pragma unroll
+  for (int l = 0; l < LP; ++l) {
+    float2 hc = make_float2(0.f, 0.f);
+    if (l < nl) hc = __ldg(reinterpret_cast<const float2*>(hlast + (size_t)(l0 + l) * nlast + col));
+    acc[l][0].x *= hc.x; acc[l][0].y *= hc.x;
+    acc[l][1].x *= hc.y; acc[l][1].y *= hc.y;
+  }
+  for (int off = blast >= 2 ? blast / 2 : 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int l = 0; l < LP; ++l)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        acc[l][e].x += __shfl_xor_sync(0xffffffffu, acc[l][e].x, off);
+        acc[l][e].y += __shfl_xor_sync(0xffffffffu, acc[l][e].y, off);
+      }
+  }
+  if (blast == 1) {
+#pragma unroll
+    for (int l = 0; l < LP; ++l) acc[l][0] = cadd(acc[l][0], acc[l][1]);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Fused mode: persistent, one CTA per frame.  D in {1, 2}, N_last >= 64.
+// smem: F [G][nl][bouter][blast+1] | Gb [nl][bouter][blast+1] | tw[128] float2 |
+//       rowW [N0][LP] float (D == 2)
+// ------------------------------------------------------------------------------------
+template <int LP, int U>
+__global__ void __launch_bounds__(kThreads) k_fused(PlanDev pd, const float4* __restrict__ x,
+                                                    int64_t batch, int l0, int nl,
+                                                    uint32_t* __restrict__ bitmaps,
+                                                    float2* __restrict__ spectra) {
+  extern __shared__ float4 smem_f4[];
+  const int D = pd.D;
+  const int blast = pd.blast, nlast = pd.nlast, bouter = pd.bouter;
+  const int fstride = blast + 1;
+  const int nseg = nlast >> 6;
+  const int G = (D == 1) ? (nseg < 8 ? nseg : 8) : 1;
+  float2* F = reinterpret_cast<float2*>(smem_f4);
+  const int fslot = nl * bouter * fstride;        // one group's slot
+  float2* Gb = F + (size_t)G * fslot;             // FFT buffer [nl][bouter][fstride]
+  float2* tw = Gb + fslot;                        // 128 twiddles
+  float* rowW = reinterpret_cast<float*>(tw + 128);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+
+  load_twiddles(tw);
+  if (D == 2) {
+    const int n0 = pd.n[0];
+    for (int i = tid; i < n0 * LP; i += blockDim.x) {
+      int s0 = i / LP, l = i - s0 * LP;
+      rowW[i] = l < nl ? pd.h[0][(size_t)(l0 + l) * n0 + s0] : 0.f;
+    }
+  }
+  const float* __restrict__ hlast = pd.h[D - 1];
+  const int ntasks = bouter * G;
+  const int nrows = nlast >> 1;                   // float4 per row
+  const int fold_lanes = blast >= 2 ? blast / 2 : 1;
+  const int fold_e = blast >= 2 ? 2 : 1;
+
+  for (int64_t frame = blockIdx.x; frame < batch; frame += gridDim.x) {
+    for (int i = tid; i < G * fslot; i += blockDim.x) F[i] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const float4* __restrict__ xf = x + frame * (pd.ntot >> 1);
+    for (int task = warp; task < ntasks; task += nwarps) {
+      const int kappa = task / G, g = task - kappa * G;
+      for (int seg = g; seg < nseg; seg += G) {
+        float2 acc[LP][2];
+#pragma unroll
+        for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
+        const int col4 = seg * 32 + lane;
+        if (D == 2) {
+          const int A0 = pd.a[0], B0 = pd.b[0];
+          for (int a = 0; a < A0; a += U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              int s0 = kappa + B0 * (a + u);
+              v[u] = (a + u < A0) ? ld_stream(xf + (size_t)s0 * nrows + col4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              int s0 = kappa + B0 * (a + u);
+              if (a + u >= A0) s0 = kappa;        // weight irrelevant: v == 0
+              const float2* wr = reinterpret_cast<const float2*>(rowW + s0 * LP);
+#pragma unroll
+              for (int l2 = 0; l2 < LP / 2; ++l2) {
+                float2 w = wr[l2];
+                mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
+                mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
+                mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
+                mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+              }
+            }
+          }
+        } else {
+          float4 v = ld_stream(xf + col4);
+#pragma unroll
+          for (int l = 0; l < LP; ++l) {
+            acc[l][0] = make_float2(v.x, v.y);
+            acc[l][1] = make_float2(v.z, v.w);
+          }
+        }
+        colweight_fold<LP>(acc, hlast, l0, nl, nlast, 2 * col4, blast);
+        if (lane < fold_lanes) {
+          float2* slot = F + (size_t)g * fslot + kappa * fstride + 2 * lane;
+#pragma unroll
+          for (int l = 0; l < LP; ++l)
+            if (l < nl)
+              for (int e = 0; e < fold_e; ++e) {
+                float2* dst = slot + (size_t)l * bouter * fstride + e;
+                *dst = cadd(*dst, acc[l][e]);
+              }
+        }
+      }
+    }
+    __syncthreads();
+    if (G > 1) {                                  // deterministic combine of segment groups
+      for (int i = tid; i < fslot; i += blockDim.x) {
+        float2 s = F[i];
+        for (int gg = 1; gg < G; ++gg) s = cadd(s, F[(size_t)gg * fslot + i]);
+        F[i] = s;
+      }
+      __syncthreads();
+    }
+    // residue -> bucket (b_d = sigma^{-1}(r_d - tau_d) mod B_d, I3) with the half-bucket
+    // twiddles e^{-j pi b_d / B_d} (L1), written bit-reversed for the in-place DIT FFT.
+    {
+      const int dl = D - 1;
+      const int lgbl = pd.lgb[dl], lgb0 = pd.lgb[0];
+      const int nel = nl * bouter * blast;
+      for (int i = tid; i < nel; i += blockDim.x) {
+        int l = i / (bouter * blast), rem = i - l * bouter * blast;
+        int ro = rem >> lgbl, rl = rem & (blast - 1);
+        const LoopDev& lp = pd.loops[l0 + l];
+        int bl = (lp.sinv[dl] * (rl - lp.tau[dl])) & (blast - 1);
+        float2 v = F[((size_t)l * bouter + ro) * fstride + rl];
+        if (pd.shift[dl]) v = cmul(v, tw[bl << (6 - lgbl)]);
+        int bo = 0;
+        if (D == 2) {
+          bo = (lp.sinv[0] * (ro - lp.tau[0])) & (bouter - 1);
+          if (pd.shift[0]) v = cmul(v, tw[bo << (6 - lgb0)]);
+          bo = brev(bo, lgb0);
+        }
+        Gb[((size_t)l * bouter + bo) * fstride + brev(bl, lgbl)] = v;
+      }
+    }
+    __syncthreads();
+    {
+      View vw;
+      vw.k = 3;
+      vw.n[0] = nl; vw.lg[0] = 0; vw.st[0] = bouter * fstride;
+      vw.n[1] = bouter; vw.lg[1] = D == 2 ? pd.lgb[0] : 0; vw.st[1] = fstride;
+      vw.n[2] = blast; vw.lg[2] = pd.lgb[D - 1]; vw.st[2] = 1;
+      fft_axis(Gb, vw, 2, tw);
+      if (D == 2) fft_axis(Gb, vw, 1, tw);
+    }
+    // |fhat|^2 > gamma_l -> ballot -> bitmap words (Alg. 1 l.10)
+    const int wpl = pd.wpl;
+    const int nitems = nl * wpl * 32;
+    for (int it = tid; it < nitems; it += blockDim.x) {
+      int l = it / (wpl * 32), rem = it - l * wpl * 32;
+      int k = rem;                                 // flat bucket index
+      bool bit = false;
+      if (k < pd.btot) {
+        int ko = k / blast, kl = k - ko * blast;
+        float2 v = Gb[((size_t)l * bouter + ko) * fstride + kl];
+        float pw = v.x * v.x + v.y * v.y;
+        bit = pw > pd.loops[l0 + l].gamma;
+        if (spectra) spectra[((size_t)frame * nl + l) * pd.btot + k] = v;
+      }
+      unsigned word = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0) bitmaps[((size_t)frame * nl + l) * wpl + (rem >> 5)] = word;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Split mode, kernel 1: one CTA per (outer residue class kappa, frame); D in {2, 3}.
+// smem: tw[128] | sbo[32] | rw [RA][LP] float | part [nwarps][nl][blast] | R [nl][blast+1]
+// Output fbuf[frame][l][Bo(l)][k_last]: last-dim FFT done, outer twiddles applied.
+// ------------------------------------------------------------------------------------
+template <int LP, int U>
+__global__ void __launch_bounds__(kThreads) k_split_fold(PlanDev pd, const float4* __restrict__ x,
+                                                         int l0, int nl, uint32_t* __restrict__ bitmaps) {
+  extern __shared__ float4 smem_f4[];
+  const int D = pd.D;
+  const int kappa = blockIdx.x;
+  const int64_t frame = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int blast = pd.blast, nlast = pd.nlast;
+  const int RA = pd.aouter;
+  float2* tw = reinterpret_cast<float2*>(smem_f4);
+  int* sbo = reinterpret_cast<int*>(tw + 128);       // [32] outer bucket per loop
+  float* rw = reinterpret_cast<float*>(sbo + kMaxLoops);
+  float2* part = reinterpret_cast<float2*>(rw + (size_t)RA * LP);
+  float2* R = part + (size_t)nwarps * nl * blast;
+  load_twiddles(tw);
+
+  // outer residues of the class and row enumeration
+  int r0, r1 = 0;
+  if (D == 3) { r0 = kappa / pd.b[1]; r1 = kappa - r0 * pd.b[1]; } else { r0 = kappa; }
+  for (int i = tid; i < RA * LP; i += blockDim.x) {
+    int q = i / LP, l = i - q * LP;
+    float w = 0.f;
+    if (l < nl) {
+      if (D == 3) {
+        int a0 = q / pd.a[1], a1 = q - a0 * pd.a[1];
+        int s0 = r0 + pd.b[0] * a0, s1 = r1 + pd.b[1] * a1;
+        w = pd.h[0][(size_t)(l0 + l) * pd.n[0] + s0] * pd.h[1][(size_t)(l0 + l) * pd.n[1] + s1];
+      } else {
+        int s0 = r0 + pd.b[0] * q;
+        w = pd.h[0][(size_t)(l0 + l) * pd.n[0] + s0];
+      }
+    }
+    rw[i] = w;
+  }
+  // zero this frame's bitmap words (K2 sets bits with atomicOr)
+  {
+    const int64_t words = (int64_t)nl * pd.wpl;
+    uint32_t* bm = bitmaps + frame * words;
+    for (int64_t w = (int64_t)kappa * blockDim.x + tid; w < words; w += (int64_t)gridDim.x * blockDim.x) bm[w] = 0u;
+  }
+  for (int i = tid; i < nwarps * nl * blast; i += blockDim.x) part[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+
+  const int nseg = nlast >= 64 ? nlast >> 6 : 1;
+  const int rpw = nlast >= 64 ? 1 : 64 / nlast;      // rows per warp-load
+  const int lpr = 32 / rpw;                          // lanes per row
+  const int lane_row = lane / lpr, lane_c4 = lane - lane_row * lpr;
+  const int nq = (RA + rpw - 1) / rpw;               // warp-load row groups
+  const int nrows4 = nlast >> 1;
+  const float4* __restrict__ xf = x + frame * (pd.ntot >> 1);
+  const int fold_lanes = blast >= 2 ? blast / 2 : 1;
+  const int fold_e = blast >= 2 ? 2 : 1;
+
+  int seg_start, seg_step, wsub, wps;
+  if (nseg >= nwarps) { seg_start = warp; seg_step = nwarps; wsub = 0; wps = 1; }
+  else {
+    wps = nwarps / nseg;
+    seg_start = warp < wps * nseg ? warp % nseg : nseg;
+    seg_step = nseg;
+    wsub = warp / nseg;
+  }
+  for (int seg = seg_start; seg < nseg; seg += seg_step) {
+    float2 acc[LP][2];
+#pragma unroll
+    for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
+    const int c4 = seg * 32 + lane_c4;
+    for (int qg = wsub; qg < nq; qg += U * wps) {
+      float4 v[U];
+      int qq[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int q = (qg + u * wps) * rpw + lane_row;
+        qq[u] = q;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (qg + u * wps < nq && q < RA) {
+          int64_t row;
+          if (D == 3) {
+            int a0 = q / pd.a[1], a1 = q - a0 * pd.a[1];
+            row = (int64_t)(r0 + pd.b[0] * a0) * pd.n[1] + (r1 + pd.b[1] * a1);
+          } else {
+            row = r0 + (int64_t)pd.b[0] * q;
+          }
+          v[u] = ld_stream(xf + row * nrows4 + c4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int q = qq[u] < RA ? qq[u] : 0;
+        const float2* wr = reinterpret_cast<const float2*>(rw + (size_t)q * LP);
+#pragma unroll
+        for (int l2 = 0; l2 < LP / 2; ++l2) {
+          float2 w = wr[l2];
+          mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
+          mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
+          mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
+          mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+        }
+      }
+    }
+    colweight_fold<LP>(acc, pd.h[D - 1], l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
+    if (lane < fold_lanes) {
+#pragma unroll
+      for (int l = 0; l < LP; ++l)
+        if (l < nl)
+          for (int e = 0; e < fold_e; ++e) {
+            float2* dst = part + ((size_t)warp * nl + l) * blast + 2 * lane + e;
+            *dst = cadd(*dst, acc[l][e]);
+          }
+    }
+  }
+  __syncthreads();
+  // combine warps (fixed order), residue -> bucket with all half twiddles (I3, L1), written
+  // bit-reversed along the last dim; outer bucket index Bo(l) of this class per loop.
+  const int rstride = blast + 1;
+  const int lgbl = pd.lgb[D - 1];
+  for (int i = tid; i < nl * blast; i += blockDim.x) {
+    int l = i >> lgbl, r = i & (blast - 1);
+    float2 s = make_float2(0.f, 0.f);
+    for (int w = 0; w < nwarps; ++w) s = cadd(s, part[((size_t)w * nl + l) * blast + r]);
+    const LoopDev& lp = pd.loops[l0 + l];
+    const int dl = D - 1;
+    int bl = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
+    if (pd.shift[dl]) s = cmul(s, tw[bl << (6 - lgbl)]);
+    int b0 = (lp.sinv[0] * (r0 - lp.tau[0])) & (pd.b[0] - 1);
+    if (pd.shift[0]) s = cmul(s, tw[b0 << (6 - pd.lgb[0])]);
+    int bo = b0;
+    if (D == 3) {
+      int b1 = (lp.sinv[1] * (r1 - lp.tau[1])) & (pd.b[1] - 1);
+      if (pd.shift[1]) s = cmul(s, tw[b1 << (6 - pd.lgb[1])]);
+      bo = b0 * pd.b[1] + b1;
+    }
+    if (r == 0) sbo[l] = bo;
+    R[(size_t)l * rstride + brev(bl, lgbl)] = s;
+  }
+  __syncthreads();
+  {
+    View vw;
+    vw.k = 2;
+    vw.n[0] = nl; vw.lg[0] = 0; vw.st[0] = rstride;
+    vw.n[1] = blast; vw.lg[1] = lgbl; vw.st[1] = 1;
+    fft_axis(R, vw, 1, tw);
+  }
+  for (int i = tid; i < nl * blast; i += blockDim.x) {
+    int l = i >> lgbl, k = i & (blast - 1);
+    pd.fbuf[(((size_t)frame * nl + l) * pd.bouter + sbo[l]) * blast + k] = R[(size_t)l * rstride + k];
+  }
+}
+
+// Split mode, kernel 2: one CTA per (loop, k_last, frame): FFT over the outer dims, power,
+// NP threshold, bitmap bits (atomicOr), optional spectra.
+__global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, int l0, int nl,
+                                                        uint32_t* __restrict__ bitmaps,
+                                                        float2* __restrict__ spectra) {
+  extern __shared__ float4 smem_f4[];
+  float2* tw = reinterpret_cast<float2*>(smem_f4);
+  float2* V = tw + 128;
+  const int D = pd.D;
+  const int blast = pd.blast;
+  const int l = blockIdx.x / blast, kl = blockIdx.x - l * blast;
+  const int64_t frame = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int b0 = pd.b[0], b1 = D == 3 ? pd.b[1] : 1;
+  const int vstride = b1 + 1;                        // padded rows [B0][B1+1]
+  const float2* src = pd.fbuf + (((size_t)frame * nl + l) * pd.bouter) * blast + kl;
+  const int lgb0 = pd.lgb[0], lgb1 = D == 3 ? pd.lgb[1] : 0;
+  load_twiddles(tw);
+  for (int o = tid; o < pd.bouter; o += blockDim.x) {
+    int o0 = o >> lgb1, o1 = o & (b1 - 1);
+    V[brev(o0, lgb0) * vstride + brev(o1, lgb1)] = src[(size_t)o * blast];
+  }
+  __syncthreads();
+  {
+    View vw;
+    vw.k = 3;
+    vw.n[0] = 1; vw.lg[0] = 0; vw.st[0] = 0;
+    vw.n[1] = b0; vw.lg[1] = lgb0; vw.st[1] = vstride;
+    vw.n[2] = b1; vw.lg[2] = lgb1; vw.st[2] = 1;
+    if (D == 3) fft_axis(V, vw, 2, tw);
+    fft_axis(V, vw, 1, tw);
+  }
+  const float gamma = pd.loops[l0 + l].gamma;
+  uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
+  for (int o = tid; o < pd.bouter; o += blockDim.x) {
+    int o0 = o / b1, o1 = o - o0 * b1;
+    float2 v = V[o0 * vstride + o1];
+    int64_t k = (int64_t)o * blast + kl;
+    if (v.x * v.x + v.y * v.y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
+    if (spectra) spectra[((size_t)frame * nl + l) * pd.btot + k] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 vote: one CTA per (prefix, frame).  Word-parallel reverse map (I1): for the row dim
+// rd = D-2 and last dim ld = D-1, E[l][k_rd][w] is the 32-location mask of row-bucket k_rd
+// expanded over last-dim locations 32w..32w+31; each (row, word) then ORs nothing — it adds
+// one mask per loop into bit-sliced counters and compares with mu.
+// smem: bm [L][wpl] | E [L][B_rd][W_last]
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
+                                                   int64_t d0b, int64_t d0e,
+                                                   uint32_t* __restrict__ detect, uint8_t* __restrict__ counts) {
+  extern __shared__ float4 smem_f4[];
+  const int D = pd.D, L = pd.L, wpl = pd.wpl;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_f4);
+  const int ld = D - 1;
+  const int nld = pd.n[ld];
+  const int wlast = nld >> 5;
+  const int brd = D >= 2 ? pd.b[D - 2] : 1;
+  uint32_t* E = bm + (size_t)L * wpl;
+  const int64_t frame = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t i0 = d0b + blockIdx.x;              // prefix (D == 3)
+
+  const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
+  for (int i = tid; i < L * wpl; i += blockDim.x) bm[i] = src[i];
+  __syncthreads();
+  // E[l][krd][w]
+  const int nE = L * brd * wlast;
+  for (int it = warp; it < nE; it += nwarps) {
+    int l = it / (brd * wlast), rem = it - l * brd * wlast;
+    int krd = rem / wlast, w = rem - krd * wlast;
+    const LoopDev& lp = pd.loops[l];
+    int kpre = 0;
+    if (D == 3) kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+    int ilast = (w << 5) + lane;
+    int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> pd.lga[ld];
+    int64_t flat = ((int64_t)kpre * brd + krd) * pd.blast + klast;
+    uint32_t bit = (bm[(size_t)l * wpl + (flat >> 5)] >> (flat & 31)) & 1u;
+    uint32_t word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) E[it] = word;
+  }
+  __syncthreads();
+  // rows of this CTA
+  int64_t rbeg, rend;
+  int64_t out_base;                                  // word offset of this CTA's first row
+  const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
+  const int64_t slab_words = slab_locs >> 5;
+  if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * wlast; }
+  else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
+  else { rbeg = 0; rend = 1; out_base = 0; }
+  const int nrd = D >= 2 ? pd.n[D - 2] : 1;
+  const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
+  const int64_t nitems = (rend - rbeg) * wlast;
+  const int mu = pd.mu;
+  for (int64_t it = tid; it < nitems; it += blockDim.x) {
+    int64_t ri = it / wlast;
+    int w = (int)(it - ri * wlast);
+    int64_t row = rbeg + ri;
+    uint32_t pl[6] = {0, 0, 0, 0, 0, 0};
+    for (int l = 0; l < L; ++l) {
+      int krd = 0;
+      if (D >= 2) krd = (int)(((int64_t)pd.loops[l].sig[D - 2] * row) & (nrd - 1)) >> lga_rd;
+      uint32_t carry = E[((size_t)l * brd + krd) * wlast + w];
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        uint32_t t = pl[b] & carry;
+        pl[b] ^= carry;
+        carry = t;
+      }
+    }
+    // bit-sliced compare: count >= mu
+    uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+    for (int b = 5; b >= 0; --b) {
+      if ((mu >> b) & 1) eq &= pl[b];
+      else { gt |= eq & pl[b]; eq &= ~pl[b]; }
+    }
+    const int64_t widx = out_base + ri * wlast + w;
+    detect[frame * slab_words + widx] = gt | eq;
+    if (counts) {
+      uint8_t* cdst = counts + frame * slab_locs + widx * 32;
+      for (int j = 0; j < 32; ++j) {
+        int c = 0;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) c |= ((pl[b] >> j) & 1u) << b;
+        cdst[j] = (uint8_t)c;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K4 compaction: detection bitmap -> ascending flat indices.
+// ------------------------------------------------------------------------------------
+constexpr int kWordsPerThread = (int)(kChunkWords / kThreads);
+
+__global__ void __launch_bounds__(kThreads) k_count(const uint32_t* __restrict__ det, int64_t nwords,
+                                                    long long* __restrict__ chunk_counts) {
+  __shared__ int red[kThreads / 32];
+  const int64_t base = (int64_t)blockIdx.x * kChunkWords + (int64_t)threadIdx.x * kWordsPerThread;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kWordsPerThread; ++i) if (base + i < nwords) c += __popc(det[base + i]);
+  for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int i = 0; i < kThreads / 32; ++i) s += red[i];
+    chunk_counts[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan(long long* __restrict__ chunk_counts, int64_t nchunks,
+                                               long long* __restrict__ d_count) {
+  __shared__ long long part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nchunks + 1023) / 1024;
+  const int64_t b = t * per, e = b + per < nchunks ? b + per : nchunks;
+  long long s = 0;
+  for (int64_t i = b; i < e; ++i) s += chunk_counts[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    long long run = 0;
+    for (int i = 0; i < 1024; ++i) { long long v = part[i]; part[i] = run; run += v; }
+    *d_count = run;
+  }
+  __syncthreads();
+  long long run = part[t];
+  for (int64_t i = b; i < e; ++i) { long long v = chunk_counts[i]; chunk_counts[i] = run; run += v; }
+}
+
+__global__ void __launch_bounds__(kThreads) k_write(const uint32_t* __restrict__ det, int64_t nwords,
+                                                    const long long* __restrict__ chunk_off,
+                                                    long long* __restrict__ idx, int64_t capacity) {
+  __shared__ int wsum[kThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kChunkWords + (int64_t)tid * kWordsPerThread;
+  uint32_t w[kWordsPerThread];
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kWordsPerThread; ++i) {
+    w[i] = base + i < nwords ? det[base + i] : 0u;
+    c += __popc(w[i]);
+  }
+  int incl = c;
+  for (int off = 1; off < 32; off <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int i = 0; i < warp; ++i) wbase += wsum[i];
+  long long pos = chunk_off[blockIdx.x] + wbase + incl - c;
+#pragma unroll
+  for (int i = 0; i < kWordsPerThread; ++i) {
+    uint32_t v = w[i];
+    while (v) {
+      int bit = __ffs(v) - 1;
+      v &= v - 1;
+      if (pos < capacity) idx[pos] = (long long)(base + i) * 32 + bit;
+      ++pos;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Host launchers
+// ------------------------------------------------------------------------------------
+static rsft_status check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RSFT_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return RSFT_E_CUDA;
+}
+
+template <int LP>
+static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
+                                  uint32_t* bm, void* spectra, cudaStream_t st) {
+  constexpr int U = LP <= 8 ? 8 : 4;
+  auto kern = k_fused<LP, U>;
+  const int D = p->D;
+  const int64_t blast = p->b[D - 1], nlast = p->n[D - 1], bouter = p->btot / blast;
+  const int64_t nseg = nlast / 64;
+  const int64_t G = D == 1 ? (nseg < 8 ? nseg : 8) : 1;
+  size_t smem = (size_t)(G + 1) * nl * bouter * (blast + 1) * 8 + 128 * 8 + (D == 2 ? (size_t)p->n[0] * LP * 4 : 0);
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem), "occupancy");
+  if (s) return s;
+  if (nb < 1) nb = 1;
+  int64_t grid = (int64_t)nb * p->num_sms;
+  if (grid > batch) grid = batch;
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, reinterpret_cast<const float4*>(d_x), batch, l0, nl,
+                                               bm, reinterpret_cast<float2*>(spectra));
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_fused launch");
+}
+
+template <int LP>
+static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
+                                  uint32_t* bm, void* spectra, cudaStream_t st) {
+  constexpr int U = LP <= 8 ? 8 : 4;
+  auto kern = k_split_fold<LP, U>;
+  const int D = p->D;
+  const int64_t blast = p->b[D - 1];
+  const int64_t RA = p->dev.aouter;
+  const int nwarps = kThreads / 32;
+  size_t smem = 128 * 8 + kMaxLoops * 4 + (size_t)RA * LP * 4 + (size_t)nwarps * nl * blast * 8 +
+                (size_t)nl * (blast + 1) * 8;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  dim3 grid((unsigned)p->dev.bouter, (unsigned)batch);
+  kern<<<grid, kThreads, smem, st>>>(p->dev, reinterpret_cast<const float4*>(d_x), l0, nl, bm);
+  p->last_launches += 1;
+  s = check(cudaGetLastError(), "k_split_fold launch");
+  if (s) return s;
+  const int64_t b1 = D == 3 ? p->b[1] : 1;
+  size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
+  s = check(cudaFuncSetAttribute(k_split_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), "smem attr");
+  if (s) return s;
+  dim3 grid2((unsigned)(nl * blast), (unsigned)batch);
+  k_split_fft<<<grid2, kThreads, smem2, st>>>(p->dev, l0, nl, bm, reinterpret_cast<float2*>(spectra));
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_split_fft launch");
+}
+
+#define RSFT_DISPATCH_LP(FN, LPV, ...)                   \
+  switch (LPV) {                                         \
+    case 2: return FN<2>(__VA_ARGS__);                   \
+    case 4: return FN<4>(__VA_ARGS__);                   \
+    case 6: return FN<6>(__VA_ARGS__);                   \
+    case 8: return FN<8>(__VA_ARGS__);                   \
+    case 12: return FN<12>(__VA_ARGS__);                 \
+    case 16: return FN<16>(__VA_ARGS__);                 \
+    case 24: return FN<24>(__VA_ARGS__);                 \
+    case 32: return FN<32>(__VA_ARGS__);                 \
+    default: return RSFT_E_UNSUPPORTED;                  \
+  }
+
+rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                           void* spectra, cudaStream_t st) {
+  int mode = resolve_mode(p, batch);
+  int lp = loop_pad(nl);
+  if (mode == RSFT_MODE_FUSED) { RSFT_DISPATCH_LP(launch_fused_t, lp, p, d_x, batch, l0, nl, bm, spectra, st); }
+  if (mode == RSFT_MODE_SPLIT) { RSFT_DISPATCH_LP(launch_split_t, lp, p, d_x, batch, l0, nl, bm, spectra, st); }
+  return RSFT_E_UNSUPPORTED;
+}
+
+rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                          uint32_t* det, uint8_t* counts, cudaStream_t st) {
+  const int D = p->D;
+  const int64_t nld = p->n[D - 1];
+  const int64_t brd = D >= 2 ? p->b[D - 2] : 1;
+  size_t smem = (size_t)p->L * p->dev.wpl * 4 + (size_t)p->L * brd * (nld / 32) * 4;
+  rsft_status s = check(cudaFuncSetAttribute(k_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  dim3 grid(D == 3 ? (unsigned)(d0e - d0b) : 1u, (unsigned)batch);
+  k_vote<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, det, counts);
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_vote launch");
+}
+
+rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
+                           int64_t capacity, int64_t* d_count, cudaStream_t st) {
+  const int64_t nwords = batch * ((p->ntot + 31) / 32);
+  const int64_t nchunks = (nwords + kChunkWords - 1) / kChunkWords;
+  if (nchunks > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;
+  k_count<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, p->dev.chunk_counts);
+  k_scan<<<1, 1024, 0, st>>>(p->dev.chunk_counts, nchunks, reinterpret_cast<long long*>(d_count));
+  k_write<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, p->dev.chunk_counts,
+                                                  reinterpret_cast<long long*>(idx), capacity);
+  p->last_launches += 3;
+  return check(cudaGetLastError(), "compaction launch");
+}
+
+rsft_status upload_twiddles(cudaStream_t st) {
+  float2 tw[128];
+  for (int k = 0; k < 128; ++k) {
+    double a = -2.0 * M_PI * (double)k / 128.0;
+    tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  return check(cudaMemcpyToSymbolAsync(c_tw128, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st), "twiddles");
+}
+
+}  // namespace rsft

@@ -1,0 +1,86 @@
+// Internal definitions shared by the host plan (plan.cpp) and the CUDA side (kernels.cu).
+// Product code only: nothing here is shared with the oracle (oracle/ is NumPy).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "../../include/rsft.h"
+
+namespace rsft {
+
+constexpr int kMaxDim = 3;
+constexpr int kMaxLoops = 32;
+constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
+constexpr int64_t kChunkWords = 2048;  // compaction chunk: words of the detection bitmap
+constexpr int kThreads = 256;          // CTA size of every kernel
+
+// Per-loop device record: schedule + threshold (Def. 1; Eq. tpd).
+struct LoopDev {
+  int32_t sig[kMaxDim];
+  int32_t sinv[kMaxDim];
+  int32_t tau[kMaxDim];
+  float gamma;
+  int32_t pad;
+};
+
+// Plan view passed by value to every kernel.
+struct PlanDev {
+  int32_t D;
+  int32_t L;                       // loops in the plan
+  int32_t mu;
+  int32_t nplanes;                 // bit planes of the vote counter (L < 2^nplanes)
+  int32_t n[kMaxDim], b[kMaxDim], a[kMaxDim];
+  int32_t lgn[kMaxDim], lgb[kMaxDim], lga[kMaxDim];
+  int32_t shift[kMaxDim];          // 1 if B_d < N_d (half-bucket twiddle, L1), else 0
+  int64_t ntot, btot;
+  int32_t wpl;                     // bitmap words per loop = ceil(btot/32)
+  int32_t nlast, blast;            // N_{D-1}, B_{D-1}
+  int64_t rows;                    // ntot / nlast
+  int32_t bouter;                  // prod_{d<D-1} B_d
+  int32_t aouter;                  // prod_{d<D-1} A_d (rows per outer residue class)
+  const LoopDev* loops;            // [L]
+  const float* h[kMaxDim];         // [L][N_d] fp32 weight tables h_{l,d}[s] (I3)
+  float2* fbuf;                    // split mode intermediate [batch][L][B_tot]
+  long long* chunk_counts;         // compaction scratch
+  int64_t chunk_capacity;
+};
+
+struct Workspace {
+  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, total;
+  int64_t chunk_capacity;
+};
+
+}  // namespace rsft
+
+struct rsft_plan_s {
+  rsft_params P;
+  int D = 1, L = 1, mu = 1;
+  int64_t n[3] = {1, 1, 1}, b[3] = {1, 1, 1}, a[3] = {1, 1, 1}, W[3] = {0, 0, 0};
+  int64_t ntot = 1, btot = 1;
+  std::vector<int64_t> sigma, sinv, tau;          // [L*D]
+  std::vector<double> prewin[3], flatg[3];        // fp64 windows [N_d]
+  std::vector<double> hd[3];                      // fp64 weights [L][N_d]
+  std::vector<float> hf[3];                       // fp32 weights [L][N_d]
+  std::vector<double> beta, gamma;                // [L]
+  rsft::Workspace ws{};
+  // binding
+  bool bound = false;
+  int device = -1;
+  int num_sms = 148;
+  void* d_ws = nullptr;
+  rsft::PlanDev dev{};
+  int32_t last_launches = 0;
+};
+
+namespace rsft {
+// plan.cpp
+rsft_status rebuild_tables(rsft_plan_s* p);
+void layout_workspace(rsft_plan_s* p);
+int resolve_mode(const rsft_plan_s* p, int64_t batch);
+int loop_pad(int nl);
+void set_error(const std::string& s);
+}  // namespace rsft

@@ -1,0 +1,191 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs
+and the same seeded (sigma, tau).  Buckets within 1e-4 relative (noise-std floor), first-stage
+bits exact outside the 1e-3 near-threshold band, detection sets inside the ambiguity envelope,
+vote counts inside [abar_min, abar_max], index lists exact (BASELINE north_star)."""
+import zlib
+
+import numpy as np
+import pytest
+
+from oracle import rsft_ref as R
+import synth
+from gpu_helpers import check_frame, check_index_list, gpu_run, make_plan, oracle_params
+
+pytestmark = pytest.mark.gpu
+
+
+def frames(wl, batch, start=0):
+    return synth.gen_batch(wl, range(start, start + batch))
+
+
+def run_case(op, x, mode="auto", check=None, loops=None):
+    import torch
+    torch.cuda.init()
+    plan = make_plan(op, max_batch=x.shape[0], mode=mode).bind()
+    sig, _, tau = plan.schedule()
+    tb = R.make_tables(op)
+    np.testing.assert_array_equal(sig, tb.sigma)
+    np.testing.assert_array_equal(tau, tb.tau)
+    res = gpu_run(plan, x)
+    check_index_list(res, plan.ntot, x.shape[0])
+    reps = []
+    for f in (range(x.shape[0]) if check is None else check):
+        reps.append(check_frame(res, f, x[f], op, tb))
+    return plan, res, reps
+
+
+# ----------------------------------------------------------------------------- CI sizes
+CASES = [
+    # name, n, b, loops, extra oracle params, batch, mode
+    ("1d_w256_tau", (1024,), (32,), 5, dict(support=(256,), random_tau=True, p_fa=1e-3), 3, "fused"),
+    ("1d_b64_full", (2048,), (64,), 3, dict(p_fa=1e-3), 2, "fused"),
+    ("2d_fused", (128, 128), (16, 8), 6, dict(p_fa=1e-4, random_tau=True), 5, "fused"),
+    ("2d_fused_mu", (128, 64), (8, 16), 7, dict(p_fa=1e-3, mu=4), 4, "fused"),
+    ("2d_split_rpw1", (128, 64), (16, 16), 6, dict(p_fa=1e-4), 2, "split"),
+    ("2d_split_rpw2", (256, 32), (16, 8), 4, dict(p_fa=1e-4, random_tau=True), 2, "split"),
+    ("3d_split", (64, 32, 32), (8, 4, 8), 8, dict(p_fa=1e-5, random_tau=True), 2, "split"),
+    ("3d_split_L12", (32, 16, 64), (4, 4, 8), 12, dict(p_fa=1e-4, mu=9), 1, "split"),
+    ("3d_L1", (16, 16, 64), (4, 8, 16), 1, dict(p_fa=1e-3), 1, "split"),
+    ("2d_B_eq_N_dim0", (64, 128), (64, 8), 3, dict(p_fa=1e-3), 3, "fused"),
+    ("2d_B1_dim0", (64, 128), (1, 16), 3, dict(p_fa=1e-3), 2, "fused"),
+    ("2d_Blast1", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "fused"),
+    ("2d_Blast1_split", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "split"),
+    ("2d_rect_cheb40", (128, 128), (16, 16), 4, dict(prewin="cheb", prewin_param=40.0, p_fa=1e-4), 2, "fused"),
+    ("3d_B_eq_N_last", (16, 32, 32), (4, 8, 32), 3, dict(p_fa=1e-3), 1, "split"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_parity_ci_sizes(case):
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    plan, res, reps = run_case(op, x, mode=mode)
+    assert plan.mode == (1 if mode == "fused" else 2)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+def test_parity_persistent_many_frames():
+    """More frames than resident CTAs: each persistent CTA loops over several frames."""
+    op = oracle_params((64, 64), (8, 8), 3, p_fa=1e-3, seed=5)
+    wl = synth.Workload("many", (64, 64), (8, 8), 3, 1e-3, 1.0, (2, 6), (0.0, 20.0), 700, data_seed=9)
+    x = frames(wl, 700)
+    run_case(op, x, mode="fused", check=[0, 1, 2, 296, 297, 350, 591, 699])
+
+
+def test_zero_and_noise_only_frames():
+    op = oracle_params((128, 64), (16, 8), 4, p_fa=1e-2, seed=2)
+    x = np.zeros((3, 128, 64), dtype=np.complex64)
+    x[1] = synth.gen_noise_only((128, 64), 1.0, 4)
+    plan, res, _ = run_case(op, x, mode="fused")
+    assert not res["bm"][0].any() and not res["det"][0].any()
+
+
+def test_gamma_override_noiseless_ongrid_truth():
+    """Noiseless on-grid tones, tiny gamma: every tone cell detected (Prop. 3), GPU == oracle."""
+    n, b = (128, 64), (16, 8)
+    op = oracle_params(n, b, 4, gamma_override=1e-3, seed=5)
+    rng = np.random.default_rng(4)
+    bins = np.stack([rng.integers(0, n[0], 5), rng.integers(0, n[1], 5)], axis=1)
+    x = synth.gen_ongrid(n, bins, np.exp(2j * np.pi * rng.random(5))).astype(np.complex64)[None]
+    plan, res, _ = run_case(op, x, mode="fused")
+    from paper_1610_01050_b200 import rsft as B
+    det = B.bitmap_to_bool(res["det"][0], 128 * 64).reshape(n)
+    for i0, i1 in bins:
+        assert det[i0, i1]
+
+
+def test_loop_range_and_slabs():
+    """Loop-sharded execute (loops [lb, le)) equals the matching slice of the full run, and
+    sharded voting over dim-0 slabs equals the matching slice of the full detection."""
+    import torch
+    for n, b, L in [((64, 32, 32), (8, 4, 8), 6), ((128, 64), (16, 8), 6)]:
+        op = oracle_params(n, b, L, p_fa=1e-3, seed=11)
+        wl = synth.Workload("lr", n, b, L, 1e-3, 1.0, (4, 8), (0.0, 20.0), 2, data_seed=3)
+        x = frames(wl, 2)
+        plan = make_plan(op, max_batch=2).bind()
+        xt = torch.from_numpy(x).cuda()
+        full = plan.execute(xt)
+        parts = [plan.execute(xt, loop_begin=a, loop_end=e) for a, e in [(0, 2), (2, 5), (5, 6)]]
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(torch.cat(parts, dim=1).cpu().numpy(), full.cpu().numpy())
+        det = plan.detect(full).cpu().numpy()
+        per_row = plan.ntot // n[0] // 32
+        for a, e in [(0, 8), (8, 40), (40, n[0])]:
+            d = plan.detect(full, dim0=(a, e)).cpu().numpy()
+            np.testing.assert_array_equal(d, det[:, a * per_row:e * per_row])
+
+
+def test_run_host_end_to_end():
+    import torch
+    op = oracle_params((128, 64), (16, 8), 4, p_fa=1e-3, seed=6)
+    wl = synth.Workload("rh", (128, 64), (16, 8), 4, 1e-3, 1.0, (4, 8), (0.0, 20.0), 3, data_seed=5)
+    x = frames(wl, 3)
+    plan = make_plan(op, max_batch=3).bind()
+    cap = 1 << 16
+    scratch = torch.empty(plan.host_scratch_bytes(3, cap), dtype=torch.uint8, device="cuda")
+    hx = torch.from_numpy(x).pin_memory()
+    idx, count = plan.run_host(hx, cap, scratch)
+    res = gpu_run(plan, x)
+    np.testing.assert_array_equal(idx, res["idx"])
+    assert count == res["count"]
+    tb = R.make_tables(op)
+    for f in range(3):
+        check_frame(res, f, x[f], op, tb)
+
+
+def test_compaction_capacity_overflow():
+    import torch
+    op = oracle_params((64, 64), (8, 8), 2, p_fa=0.3, mu=1, seed=1)
+    wl = synth.Workload("cap", (64, 64), (8, 8), 2, 0.3, 1.0, (4, 8), (0.0, 20.0), 2, data_seed=2)
+    x = frames(wl, 2)
+    plan = make_plan(op, max_batch=2).bind()
+    res = gpu_run(plan, x, capacity=10)
+    assert res["count"] > 10 and res["idx"].size == 10
+    full = gpu_run(plan, x)
+    np.testing.assert_array_equal(res["idx"], full["idx"][:10])
+
+
+def test_determinism_bitwise():
+    import torch
+    op = oracle_params((64, 32, 32), (8, 4, 8), 4, p_fa=1e-3, seed=3)
+    wl = synth.Workload("det", (64, 32, 32), (8, 4, 8), 4, 1e-3, 1.0, (4, 8), (0.0, 20.0), 1, data_seed=8)
+    x = frames(wl, 1)
+    plan = make_plan(op).bind()
+    a = gpu_run(plan, x)
+    b = gpu_run(plan, x)
+    np.testing.assert_array_equal(a["spectra"].view(np.uint64), b["spectra"].view(np.uint64))
+
+
+# ----------------------------------------------------------------------------- full sizes
+def wl_params(wl):
+    return oracle_params(wl.n, wl.b, wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
+                         seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu)
+
+
+@pytest.mark.parametrize("name", ["c1_1d", "c2_2d", "c3_3d"])
+def test_parity_full_size_single_frame(name):
+    wl = synth.WORKLOADS[name]
+    x = frames(wl, 1)
+    _, _, reps = run_case(wl_params(wl), x)
+    assert reps[0]["max_ratio"] < 1e-4
+
+
+def test_parity_c4_full_batch_sampled():
+    """c4 at full size in the bench launch configuration (4096 frames, fused persistent
+    kernel); sampled frames checked against the oracle one by one.  The batch tiles 64
+    distinct seeded frames (bench.py uses the same recipe with a larger pool)."""
+    wl = synth.C4
+    pool = frames(wl, 64)
+    x = np.concatenate([pool] * (wl.batch // 64), axis=0)
+    _, res, reps = run_case(wl_params(wl), x, check=[0, 1, 63, 2047, 4095])
+    assert reps[0]["max_ratio"] < 1e-4
+
+
+def test_parity_c5_full_cube():
+    """c5 (512 MiB cube, L=16, split mode): every loop's buckets and bits, and the detection
+    set, against the oracle (slow: the oracle runs Alg. 1 literally on 2^26 samples)."""
+    wl = synth.C5
+    x = frames(wl, 1)
+    run_case(wl_params(wl), x)

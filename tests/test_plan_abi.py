@@ -1,0 +1,139 @@
+"""CPU tests of the C ABI (no GPU): the library loads, exports every symbol include/rsft.h
+declares, validates arguments, and its host plan (C++ fp64) agrees with the oracle's
+independently written NumPy tables (windows, schedule, beta, gamma, weights)."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import rsft_ref as R
+import synth
+
+P = pytest.importorskip("paper_1610_01050_b200")
+from paper_1610_01050_b200 import rsft as B  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "rsft.h")) as f:
+        txt = f.read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(rsft_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = B.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(B.EXPORTED) == syms
+
+
+def oracle_params(wl, **kw):
+    d = dict(n=wl.n, b=wl.b, loops=wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
+             seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu)
+    d.update(kw)
+    return R.Params(**d)
+
+
+def plan_for(wl, **kw):
+    d = dict(support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var, seed=wl.sched_seed,
+             random_tau=wl.random_tau, mu=wl.mu, max_batch=wl.batch)
+    d.update(kw)
+    return B.Plan(wl.n, wl.b, wl.loops, **d)
+
+
+@pytest.mark.parametrize("wl", list(synth.WORKLOADS.values()), ids=list(synth.WORKLOADS))
+def test_plan_tables_match_oracle(wl):
+    """T2: C++ plan vs NumPy oracle, both fp64, to 1e-12 (windows, beta, gamma) and exact
+    (schedule); fp32 weight tables equal the oracle-derived h_{l,d}[s] after fp32 rounding."""
+    if wl.name == "c5_cube":
+        wl = wl.with_(loops=4)
+    p = plan_for(wl)
+    op = oracle_params(wl)
+    tb = R.make_tables(op)
+    sig, sinv, tau = p.schedule()
+    np.testing.assert_array_equal(sig, tb.sigma)
+    np.testing.assert_array_equal(sinv, tb.sigma_inv)
+    np.testing.assert_array_equal(tau, tb.tau)
+    for d in range(len(wl.n)):
+        np.testing.assert_allclose(p.window(d, 0), tb.prewin[d], rtol=0, atol=1e-10)
+        g = R.flat_prototype(wl.n[d], wl.b[d], op.support[d], op.flat_atten_db)
+        np.testing.assert_allclose(p.window(d, 1), g, rtol=0, atol=1e-10)
+        # I3 weights from the oracle's pieces: h[s] = w[s] g[t] (-1)^floor(t/B), t = sinv (s - tau)
+        h = p.window(d, 2)
+        n, b = wl.n[d], wl.b[d]
+        s = np.arange(n)
+        for l in range(wl.loops):
+            t = (int(tb.sigma_inv[l, d]) * (s - int(tb.tau[l, d]))) % n
+            sign = np.where((t // b) % 2 == 1, -1.0, 1.0) if b < n else np.ones(n)
+            want = (tb.prewin[d] * g[t] * sign).astype(np.float32).astype(np.float64)
+            np.testing.assert_allclose(h[l], want, rtol=2e-7, atol=1e-12)
+    be, ga = p.thresholds()
+    for l in range(wl.loops):
+        assert math.isclose(be[l], R.beta(op, tb, l), rel_tol=1e-12)
+        assert math.isclose(ga[l], R.gamma(op, tb, l), rel_tol=1e-12)
+
+
+def test_cheb_prewindow_and_gamma_override():
+    p = B.Plan((256, 64), (16, 8), 3, prewin="cheb", prewin_param=40.0, gamma_override=7.5, seed=3)
+    op = R.Params(n=(256, 64), b=(16, 8), loops=3, prewin="cheb", prewin_param=40.0, gamma_override=7.5, seed=3)
+    tb = R.make_tables(op)
+    for d in range(2):
+        np.testing.assert_allclose(p.window(d, 0), tb.prewin[d], rtol=0, atol=1e-10)
+    assert np.all(p.thresholds()[1] == 7.5)
+
+
+def test_set_schedule_roundtrip_and_errors():
+    p = B.Plan((64, 32), (8, 4), 2, seed=1)
+    p.set_schedule([[3, 5], [7, 9]], [[1, 2], [3, 4]])
+    s, si, t = p.schedule()
+    assert s.tolist() == [[3, 5], [7, 9]] and t.tolist() == [[1, 2], [3, 4]]
+    assert ((s * si) % np.array([64, 32]) == 1).all()
+    with pytest.raises(B.RsftError) as e:
+        p.set_schedule([[4, 5], [7, 9]])
+    assert e.value.status == 3                                        # RSFT_E_SIGMA
+    op = R.Params(n=(64, 32), b=(8, 4), loops=2)
+    tb = R.make_tables(op, schedule_override=([[3, 5], [7, 9]], [[1, 2], [3, 4]]))
+    be, _ = p.thresholds()
+    assert math.isclose(be[1], R.beta(op, tb, 1), rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(n=(100,), b=(4,), loops=1), 2),                   # N not a power of two
+    (dict(n=(64,), b=(128,), loops=1), 2),                  # B > N
+    (dict(n=(1024,), b=(128,), loops=1), 4),                # B > 64 unsupported
+    (dict(n=(64,), b=(8,), loops=1, support=(24,)), 2),     # 2B does not divide W
+    (dict(n=(64,), b=(8,), loops=0), 1),
+    (dict(n=(64,), b=(8,), loops=40), 4),                   # L > 32
+    (dict(n=(64,), b=(8,), loops=4, mu=5), 1),              # mu > L
+    (dict(n=(64,), b=(8,), loops=4, p_fa=1.5), 1),
+    (dict(n=(16,), b=(8,), loops=1), 4),                    # N_last < 32
+    (dict(n=(8, 8, 8, 8), b=(2, 2, 2, 2), loops=1), 4),     # D > 3
+])
+def test_plan_argument_errors(kw, status):
+    n = kw.pop("n")
+    b = kw.pop("b")
+    loops = kw.pop("loops")
+    with pytest.raises(B.RsftError) as e:
+        B.Plan(n, b, loops, **kw)
+    assert e.value.status == status
+
+
+def test_device_calls_require_bind():
+    p = B.Plan((64, 64), (8, 8), 2)
+    with pytest.raises(B.RsftError) as e:
+        p._need_bind()
+    assert e.value.status == 7
+
+
+def test_mode_resolution():
+    assert B.Plan((1024, 256), (32, 16), 6, max_batch=4096).mode == 1          # fused
+    assert B.Plan((2048, 512, 64), (64, 32, 8), 16).mode == 2                  # split
+    assert B.Plan((4096,), (64,), 8, support=(512,)).mode == 1
+    assert B.Plan((256, 256), (16, 16), 6, max_batch=1).mode == 2
+    assert B.Plan((512, 128, 32), (32, 16, 8), 8).mode == 2
