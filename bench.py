@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""RSFT hot-path benchmark (BASELINE.json metric: RSFT frames/s and fused-bucketize HBM GB/s
+as a fraction of the B200 peak, at 1/2/4/8 GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4_batched_2d|c5_cube]
+                    [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...         (one rank per GPU, NCCL)
+
+A step is one pass of the whole hot path (execute = fused fold+FFT+threshold, detect = vote,
+compact = sorted index list) over one batch of synthetic frames resident in HBM.  Default
+workload: c4 (BASELINE configs[3]: 1024x256 complex64 frames, B=32x16, L=6, P_fa=1e-6),
+4096 frames per GPU (weak scaling: frames shard across GPUs, no collective in the data path).
+`--workload c5_cube` runs the single 512 MiB cube with its L=16 loops sharded across ranks
+and an NCCL all-gather of the per-loop bitmaps before voting.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle (the only
+reference this paper has: it publishes no code) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "RSFT frames/sec and fused-bucketize HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML (nvidia-smi fallback) in a thread."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def host_frames(wl, rank, frames, pool):
+    """`frames` frames for this rank: a pool of `pool` distinct seeded frames tiled."""
+    base = synth.gen_batch(wl, range(rank * pool, rank * pool + pool))
+    reps = (frames + pool - 1) // pool
+    return np.concatenate([base] * reps, axis=0)[:frames]
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_worker(args):
+    """Run the oracle on the given frames; inputs are generated before the clock starts."""
+    wl_name, frame_ids = args
+    from oracle import rsft_ref as R
+    wl = synth.WORKLOADS[wl_name]
+    op = R.Params(n=wl.n, b=wl.b, loops=wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
+                  seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu)
+    tb = R.make_tables(op)
+    xs = [synth.gen_frame(wl, f) for f in frame_ids]
+    t = time.perf_counter()
+    for x in xs:
+        R.rsft_run(x, op, tb)
+    return time.perf_counter() - t
+
+
+def oracle_rate(wl, budget_s=12.0, max_cores=32):
+    """Oracle frames/s on the host cores: a process pool (1 BLAS/OpenMP thread each) over a
+    bounded sample of frames of the workload; rate = frames / slowest worker's oracle time.
+    Returns (frames/s, cores, sample description)."""
+    import multiprocessing as mp
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    cores = max(1, min(len(os.sched_getaffinity(0)), max_cores))
+    one = oracle_worker((wl.name, [0]))                 # calibrate on one core
+    if wl.name == "c5_cube":
+        cores = 1
+    per_core = max(1, int(budget_s / (2.0 * max(one, 1e-3))))
+    nframes = per_core * cores
+    chunks = [(wl.name, list(range(i, nframes, cores))) for i in range(cores)]
+    if cores == 1:
+        el = oracle_worker(chunks[0])
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(cores) as pool:
+            el = max(pool.map(oracle_worker, chunks))
+    return nframes / el, cores, (f"{nframes} frames of {wl.name}: oracle rsft_run (fp64, literal Alg. 1), "
+                                 f"{cores} processes x 1 thread, input generation untimed")
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = synth.WORKLOADS[a.workload]
+    rates = []
+    sample = None
+    cores = 1
+    steps = max(1, a.steps)
+    budget = max(2.0, min(20.0, 150.0 / steps))         # whole run within a few minutes
+    for _ in range(steps):
+        r, cores, sample = oracle_rate(wl, budget_s=budget)
+        rates.append(r)
+    value = float(statistics.median(rates))
+    frames_per_step = wl.batch
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": a.gpus,
+        "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * frames_per_step / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Eq. sig_model frames)",
+        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": wl.loops, "p_fa": wl.p_fa},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main_gpu(a):
+    import torch
+    import torch.distributed as dist
+    from paper_1610_01050_b200 import rsft as B
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = synth.WORKLOADS[a.workload]
+    stream = torch.cuda.current_stream()
+
+    if wl.name == "c5_cube":
+        return bench_c5(a, wl, rank, world, dev)
+
+    frames = a.frames or wl.batch
+    plan = B.Plan(wl.n, wl.b, wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
+                  seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu, max_batch=frames).bind()
+    hx = host_frames(wl, rank, frames, a.pool)
+    x = torch.from_numpy(hx).to(dev)
+    bm = plan.new_bitmaps(frames)
+    det = torch.empty((frames, plan.detect_words), dtype=torch.int32, device=dev)
+    cap = frames * 4096
+    idx = torch.empty(cap, dtype=torch.int64, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def step(events=None):
+        if events is not None:
+            events[0].record(stream)
+        plan.execute(x, bitmaps=bm)
+        n = plan.last_launch_count()
+        if events is not None:
+            events[1].record(stream)
+        plan.detect(bm, detect=det)
+        n += plan.last_launch_count()
+        plan.compact(det, cap, idx=idx, count=cnt)
+        n += plan.last_launch_count()
+        return n
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches = 0
+    t0.record(stream)
+    for k in range(a.steps):
+        launches += step(ev[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t0.elapsed_time(t1)
+    k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    el = torch.tensor([elapsed_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(el.item())
+    detections = int(cnt.item())
+
+    # e2e through the C ABI on HOST buffers (H2D copy + kernels + D2H of count and indices)
+    e2e = None
+    if not a.no_e2e:
+        hpin = torch.from_numpy(hx).pin_memory()
+        scratch = torch.empty(plan.host_scratch_bytes(frames, cap), dtype=torch.uint8, device=dev)
+        plan.run_host(hpin, cap, scratch)
+        e_steps = max(1, min(a.steps, 5))
+        if world > 1:
+            dist.barrier()
+        tt0, tt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        tt0.record(stream)
+        nidx = 0
+        for _ in range(e_steps):
+            _, c = plan.run_host(hpin, cap, scratch)
+            nidx = min(c, cap)
+        tt1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([tt0.elapsed_time(tt1) / e_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * frames / (float(e_ms.item()) / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": int(hpin.numel() * 8), "d2h_bytes_per_step": int(8 + 8 * nidx)}
+        del scratch, hpin
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (fused fold + FFT + threshold, one launch per step)
+    peak, peak_src = load_peaks()
+    k1_avg = statistics.mean(k1_ms)
+    algo_bytes = frames * (8 * plan.ntot + plan.loops * plan.bitmap_words * 4)
+    achieved = algo_bytes / (k1_avg / 1000.0) / 1e9
+    step_ms = elapsed_ms / a.steps
+    value = world * frames / (step_ms / 1000.0)
+    cpu = None
+    if not a.no_cpu:
+        r, cores, sample = oracle_rate(wl, budget_s=a.cpu_budget)
+        cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample}
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic: {a.pool} distinct seeded Eq. sig_model frames per GPU tiled to {frames}",
+        "config": {"workload": wl.name, "frames_per_gpu": frames, "n": list(wl.n), "b": list(wl.b),
+                   "loops": wl.loops, "p_fa": wl.p_fa, "mu": plan.loops if not wl.mu else wl.mu,
+                   "mode": {1: "fused", 2: "split"}.get(plan.mode, plan.mode),
+                   "l2": f"inputs {frames * plan.ntot * 8 / 2**30:.1f} GiB per GPU >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"frames sharded over {world} GPU(s), no data-path collective"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": load_traffic(wl.name),
+                     "kernel": "k_fused (fold+FFT+threshold)", "algorithmic_bytes_per_launch": algo_bytes,
+                     "avg_launch_ms": k1_avg, "share_of_step": k1_avg / step_ms, "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "detections_per_step": detections,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_c5(a, wl, rank, world, dev):
+    """Single 512 MiB cube, L=16 loops sharded over ranks, NCCL all-gather of the per-loop
+    bitmaps (2 KiB/loop), then voting on this rank's dim-0 slab (BASELINE configs[4])."""
+    import torch
+    import torch.distributed as dist
+    from paper_1610_01050_b200 import rsft as B
+
+    stream = torch.cuda.current_stream()
+    plan = B.Plan(wl.n, wl.b, wl.loops, p_fa=wl.p_fa, noise_var=wl.noise_var, seed=wl.sched_seed,
+                  mu=wl.mu, max_batch=1).bind()
+    L = wl.loops
+    assert L % world == 0, "loops must divide evenly over ranks"
+    lb, le = rank * L // world, (rank + 1) * L // world
+    n0 = wl.n[0]
+    d0b, d0e = rank * n0 // world, (rank + 1) * n0 // world
+    x = torch.from_numpy(synth.gen_batch(wl, [0])).to(dev)
+    mine = plan.new_bitmaps(1, le - lb)
+    full = plan.new_bitmaps(1)
+    gath = torch.empty((world, le - lb, plan.bitmap_words), dtype=torch.int32, device=dev)
+    slab_words = (d0e - d0b) * (plan.ntot // n0) // 32
+    det = torch.empty((1, slab_words), dtype=torch.int32, device=dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        plan.execute(x, loop_begin=lb, loop_end=le, bitmaps=mine)
+        n = plan.last_launch_count()
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gath, mine[0])
+            full.copy_(gath.reshape(1, L, plan.bitmap_words))
+            src = full
+        else:
+            src = mine
+        plan.detect(src, dim0=(d0b, d0e), detect=det)
+        n += plan.last_launch_count()
+        return n
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches = 0
+    t0.record(stream)
+    for k in range(a.steps):
+        launches += step(ev[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    el = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    step_ms = float(el.item()) / a.steps
+    k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    peak, peak_src = load_peaks()
+    algo = 8 * plan.ntot + (le - lb) * plan.bitmap_words * 4
+    out = {
+        "metric": METRIC, "value": 1000.0 / step_ms, "unit": "cubes/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic: 1 seeded Eq. sig_model cube",
+        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": L,
+                   "parallelism": f"loops sharded {world} ways + NCCL all-gather of bitmaps"},
+        "roofline": {"bound": "hbm", "achieved": algo / (k1 / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": algo / (k1 / 1000.0) / 1e9 / peak, "traffic": load_traffic(wl.name),
+                     "kernel": "k_split_fold + k_split_fft", "avg_launch_ms": k1, "peak_source": peak_src},
+        "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None, "e2e": None,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c4_batched_2d", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the workload's batch)")
+    ap.add_argument("--pool", type=int, default=256, help="distinct seeded frames per GPU (tiled)")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        return run_reference(a)
+    return main_gpu(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -14,7 +14,9 @@
 // Fused mode (D <= 2, many frames): K1 + K2 in one persistent kernel, one CTA per frame;
 // the [L][B] buckets never leave shared memory.  Split mode (D >= 2, big frames): K1 per
 // (frame, outer residue class) + an outer-dimension FFT kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdio>
 #include <string>
@@ -31,12 +33,17 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
-// Streaming 16-byte load: x is read exactly once, keep it out of L1.
+// Streaming 16-byte load of x (read exactly once: no L1 allocation).  Volatile so that a
+// row group's U loads stay in program order; pin() below then forces all U loads to be
+// issued before the first FMA consumes any of them (U x 512 B in flight per warp).
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
   return r;
+}
+__device__ __forceinline__ void pin(float4& a) {
+  asm volatile("" : "+f"(a.x), "+f"(a.y), "+f"(a.z), "+f"(a.w));
 }
 
 __device__ __forceinline__ int brev(int v, int lg) { return lg ? (int)(__brev((unsigned)v) >> (32 - lg)) : 0; }
@@ -125,155 +132,296 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
 }
 
 // ------------------------------------------------------------------------------------
-// Fused mode: persistent, one CTA per frame.  D in {1, 2}, N_last >= 64.
-// smem: F [G][nl][bouter][blast+1] | Gb [nl][bouter][blast+1] | tw[128] float2 |
-//       rowW [N0][LP] float (D == 2)
+// TMA bulk-copy pipeline (per warp): lane 0 streams row segments of x global -> shared
+// with cp.async.bulk (SASS UBLKCP) into a kStages-deep ring, completion tracked by one
+// mbarrier per stage (expect_tx / complete_tx); all lanes wait on the stage's phase, read
+// their 16 B with LDS.128 and run the FFMA2 fold.  Bytes in flight per warp are explicit
+// ((kStages-1) x U x 512 B), independent of registers and of ptxas scheduling.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// Tensor-map TMA (cp.async.bulk.tensor; SASS UTMALDG): one instruction moves a whole box
+// (U rows x 512 B of one residue class), zero-filling out-of-bounds rows.
+__device__ __forceinline__ void tma_load_4d(void* dst, uint64_t tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4, %5}], [%6];"
+               :: "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, uint64_t tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  }
+}
+
+// One row group: U row-loads of 32 float4 (512 B) per warp, already in the stage buffer.
+// acc[l] += w_row[l] * x for each row; rows >= cnt contribute nothing.
+template <int LP, int U>
+__device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* __restrict__ buf, int lane,
+                                           int cnt, const float* const (&wrow)[U]) {
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    v[u] = buf[u * 32 + lane];
+    if (u >= cnt) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
+#pragma unroll
+    for (int l2 = 0; l2 < LP / 2; ++l2) {
+      float2 w = wr[l2];
+      mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
+      mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
+      mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
+      mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Fused mode: persistent CTAs, one frame at a time per CTA.  D in {1, 2}, N_last >= 64.
+// Warp task = (outer residue class kappa, segment group g); unit = (task, 64-column
+// segment); a unit folds the A0 rows of class kappa over its segment (D == 1: one row).
+// smem: ring [nwarps][S][U][32] float4 | bars [nwarps][S] | F [G][nl][bouter][blast+1] |
+//       tw[128] | rowW [N0+1][LP] float (row N0 = zeros)
 // ------------------------------------------------------------------------------------
 template <int LP, int U>
-__global__ void __launch_bounds__(kThreads) k_fused(PlanDev pd, const float4* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
                                                     int64_t batch, int l0, int nl,
                                                     uint32_t* __restrict__ bitmaps,
                                                     float2* __restrict__ spectra) {
-  extern __shared__ float4 smem_f4[];
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int S = kStages;
   const int D = pd.D;
   const int blast = pd.blast, nlast = pd.nlast, bouter = pd.bouter;
   const int fstride = blast + 1;
   const int nseg = nlast >> 6;
   const int G = (D == 1) ? (nseg < 8 ? nseg : 8) : 1;
-  float2* F = reinterpret_cast<float2*>(smem_f4);
-  const int fslot = nl * bouter * fstride;        // one group's slot
-  float2* Gb = F + (size_t)G * fslot;             // FFT buffer [nl][bouter][fstride]
-  float2* tw = Gb + fslot;                        // 128 twiddles
-  float* rowW = reinterpret_cast<float*>(tw + 128);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  float4* ring = reinterpret_cast<float4*>(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)nwarps * S * U * 32);
+  float2* F = reinterpret_cast<float2*>(bars + nwarps * S);
+  const int fslot = nl * bouter * fstride;
+  float2* tw = F + (size_t)G * fslot;
+  float* rowW = reinterpret_cast<float*>(tw + 128);
+  float4* myring = ring + (size_t)warp * S * U * 32;
+  uint64_t* mybar = bars + warp * S;
 
+  const int n0 = D == 2 ? pd.n[0] : 1;
   load_twiddles(tw);
-  if (D == 2) {
-    const int n0 = pd.n[0];
-    for (int i = tid; i < n0 * LP; i += blockDim.x) {
-      int s0 = i / LP, l = i - s0 * LP;
-      rowW[i] = l < nl ? pd.h[0][(size_t)(l0 + l) * n0 + s0] : 0.f;
-    }
+  for (int i = tid; i < (n0 + 1) * LP; i += blockDim.x) {
+    int s0 = i / LP, l = i - s0 * LP;
+    float w = 0.f;
+    if (l < nl && s0 < n0) w = D == 2 ? pd.h[0][(size_t)(l0 + l) * n0 + s0] : 1.f;
+    rowW[i] = w;
   }
+  if (lane == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&mybar[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
   const float* __restrict__ hlast = pd.h[D - 1];
   const int ntasks = bouter * G;
-  const int nrows = nlast >> 1;                   // float4 per row
+  const int A0 = D == 2 ? pd.a[0] : 1, B0 = D == 2 ? pd.b[0] : 1;
+  const int spt = nseg / G;                        // segments per task
+  const int ntw = warp < ntasks ? (ntasks - 1 - warp) / nwarps + 1 : 0;
+  // D == 2: unit = (task, segment), groups of U rows of the class.  D == 1: unit = task,
+  // groups of U consecutive 64-column segments of the single row.
+  const int units = D == 2 ? ntw * spt : ntw;
+  const int ngrp = D == 2 ? (A0 + U - 1) / U : (spt + U - 1) / U;
+  const int64_t per_frame = (int64_t)units * ngrp;
+  const int64_t nfr = batch > (int64_t)blockIdx.x ? (batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nfr * per_frame;
   const int fold_lanes = blast >= 2 ? blast / 2 : 1;
   const int fold_e = blast >= 2 ? 2 : 1;
+  const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
 
-  for (int64_t frame = blockIdx.x; frame < batch; frame += gridDim.x) {
-    for (int i = tid; i < G * fslot; i += blockDim.x) F[i] = make_float2(0.f, 0.f);
-    __syncthreads();
-    const float4* __restrict__ xf = x + frame * (pd.ntot >> 1);
-    for (int task = warp; task < ntasks; task += nwarps) {
-      const int kappa = task / G, g = task - kappa * G;
-      for (int seg = g; seg < nseg; seg += G) {
+  auto issue = [&](int64_t q) {                    // lane 0: TMA box of group q -> stage q % S
+    int64_t fi = q / per_frame;
+    int rem = (int)(q - fi * per_frame);
+    int unit = rem / ngrp, grp = rem - unit * ngrp;
+    int frame = (int)(blockIdx.x + fi * gridDim.x);
+    int st = (int)(q % S);
+    mbar_expect_tx(&mybar[st], (uint32_t)U * 512u);
+    float4* dst = myring + (size_t)st * U * 32;
+    if (D == 2) {                                  // box [64 cols][U rows a] of class kappa
+      int tk = unit / spt, seg = unit - tk * spt;
+      int kappa = warp + tk * nwarps;
+      tma_load_4d(dst, tmap_ptr, seg * 64, kappa, grp * U, frame, &mybar[st]);
+    } else {                                       // box [64 cols][U segments]
+      int g = warp + unit * nwarps;
+      tma_load_3d(dst, tmap_ptr, 0, g * spt + grp * U, frame, &mybar[st]);
+    }
+  };
+
+  if (lane == 0)
+    for (int64_t j = 0; j < S - 1 && j < total; ++j) issue(j);
+  int64_t q = 0;
+  for (int64_t fi = 0; fi < nfr; ++fi) {
+    const int64_t frame = blockIdx.x + fi * gridDim.x;
+    for (int unit = 0; unit < units; ++unit) {
+      if (D == 2) {
+        const int tk = unit / spt, seg = unit - tk * spt;
+        const int kappa = warp + tk * nwarps;
         float2 acc[LP][2];
 #pragma unroll
         for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-        const int col4 = seg * 32 + lane;
-        if (D == 2) {
-          const int A0 = pd.a[0], B0 = pd.b[0];
-          for (int a = 0; a < A0; a += U) {
-            float4 v[U];
+        for (int grp = 0; grp < ngrp; ++grp, ++q) {
+          if (lane == 0 && q + S - 1 < total) issue(q + S - 1);
+          const int st = (int)(q % S);
+          mbar_wait(&mybar[st], (uint32_t)((q / S) & 1));
+          const int a0 = grp * U;
+          const int cnt = A0 - a0 < U ? A0 - a0 : U;
+          const float* wrow[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              int s0 = kappa + B0 * (a + u);
-              v[u] = (a + u < A0) ? ld_stream(xf + (size_t)s0 * nrows + col4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              int s0 = kappa + B0 * (a + u);
-              if (a + u >= A0) s0 = kappa;        // weight irrelevant: v == 0
-              const float2* wr = reinterpret_cast<const float2*>(rowW + s0 * LP);
-#pragma unroll
-              for (int l2 = 0; l2 < LP / 2; ++l2) {
-                float2 w = wr[l2];
-                mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
-                mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
-                mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
-                mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
-              }
-            }
-          }
-        } else {
-          float4 v = ld_stream(xf + col4);
-#pragma unroll
-          for (int l = 0; l < LP; ++l) {
-            acc[l][0] = make_float2(v.x, v.y);
-            acc[l][1] = make_float2(v.z, v.w);
-          }
+          for (int u = 0; u < U; ++u) wrow[u] = rowW + (u < cnt ? kappa + B0 * (a0 + u) : n0) * LP;
+          fold_group<LP, U>(acc, myring + (size_t)st * U * 32, lane, cnt, wrow);
+          __syncwarp();
         }
-        colweight_fold<LP>(acc, hlast, l0, nl, nlast, 2 * col4, blast);
+        colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane, blast);
         if (lane < fold_lanes) {
-          float2* slot = F + (size_t)g * fslot + kappa * fstride + 2 * lane;
+          float2* slot = F + kappa * fstride + 2 * lane;
 #pragma unroll
           for (int l = 0; l < LP; ++l)
             if (l < nl)
               for (int e = 0; e < fold_e; ++e) {
                 float2* dst = slot + (size_t)l * bouter * fstride + e;
-                *dst = cadd(*dst, acc[l][e]);
+                *dst = seg == 0 ? acc[l][e] : cadd(*dst, acc[l][e]);
               }
+        }
+      } else {
+        const int g = warp + unit * nwarps;
+        for (int grp = 0; grp < ngrp; ++grp, ++q) {
+          if (lane == 0 && q + S - 1 < total) issue(q + S - 1);
+          const int st = (int)(q % S);
+          mbar_wait(&mybar[st], (uint32_t)((q / S) & 1));
+          const int cnt = spt - grp * U < U ? spt - grp * U : U;
+          for (int u = 0; u < cnt; ++u) {
+            const int seg = g * spt + grp * U + u;
+            float4 v = myring[((size_t)st * U + u) * 32 + lane];
+            float2 acc[LP][2];
+#pragma unroll
+            for (int l = 0; l < LP; ++l) {
+              acc[l][0] = make_float2(v.x, v.y);
+              acc[l][1] = make_float2(v.z, v.w);
+            }
+            colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane, blast);
+            if (lane < fold_lanes) {
+              float2* slot = F + (size_t)g * fslot + 2 * lane;
+#pragma unroll
+              for (int l = 0; l < LP; ++l)
+                if (l < nl)
+                  for (int e = 0; e < fold_e; ++e) {
+                    float2* dst = slot + (size_t)l * fstride + e;
+                    *dst = (grp == 0 && u == 0) ? acc[l][e] : cadd(*dst, acc[l][e]);
+                  }
+            }
+          }
+          __syncwarp();
         }
       }
     }
     __syncthreads();
     if (G > 1) {                                  // deterministic combine of segment groups
       for (int i = tid; i < fslot; i += blockDim.x) {
-        float2 s = F[i];
-        for (int gg = 1; gg < G; ++gg) s = cadd(s, F[(size_t)gg * fslot + i]);
-        F[i] = s;
+        float2 sum = F[i];
+        for (int gg = 1; gg < G; ++gg) sum = cadd(sum, F[(size_t)gg * fslot + i]);
+        F[i] = sum;
       }
       __syncthreads();
     }
     // residue -> bucket (b_d = sigma^{-1}(r_d - tau_d) mod B_d, I3) with the half-bucket
-    // twiddles e^{-j pi b_d / B_d} (L1), written bit-reversed for the in-place DIT FFT.
+    // twiddles e^{-j pi b_d / B_d} (L1); the permutation goes through registers, landing
+    // bit-reversed for the in-place DIT FFT.
     {
+      constexpr int PMAX = 8;                      // elements per thread per round
       const int dl = D - 1;
       const int lgbl = pd.lgb[dl], lgb0 = pd.lgb[0];
-      const int nel = nl * bouter * blast;
-      for (int i = tid; i < nel; i += blockDim.x) {
-        int l = i / (bouter * blast), rem = i - l * bouter * blast;
-        int ro = rem >> lgbl, rl = rem & (blast - 1);
-        const LoopDev& lp = pd.loops[l0 + l];
-        int bl = (lp.sinv[dl] * (rl - lp.tau[dl])) & (blast - 1);
-        float2 v = F[((size_t)l * bouter + ro) * fstride + rl];
-        if (pd.shift[dl]) v = cmul(v, tw[bl << (6 - lgbl)]);
-        int bo = 0;
-        if (D == 2) {
-          bo = (lp.sinv[0] * (ro - lp.tau[0])) & (bouter - 1);
-          if (pd.shift[0]) v = cmul(v, tw[bo << (6 - lgb0)]);
-          bo = brev(bo, lgb0);
+      const int per_loop = bouter * blast;
+      int lchunk = (PMAX * (int)blockDim.x) / per_loop;
+      if (lchunk < 1) lchunk = 1;
+      for (int lb = 0; lb < nl; lb += lchunk) {
+        const int le = lb + lchunk < nl ? lb + lchunk : nl;
+        const int nel = (le - lb) * per_loop;
+        float2 pv[PMAX];
+        int pdst[PMAX];
+#pragma unroll
+        for (int j = 0; j < PMAX; ++j) {
+          int i = tid + j * blockDim.x;
+          pdst[j] = -1;
+          if (i < nel) {
+            int l = lb + i / per_loop, rem = i - (l - lb) * per_loop;
+            int ro = rem >> lgbl, rl = rem & (blast - 1);
+            const LoopDev& lp = pd.loops[l0 + l];
+            int bl = (lp.sinv[dl] * (rl - lp.tau[dl])) & (blast - 1);
+            float2 v = F[((size_t)l * bouter + ro) * fstride + rl];
+            if (pd.shift[dl]) v = cmul(v, tw[bl << (6 - lgbl)]);
+            int bo = 0;
+            if (D == 2) {
+              bo = (lp.sinv[0] * (ro - lp.tau[0])) & (bouter - 1);
+              if (pd.shift[0]) v = cmul(v, tw[bo << (6 - lgb0)]);
+              bo = brev(bo, lgb0);
+            }
+            pv[j] = v;
+            pdst[j] = ((l * bouter + bo) * fstride) + brev(bl, lgbl);
+          }
         }
-        Gb[((size_t)l * bouter + bo) * fstride + brev(bl, lgbl)] = v;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PMAX; ++j)
+          if (pdst[j] >= 0) F[pdst[j]] = pv[j];
+        __syncthreads();
       }
     }
-    __syncthreads();
     {
       View vw;
       vw.k = 3;
       vw.n[0] = nl; vw.lg[0] = 0; vw.st[0] = bouter * fstride;
       vw.n[1] = bouter; vw.lg[1] = D == 2 ? pd.lgb[0] : 0; vw.st[1] = fstride;
       vw.n[2] = blast; vw.lg[2] = pd.lgb[D - 1]; vw.st[2] = 1;
-      fft_axis(Gb, vw, 2, tw);
-      if (D == 2) fft_axis(Gb, vw, 1, tw);
+      fft_axis(F, vw, 2, tw);
+      if (D == 2) fft_axis(F, vw, 1, tw);
     }
     // |fhat|^2 > gamma_l -> ballot -> bitmap words (Alg. 1 l.10)
     const int wpl = pd.wpl;
     const int nitems = nl * wpl * 32;
     for (int it = tid; it < nitems; it += blockDim.x) {
-      int l = it / (wpl * 32), rem = it - l * wpl * 32;
-      int k = rem;                                 // flat bucket index
+      int l = it / (wpl * 32), k = it - l * wpl * 32;   // flat bucket index
       bool bit = false;
       if (k < pd.btot) {
         int ko = k / blast, kl = k - ko * blast;
-        float2 v = Gb[((size_t)l * bouter + ko) * fstride + kl];
-        float pw = v.x * v.x + v.y * v.y;
-        bit = pw > pd.loops[l0 + l].gamma;
+        float2 v = F[((size_t)l * bouter + ko) * fstride + kl];
+        bit = v.x * v.x + v.y * v.y > pd.loops[l0 + l].gamma;
         if (spectra) spectra[((size_t)frame * nl + l) * pd.btot + k] = v;
       }
       unsigned word = __ballot_sync(0xffffffffu, bit);
-      if (lane == 0) bitmaps[((size_t)frame * nl + l) * wpl + (rem >> 5)] = word;
+      if (lane == 0) bitmaps[((size_t)frame * nl + l) * wpl + (k >> 5)] = word;
     }
     __syncthreads();
   }
@@ -281,35 +429,43 @@ __global__ void __launch_bounds__(kThreads) k_fused(PlanDev pd, const float4* __
 
 // ------------------------------------------------------------------------------------
 // Split mode, kernel 1: one CTA per (outer residue class kappa, frame); D in {2, 3}.
-// smem: tw[128] | sbo[32] | rw [RA][LP] float | part [nwarps][nl][blast] | R [nl][blast+1]
-// Output fbuf[frame][l][Bo(l)][k_last]: last-dim FFT done, outer twiddles applied.
+// Rows of the class are streamed per warp through the TMA ring (rows of N_last < 64
+// complex are packed 64/N_last per 512 B slot).
+// smem: ring [nwarps][S][U][32] | bars | tw[128] | sbo[32] | rw [RA+1][LP] |
+//       part [nwarps][nl][blast] | R [nl][blast+1]
+// Output fbuf[frame][l][Bo(l)][k_last]: last-dim FFT done, all half twiddles applied.
 // ------------------------------------------------------------------------------------
 template <int LP, int U>
-__global__ void __launch_bounds__(kThreads) k_split_fold(PlanDev pd, const float4* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
                                                          int l0, int nl, uint32_t* __restrict__ bitmaps) {
-  extern __shared__ float4 smem_f4[];
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int S = kStages;
   const int D = pd.D;
   const int kappa = blockIdx.x;
   const int64_t frame = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int blast = pd.blast, nlast = pd.nlast;
   const int RA = pd.aouter;
-  float2* tw = reinterpret_cast<float2*>(smem_f4);
+  float4* ring = reinterpret_cast<float4*>(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)nwarps * S * U * 32);
+  float2* tw = reinterpret_cast<float2*>(bars + nwarps * S);
   int* sbo = reinterpret_cast<int*>(tw + 128);       // [32] outer bucket per loop
   float* rw = reinterpret_cast<float*>(sbo + kMaxLoops);
-  float2* part = reinterpret_cast<float2*>(rw + (size_t)RA * LP);
+  float2* part = reinterpret_cast<float2*>(rw + (size_t)(RA + 1) * LP);
   float2* R = part + (size_t)nwarps * nl * blast;
+  float4* myring = ring + (size_t)warp * S * U * 32;
+  uint64_t* mybar = bars + warp * S;
   load_twiddles(tw);
 
-  // outer residues of the class and row enumeration
   int r0, r1 = 0;
   if (D == 3) { r0 = kappa / pd.b[1]; r1 = kappa - r0 * pd.b[1]; } else { r0 = kappa; }
-  for (int i = tid; i < RA * LP; i += blockDim.x) {
+  const int lga1 = D == 3 ? pd.lga[1] : 0;
+  for (int i = tid; i < (RA + 1) * LP; i += blockDim.x) {
     int q = i / LP, l = i - q * LP;
     float w = 0.f;
-    if (l < nl) {
+    if (l < nl && q < RA) {
       if (D == 3) {
-        int a0 = q / pd.a[1], a1 = q - a0 * pd.a[1];
+        int a0 = q >> lga1, a1 = q & (pd.a[1] - 1);
         int s0 = r0 + pd.b[0] * a0, s1 = r1 + pd.b[1] * a1;
         w = pd.h[0][(size_t)(l0 + l) * pd.n[0] + s0] * pd.h[1][(size_t)(l0 + l) * pd.n[1] + s1];
       } else {
@@ -319,25 +475,33 @@ __global__ void __launch_bounds__(kThreads) k_split_fold(PlanDev pd, const float
     }
     rw[i] = w;
   }
-  // zero this frame's bitmap words (K2 sets bits with atomicOr)
-  {
+  {                                                 // zero this frame's bitmap words (K2 ORs bits)
     const int64_t words = (int64_t)nl * pd.wpl;
     uint32_t* bm = bitmaps + frame * words;
     for (int64_t w = (int64_t)kappa * blockDim.x + tid; w < words; w += (int64_t)gridDim.x * blockDim.x) bm[w] = 0u;
   }
   for (int i = tid; i < nwarps * nl * blast; i += blockDim.x) part[i] = make_float2(0.f, 0.f);
+  if (lane == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&mybar[st], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
 
   const int nseg = nlast >= 64 ? nlast >> 6 : 1;
-  const int rpw = nlast >= 64 ? 1 : 64 / nlast;      // rows per warp-load
+  const int rpw = nlast >= 64 ? 1 : 64 / nlast;      // rows per 512 B slot
   const int lpr = 32 / rpw;                          // lanes per row
   const int lane_row = lane / lpr, lane_c4 = lane - lane_row * lpr;
-  const int nq = (RA + rpw - 1) / rpw;               // warp-load row groups
-  const int nrows4 = nlast >> 1;
-  const float4* __restrict__ xf = x + frame * (pd.ntot >> 1);
   const int fold_lanes = blast >= 2 ? blast / 2 : 1;
   const int fold_e = blast >= 2 ? 2 : 1;
+  // Row blocks: BR = U * rpw consecutive values of the innermost outer index a_run
+  // (a1 for D == 3, a0 for D == 2) per TMA box; a_outer = a0 for D == 3.
+  const int BR = U * rpw;
+  const int AR = D == 3 ? pd.a[1] : pd.a[0];
+  const int nb_run = (AR + BR - 1) / BR;
+  const int nblk = (D == 3 ? pd.a[0] : 1) * nb_run;
+  const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
 
+  // warp -> (segments, block subset): wps warps share a segment, interleaving its blocks
   int seg_start, seg_step, wsub, wps;
   if (nseg >= nwarps) { seg_start = warp; seg_step = nwarps; wsub = 0; wps = 1; }
   else {
@@ -346,43 +510,46 @@ __global__ void __launch_bounds__(kThreads) k_split_fold(PlanDev pd, const float
     seg_step = nseg;
     wsub = warp / nseg;
   }
-  for (int seg = seg_start; seg < nseg; seg += seg_step) {
+  const int nsegw = seg_start < nseg ? (nseg - 1 - seg_start) / seg_step + 1 : 0;
+  const int ngrp = wsub < nblk ? (nblk - 1 - wsub) / wps + 1 : 0;   // my blocks per segment
+  const int64_t total = (int64_t)nsegw * ngrp;
+
+  auto issue = [&](int64_t qg) {                     // lane 0: one TMA box per group
+    int si = (int)(qg / ngrp), k = (int)(qg - (int64_t)si * ngrp);
+    int seg = seg_start + si * seg_step;
+    int bi = wsub + k * wps;
+    int ao = bi / nb_run, rb = bi - ao * nb_run;
+    int st = (int)(qg % S);
+    mbar_expect_tx(&mybar[st], (uint32_t)U * 512u);
+    float4* dst = myring + (size_t)st * U * 32;
+    if (D == 3)
+      tma_load_4d(dst, tmap_ptr, seg * 64, r1, rb * BR, (int)(frame * pd.n[0] + r0 + pd.b[0] * ao), &mybar[st]);
+    else
+      tma_load_4d(dst, tmap_ptr, seg * 64, r0, rb * BR, (int)frame, &mybar[st]);
+  };
+
+  if (lane == 0)
+    for (int64_t j = 0; j < S - 1 && j < total; ++j) issue(j);
+  int64_t qg = 0;
+  for (int si = 0; si < nsegw; ++si) {
+    const int seg = seg_start + si * seg_step;
     float2 acc[LP][2];
 #pragma unroll
     for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-    const int c4 = seg * 32 + lane_c4;
-    for (int qg = wsub; qg < nq; qg += U * wps) {
-      float4 v[U];
-      int qq[U];
+    for (int k = 0; k < ngrp; ++k, ++qg) {
+      if (lane == 0 && qg + S - 1 < total) issue(qg + S - 1);
+      const int st = (int)(qg % S);
+      mbar_wait(&mybar[st], (uint32_t)((qg / S) & 1));
+      const int bi = wsub + k * wps;
+      const int ao = bi / nb_run, rb = bi - ao * nb_run;
+      const float* wrow[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        int q = (qg + u * wps) * rpw + lane_row;
-        qq[u] = q;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (qg + u * wps < nq && q < RA) {
-          int64_t row;
-          if (D == 3) {
-            int a0 = q / pd.a[1], a1 = q - a0 * pd.a[1];
-            row = (int64_t)(r0 + pd.b[0] * a0) * pd.n[1] + (r1 + pd.b[1] * a1);
-          } else {
-            row = r0 + (int64_t)pd.b[0] * q;
-          }
-          v[u] = ld_stream(xf + row * nrows4 + c4);
-        }
+        int arun = rb * BR + u * rpw + lane_row;
+        wrow[u] = rw + (size_t)(arun < AR ? ao * AR + arun : RA) * LP;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int q = qq[u] < RA ? qq[u] : 0;
-        const float2* wr = reinterpret_cast<const float2*>(rw + (size_t)q * LP);
-#pragma unroll
-        for (int l2 = 0; l2 < LP / 2; ++l2) {
-          float2 w = wr[l2];
-          mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
-          mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
-          mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
-          mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
-        }
-      }
+      fold_group<LP, U>(acc, myring + (size_t)st * U * 32, lane, U, wrow);
+      __syncwarp();
     }
     colweight_fold<LP>(acc, pd.h[D - 1], l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
     if (lane < fold_lanes) {
@@ -402,22 +569,22 @@ __global__ void __launch_bounds__(kThreads) k_split_fold(PlanDev pd, const float
   const int lgbl = pd.lgb[D - 1];
   for (int i = tid; i < nl * blast; i += blockDim.x) {
     int l = i >> lgbl, r = i & (blast - 1);
-    float2 s = make_float2(0.f, 0.f);
-    for (int w = 0; w < nwarps; ++w) s = cadd(s, part[((size_t)w * nl + l) * blast + r]);
+    float2 sum = make_float2(0.f, 0.f);
+    for (int w = 0; w < nwarps; ++w) sum = cadd(sum, part[((size_t)w * nl + l) * blast + r]);
     const LoopDev& lp = pd.loops[l0 + l];
     const int dl = D - 1;
     int bl = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
-    if (pd.shift[dl]) s = cmul(s, tw[bl << (6 - lgbl)]);
+    if (pd.shift[dl]) sum = cmul(sum, tw[bl << (6 - lgbl)]);
     int b0 = (lp.sinv[0] * (r0 - lp.tau[0])) & (pd.b[0] - 1);
-    if (pd.shift[0]) s = cmul(s, tw[b0 << (6 - pd.lgb[0])]);
+    if (pd.shift[0]) sum = cmul(sum, tw[b0 << (6 - pd.lgb[0])]);
     int bo = b0;
     if (D == 3) {
       int b1 = (lp.sinv[1] * (r1 - lp.tau[1])) & (pd.b[1] - 1);
-      if (pd.shift[1]) s = cmul(s, tw[b1 << (6 - pd.lgb[1])]);
+      if (pd.shift[1]) sum = cmul(sum, tw[b1 << (6 - pd.lgb[1])]);
       bo = b0 * pd.b[1] + b1;
     }
     if (r == 0) sbo[l] = bo;
-    R[(size_t)l * rstride + brev(bl, lgbl)] = s;
+    R[(size_t)l * rstride + brev(bl, lgbl)] = sum;
   }
   __syncthreads();
   {
@@ -652,26 +819,69 @@ static rsft_status check(cudaError_t e, const char* what) {
   return RSFT_E_CUDA;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Tensor map over complex64 x (8-byte elements, no swizzle, OOB -> zeros).
+static rsft_status make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+                            const cuuint64_t* strides, const cuuint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return RSFT_E_CUDA; }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_INT64, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r)); return RSFT_E_CUDA; }
+  return RSFT_OK;
+}
+
+// Map for the fold kernels: D >= 2 -> [N_last][B_o][A_o][planes] (B_o, A_o of the innermost
+// outer dim, planes = batch (D == 2) or batch * N_0 (D == 3)); D == 1 -> [64][N/64][batch].
+static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, CUtensorMap* m) {
+  const int D = p->D;
+  const uint64_t e = 8;
+  if (D == 1) {
+    cuuint64_t dims[3] = {64, (cuuint64_t)(p->n[0] / 64), (cuuint64_t)batch};
+    cuuint64_t str[2] = {64 * e, (cuuint64_t)p->n[0] * e};
+    cuuint32_t box[3] = {64, (cuuint32_t)kU, 1};
+    return make_map(m, d_x, 3, dims, str, box);
+  }
+  const int64_t nl = p->n[D - 1], no = p->n[D - 2], bo = p->b[D - 2], ao = p->a[D - 2];
+  const int64_t planes = D == 3 ? batch * p->n[0] : batch;
+  const int64_t rpw = nl >= 64 ? 1 : 64 / nl;
+  cuuint64_t dims[4] = {(cuuint64_t)nl, (cuuint64_t)bo, (cuuint64_t)ao, (cuuint64_t)planes};
+  cuuint64_t str[3] = {(cuuint64_t)(nl * e), (cuuint64_t)(bo * nl * e), (cuuint64_t)(no * nl * e)};
+  cuuint32_t box[4] = {(cuuint32_t)(nl >= 64 ? 64 : nl), 1, (cuuint32_t)(kU * rpw), 1};
+  return make_map(m, d_x, 4, dims, str, box);
+}
+
 template <int LP>
 static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                   uint32_t* bm, void* spectra, cudaStream_t st) {
-  constexpr int U = LP <= 8 ? 8 : 4;
-  auto kern = k_fused<LP, U>;
-  const int D = p->D;
-  const int64_t blast = p->b[D - 1], nlast = p->n[D - 1], bouter = p->btot / blast;
-  const int64_t nseg = nlast / 64;
-  const int64_t G = D == 1 ? (nseg < 8 ? nseg : 8) : 1;
-  size_t smem = (size_t)(G + 1) * nl * bouter * (blast + 1) * 8 + 128 * 8 + (D == 2 ? (size_t)p->n[0] * LP * 4 : 0);
-  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  auto kern = k_fused<LP, kU>;
+  const size_t smem = fused_smem_bytes(p, nl, LP);
+  CUtensorMap tmap;
+  rsft_status s = fold_map(p, d_x, batch, &tmap);
+  if (s) return s;
+  s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   int nb = 0;
   s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem), "occupancy");
   if (s) return s;
-  if (nb < 1) nb = 1;
+  if (nb < 1) { set_error("k_fused: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > batch) grid = batch;
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, reinterpret_cast<const float4*>(d_x), batch, l0, nl,
-                                               bm, reinterpret_cast<float2*>(spectra));
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra));
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_fused launch");
 }
@@ -679,18 +889,17 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
 template <int LP>
 static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                   uint32_t* bm, void* spectra, cudaStream_t st) {
-  constexpr int U = LP <= 8 ? 8 : 4;
-  auto kern = k_split_fold<LP, U>;
+  auto kern = k_split_fold<LP, kU>;
   const int D = p->D;
   const int64_t blast = p->b[D - 1];
-  const int64_t RA = p->dev.aouter;
-  const int nwarps = kThreads / 32;
-  size_t smem = 128 * 8 + kMaxLoops * 4 + (size_t)RA * LP * 4 + (size_t)nwarps * nl * blast * 8 +
-                (size_t)nl * (blast + 1) * 8;
-  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  const size_t smem = split_smem_bytes(p, nl, LP);
+  CUtensorMap tmap;
+  rsft_status s = fold_map(p, d_x, batch, &tmap);
+  if (s) return s;
+  s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   dim3 grid((unsigned)p->dev.bouter, (unsigned)batch);
-  kern<<<grid, kThreads, smem, st>>>(p->dev, reinterpret_cast<const float4*>(d_x), l0, nl, bm);
+  kern<<<grid, kThreads, smem, st>>>(p->dev, tmap, l0, nl, bm);
   p->last_launches += 1;
   s = check(cudaGetLastError(), "k_split_fold launch");
   if (s) return s;

@@ -159,21 +159,35 @@ void layout_workspace(rsft_plan_s* p) {
   w.total = off;
 }
 
-// Fused mode: one CTA per frame keeps its [L][B_tot] buckets in shared memory.
-static size_t fused_smem(const rsft_plan_s* p, int lpad) {
+// Shared-memory footprints (must match the carve-up at the top of k_fused / k_split_fold).
+size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
+  const int nwarps = kThreads / 32;
   int64_t blast = p->b[p->D - 1], nlast = p->n[p->D - 1];
   int64_t bouter = p->btot / blast;
   int64_t nseg = nlast / 64;
   int64_t groups = p->D == 1 ? (nseg < 8 ? nseg : 8) : 1;
-  size_t fbytes = (size_t)(groups + 1) * p->L * bouter * (blast + 1) * 8 + 128 * 8;
-  size_t wbytes = p->D == 2 ? (size_t)p->n[0] * lpad * 4 : 0;
-  return fbytes + wbytes;
+  int64_t n0 = p->D == 2 ? p->n[0] : 1;
+  size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
+  size_t fbytes = (size_t)groups * nl * bouter * (blast + 1) * 8 + 128 * 8;
+  return ring + fbytes + (size_t)(n0 + 1) * lpad * 4;
+}
+
+size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
+  const int nwarps = kThreads / 32;
+  int64_t blast = p->b[p->D - 1];
+  int64_t ra = 1;
+  for (int d = 0; d + 1 < p->D; ++d) ra *= p->a[d];
+  size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
+  return ring + 128 * 8 + kMaxLoops * 4 + (size_t)(ra + 1) * lpad * 4 + (size_t)nwarps * nl * blast * 8 +
+         (size_t)nl * (blast + 1) * 8;
 }
 
 int resolve_mode(const rsft_plan_s* p, int64_t batch) {
   const int64_t nlast = p->n[p->D - 1];
-  bool fused_ok = p->D <= 2 && nlast >= 64 && fused_smem(p, loop_pad(p->L)) <= 110 * 1024;
-  bool split_ok = p->D >= 2;
+  const int lp = loop_pad(p->L);
+  bool fused_ok = p->D <= 2 && nlast >= 64 && p->btot <= 8 * kThreads &&
+                  fused_smem_bytes(p, p->L, lp) <= 110 * 1024;
+  bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp) <= 220 * 1024;
   int m = p->P.mode;
   if (m == RSFT_MODE_FUSED) return fused_ok ? RSFT_MODE_FUSED : -1;
   if (m == RSFT_MODE_SPLIT) return split_ok ? RSFT_MODE_SPLIT : -1;

@@ -17,6 +17,8 @@ constexpr int kMaxLoops = 32;
 constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
 constexpr int64_t kChunkWords = 2048;  // compaction chunk: words of the detection bitmap
 constexpr int kThreads = 256;          // CTA size of every kernel
+constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
+constexpr int kU = 4;                  // 512 B row slots per ring stage
 
 // Per-loop device record: schedule + threshold (Def. 1; Eq. tpd).
 struct LoopDev {
@@ -82,5 +84,7 @@ rsft_status rebuild_tables(rsft_plan_s* p);
 void layout_workspace(rsft_plan_s* p);
 int resolve_mode(const rsft_plan_s* p, int64_t batch);
 int loop_pad(int nl);
+size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
+size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
 void set_error(const std::string& s);
 }  // namespace rsft
