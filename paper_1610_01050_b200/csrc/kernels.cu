@@ -179,16 +179,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // One row group: U row-loads of 32 float4 (512 B) per warp, already in the stage buffer.
-// acc[l] += w_row[l] * x for each row; rows >= cnt contribute nothing.
+// acc[l] += w_row[l] * x for each row.  Rows past the end of a class are zero-filled by
+// the TMA (out-of-bounds box rows) and carry the zero weight row, so they add nothing.
 template <int LP, int U>
 __device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* __restrict__ buf, int lane,
-                                           int cnt, const float* const (&wrow)[U]) {
+                                           const float* const (&wrow)[U]) {
   float4 v[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    v[u] = buf[u * 32 + lane];
-    if (u >= cnt) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  for (int u = 0; u < U; ++u) v[u] = buf[u * 32 + lane];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
@@ -255,54 +253,58 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
   // groups of U consecutive 64-column segments of the single row.
   const int units = D == 2 ? ntw * spt : ntw;
   const int ngrp = D == 2 ? (A0 + U - 1) / U : (spt + U - 1) / U;
-  const int64_t per_frame = (int64_t)units * ngrp;
   const int64_t nfr = batch > (int64_t)blockIdx.x ? (batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = nfr * per_frame;
+  const int64_t total = nfr * units * ngrp;
   const int fold_lanes = blast >= 2 ? blast / 2 : 1;
   const int fold_e = blast >= 2 ? 2 : 1;
   const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
+  const int lg_spt = __ffs(spt) - 1;               // spt is a power of two
 
-  auto issue = [&](int64_t q) {                    // lane 0: TMA box of group q -> stage q % S
-    int64_t fi = q / per_frame;
-    int rem = (int)(q - fi * per_frame);
-    int unit = rem / ngrp, grp = rem - unit * ngrp;
-    int frame = (int)(blockIdx.x + fi * gridDim.x);
-    int st = (int)(q % S);
-    mbar_expect_tx(&mybar[st], (uint32_t)U * 512u);
-    float4* dst = myring + (size_t)st * U * 32;
+  // producer cursor (lane 0): next group to load, advanced without divisions
+  int p_fi = 0, p_unit = 0, p_grp = 0, p_st = 0;
+  int64_t p_left = total;
+  auto issue_next = [&]() {
+    if (p_left <= 0) return;
+    --p_left;
+    const int frame = (int)(blockIdx.x + (int64_t)p_fi * gridDim.x);
+    mbar_expect_tx(&mybar[p_st], (uint32_t)U * 512u);
+    float4* dst = myring + (size_t)p_st * U * 32;
     if (D == 2) {                                  // box [64 cols][U rows a] of class kappa
-      int tk = unit / spt, seg = unit - tk * spt;
-      int kappa = warp + tk * nwarps;
-      tma_load_4d(dst, tmap_ptr, seg * 64, kappa, grp * U, frame, &mybar[st]);
+      const int kappa = warp + (p_unit >> lg_spt) * nwarps, seg = p_unit & (spt - 1);
+      tma_load_4d(dst, tmap_ptr, seg * 64, kappa, p_grp * U, frame, &mybar[p_st]);
     } else {                                       // box [64 cols][U segments]
-      int g = warp + unit * nwarps;
-      tma_load_3d(dst, tmap_ptr, 0, g * spt + grp * U, frame, &mybar[st]);
+      const int g = warp + p_unit * nwarps;
+      tma_load_3d(dst, tmap_ptr, 0, g * spt + p_grp * U, frame, &mybar[p_st]);
+    }
+    if (++p_st == S) p_st = 0;
+    if (++p_grp == ngrp) {
+      p_grp = 0;
+      if (++p_unit == units) { p_unit = 0; ++p_fi; }
     }
   };
 
   if (lane == 0)
-    for (int64_t j = 0; j < S - 1 && j < total; ++j) issue(j);
-  int64_t q = 0;
+    for (int j = 0; j < S - 1; ++j) issue_next();
+  int c_st = 0;
+  uint32_t c_ph = 0;
   for (int64_t fi = 0; fi < nfr; ++fi) {
     const int64_t frame = blockIdx.x + fi * gridDim.x;
     for (int unit = 0; unit < units; ++unit) {
       if (D == 2) {
-        const int tk = unit / spt, seg = unit - tk * spt;
-        const int kappa = warp + tk * nwarps;
+        const int kappa = warp + (unit >> lg_spt) * nwarps, seg = unit & (spt - 1);
         float2 acc[LP][2];
 #pragma unroll
         for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-        for (int grp = 0; grp < ngrp; ++grp, ++q) {
-          if (lane == 0 && q + S - 1 < total) issue(q + S - 1);
-          const int st = (int)(q % S);
-          mbar_wait(&mybar[st], (uint32_t)((q / S) & 1));
+        for (int grp = 0; grp < ngrp; ++grp) {
+          if (lane == 0) issue_next();
+          mbar_wait(&mybar[c_st], c_ph);
           const int a0 = grp * U;
-          const int cnt = A0 - a0 < U ? A0 - a0 : U;
           const float* wrow[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) wrow[u] = rowW + (u < cnt ? kappa + B0 * (a0 + u) : n0) * LP;
-          fold_group<LP, U>(acc, myring + (size_t)st * U * 32, lane, cnt, wrow);
+          for (int u = 0; u < U; ++u) wrow[u] = rowW + (a0 + u < A0 ? kappa + B0 * (a0 + u) : n0) * LP;
+          fold_group<LP, U>(acc, myring + (size_t)c_st * U * 32, lane, wrow);
           __syncwarp();
+          if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
         }
         colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane, blast);
         if (lane < fold_lanes) {
@@ -317,14 +319,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
         }
       } else {
         const int g = warp + unit * nwarps;
-        for (int grp = 0; grp < ngrp; ++grp, ++q) {
-          if (lane == 0 && q + S - 1 < total) issue(q + S - 1);
-          const int st = (int)(q % S);
-          mbar_wait(&mybar[st], (uint32_t)((q / S) & 1));
+        for (int grp = 0; grp < ngrp; ++grp) {
+          if (lane == 0) issue_next();
+          mbar_wait(&mybar[c_st], c_ph);
           const int cnt = spt - grp * U < U ? spt - grp * U : U;
           for (int u = 0; u < cnt; ++u) {
             const int seg = g * spt + grp * U + u;
-            float4 v = myring[((size_t)st * U + u) * 32 + lane];
+            float4 v = myring[((size_t)c_st * U + u) * 32 + lane];
             float2 acc[LP][2];
 #pragma unroll
             for (int l = 0; l < LP; ++l) {
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
             }
           }
           __syncwarp();
+          if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
         }
       }
     }
@@ -514,42 +516,55 @@ __global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __
   const int ngrp = wsub < nblk ? (nblk - 1 - wsub) / wps + 1 : 0;   // my blocks per segment
   const int64_t total = (int64_t)nsegw * ngrp;
 
-  auto issue = [&](int64_t qg) {                     // lane 0: one TMA box per group
-    int si = (int)(qg / ngrp), k = (int)(qg - (int64_t)si * ngrp);
-    int seg = seg_start + si * seg_step;
-    int bi = wsub + k * wps;
-    int ao = bi / nb_run, rb = bi - ao * nb_run;
-    int st = (int)(qg % S);
-    mbar_expect_tx(&mybar[st], (uint32_t)U * 512u);
-    float4* dst = myring + (size_t)st * U * 32;
+  // producer cursor (lane 0): (segment index, block ao/rb), advanced without divisions
+  int p_si = 0, p_k = 0, p_ao = wsub / nb_run, p_rb = wsub - (wsub / nb_run) * nb_run, p_st = 0;
+  int64_t p_left = total;
+  auto issue_next = [&]() {
+    if (p_left <= 0) return;
+    --p_left;
+    const int seg = seg_start + p_si * seg_step;
+    mbar_expect_tx(&mybar[p_st], (uint32_t)U * 512u);
+    float4* dst = myring + (size_t)p_st * U * 32;
     if (D == 3)
-      tma_load_4d(dst, tmap_ptr, seg * 64, r1, rb * BR, (int)(frame * pd.n[0] + r0 + pd.b[0] * ao), &mybar[st]);
+      tma_load_4d(dst, tmap_ptr, seg * 64, r1, p_rb * BR, (int)(frame * pd.n[0] + r0 + pd.b[0] * p_ao), &mybar[p_st]);
     else
-      tma_load_4d(dst, tmap_ptr, seg * 64, r0, rb * BR, (int)frame, &mybar[st]);
+      tma_load_4d(dst, tmap_ptr, seg * 64, r0, p_rb * BR, (int)frame, &mybar[p_st]);
+    if (++p_st == S) p_st = 0;
+    if (++p_k == ngrp) {
+      p_k = 0;
+      ++p_si;
+      p_ao = wsub / nb_run;
+      p_rb = wsub - p_ao * nb_run;
+    } else {
+      p_rb += wps;
+      while (p_rb >= nb_run) { p_rb -= nb_run; ++p_ao; }
+    }
   };
 
   if (lane == 0)
-    for (int64_t j = 0; j < S - 1 && j < total; ++j) issue(j);
-  int64_t qg = 0;
+    for (int j = 0; j < S - 1; ++j) issue_next();
+  int c_st = 0;
+  uint32_t c_ph = 0;
   for (int si = 0; si < nsegw; ++si) {
     const int seg = seg_start + si * seg_step;
     float2 acc[LP][2];
 #pragma unroll
     for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-    for (int k = 0; k < ngrp; ++k, ++qg) {
-      if (lane == 0 && qg + S - 1 < total) issue(qg + S - 1);
-      const int st = (int)(qg % S);
-      mbar_wait(&mybar[st], (uint32_t)((qg / S) & 1));
-      const int bi = wsub + k * wps;
-      const int ao = bi / nb_run, rb = bi - ao * nb_run;
+    int ao = wsub / nb_run, rb = wsub - (wsub / nb_run) * nb_run;
+    for (int k = 0; k < ngrp; ++k) {
+      if (lane == 0) issue_next();
+      mbar_wait(&mybar[c_st], c_ph);
       const float* wrow[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         int arun = rb * BR + u * rpw + lane_row;
         wrow[u] = rw + (size_t)(arun < AR ? ao * AR + arun : RA) * LP;
       }
-      fold_group<LP, U>(acc, myring + (size_t)st * U * 32, lane, U, wrow);
+      fold_group<LP, U>(acc, myring + (size_t)c_st * U * 32, lane, wrow);
       __syncwarp();
+      if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
+      rb += wps;
+      while (rb >= nb_run) { rb -= nb_run; ++ao; }
     }
     colweight_fold<LP>(acc, pd.h[D - 1], l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
     if (lane < fold_lanes) {
@@ -644,143 +659,175 @@ __global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, int l0, int 
 }
 
 // ------------------------------------------------------------------------------------
-// K3 vote: one CTA per (prefix, frame).  Word-parallel reverse map (I1): for the row dim
-// rd = D-2 and last dim ld = D-1, E[l][k_rd][w] is the 32-location mask of row-bucket k_rd
-// expanded over last-dim locations 32w..32w+31; each (row, word) then ORs nothing — it adds
-// one mask per loop into bit-sliced counters and compares with mu.
-// smem: bm [L][wpl] | E [L][B_rd][W_last]
+// K3 vote: one CTA per (prefix, frame).  Reverse mapping + accumulation + second stage
+// (Alg. 1 l.11-14; Def. 4; Eq. a_i), evaluated through identity I1
+// (Props. 3-4): abar[i] = sum_l c_l[M_l(i)] with M_l separable per dimension.
+// Word-parallel: for the row dim rd = D-2 and the last dim ld = D-1,
+//   E[l][k_rd][w] = 32-location mask {j : c_l[k_pre, k_rd, M_l,ld(32 w + j)] = 1}
+// (built with one ballot per word), so each (row, word) item costs one shared load per
+// loop plus an AND (mu = L), OR (mu = 1) or a bit-sliced counter add and compare (L10).
+// prefix = i0 for D == 3 (k_pre = M_l,0(i0)); D <= 2: one CTA per frame.
+// smem: bm [L][lw] (this CTA's slice of each loop's bitmap) | E [L][B_rd][W] | sig_rd [L]
 // ------------------------------------------------------------------------------------
+template <int CW, int MODE>      // CW words per item (1, 2, 4); MODE 0: AND, 1: OR, 2: counters
 __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
-                                                   int64_t d0b, int64_t d0e,
+                                                   int64_t d0b, int64_t d0e, int lw,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts) {
-  extern __shared__ float4 smem_f4[];
+  extern __shared__ __align__(16) uint32_t vsm[];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_f4);
   const int ld = D - 1;
-  const int nld = pd.n[ld];
-  const int wlast = nld >> 5;
+  const int nld = pd.n[ld], lga_ld = pd.lga[ld];
+  const int W = nld >> 5;                            // words per row of locations
   const int brd = D >= 2 ? pd.b[D - 2] : 1;
-  uint32_t* E = bm + (size_t)L * wpl;
+  const int blast = pd.blast;
+  uint32_t* bm = vsm;
+  uint32_t* E = bm + (((size_t)L * lw + 3) & ~size_t(3));   // 16-B aligned for uint4 loads
+  int* sig_rd = reinterpret_cast<int*>(E + (size_t)L * brd * W);
   const int64_t frame = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int64_t i0 = d0b + blockIdx.x;              // prefix (D == 3)
+  const int64_t i0 = d0b + blockIdx.x;               // prefix (D == 3)
 
+  // this CTA's slice of every loop's first-stage bitmap
   const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
-  for (int i = tid; i < L * wpl; i += blockDim.x) bm[i] = src[i];
+  const int rowbits = brd * blast;                   // bits of one k_pre slab
+  for (int i = tid; i < L * lw; i += blockDim.x) {
+    int l = i / lw, w = i - l * lw;
+    int start = 0;
+    if (D == 3 && lw < wpl) {
+      const LoopDev& lp = pd.loops[l];
+      int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+      start = (kpre * rowbits) >> 5;
+    }
+    bm[i] = src[(size_t)l * wpl + start + w];
+  }
+  for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
   __syncthreads();
-  // E[l][krd][w]
-  const int nE = L * brd * wlast;
-  for (int it = warp; it < nE; it += nwarps) {
-    int l = it / (brd * wlast), rem = it - l * brd * wlast;
-    int krd = rem / wlast, w = rem - krd * wlast;
+  // E: warp per (l, w); lane j owns location 32 w + j of the last dim
+  for (int it = warp; it < L * W; it += nwarps) {
+    const int l = it / W, w = it - l * W;
     const LoopDev& lp = pd.loops[l];
-    int kpre = 0;
-    if (D == 3) kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-    int ilast = (w << 5) + lane;
-    int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> pd.lga[ld];
-    int64_t flat = ((int64_t)kpre * brd + krd) * pd.blast + klast;
-    uint32_t bit = (bm[(size_t)l * wpl + (flat >> 5)] >> (flat & 31)) & 1u;
-    uint32_t word = __ballot_sync(0xffffffffu, bit);
-    if (lane == 0) E[it] = word;
+    int base = 0;                                    // bit offset of k_pre's slab in bm[l]
+    if (D == 3) {
+      int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+      base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+    }
+    const int ilast = (w << 5) + lane;
+    const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
+    const uint32_t* b = bm + (size_t)l * lw;
+    for (int krd = 0; krd < brd; ++krd) {
+      int flat = base + krd * blast + klast;
+      uint32_t bit = (b[flat >> 5] >> (flat & 31)) & 1u;
+      uint32_t word = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+    }
   }
   __syncthreads();
-  // rows of this CTA
-  int64_t rbeg, rend;
-  int64_t out_base;                                  // word offset of this CTA's first row
+  int64_t rbeg, rend, out_base;
   const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
   const int64_t slab_words = slab_locs >> 5;
-  if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * wlast; }
+  if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * W; }
   else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
   else { rbeg = 0; rend = 1; out_base = 0; }
   const int nrd = D >= 2 ? pd.n[D - 2] : 1;
   const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
-  const int64_t nitems = (rend - rbeg) * wlast;
+  const int chunks = W / CW;
+  const int64_t nitems = (rend - rbeg) * chunks;
   const int mu = pd.mu;
   for (int64_t it = tid; it < nitems; it += blockDim.x) {
-    int64_t ri = it / wlast;
-    int w = (int)(it - ri * wlast);
-    int64_t row = rbeg + ri;
-    uint32_t pl[6] = {0, 0, 0, 0, 0, 0};
-    for (int l = 0; l < L; ++l) {
-      int krd = 0;
-      if (D >= 2) krd = (int)(((int64_t)pd.loops[l].sig[D - 2] * row) & (nrd - 1)) >> lga_rd;
-      uint32_t carry = E[((size_t)l * brd + krd) * wlast + w];
+    const int64_t ri = it / chunks;
+    const int w0 = (int)(it - ri * chunks) * CW;
+    const int64_t row = rbeg + ri;
+    uint32_t acc[CW];
+    uint32_t pl[CW][6];
 #pragma unroll
-      for (int b = 0; b < 6; ++b) {
-        uint32_t t = pl[b] & carry;
-        pl[b] ^= carry;
-        carry = t;
+    for (int c = 0; c < CW; ++c) {
+      acc[c] = MODE == 0 ? 0xffffffffu : 0u;
+#pragma unroll
+      for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
+    }
+    for (int l = 0; l < L; ++l) {
+      const int krd = D >= 2 ? (int)(((int64_t)sig_rd[l] * row) & (nrd - 1)) >> lga_rd : 0;
+      const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
+      uint32_t m[CW];
+      if (CW == 4) {
+        uint4 v = *reinterpret_cast<const uint4*>(e);
+        m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y; m[CW > 2 ? 2 : 0] = v.z; m[CW > 3 ? 3 : 0] = v.w;
+      } else if (CW == 2) {
+        uint2 v = *reinterpret_cast<const uint2*>(e);
+        m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
+      } else {
+        m[0] = e[0];
+      }
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        if (MODE == 0) acc[c] &= m[c];
+        else if (MODE == 1) acc[c] |= m[c];
+        else {
+          uint32_t carry = m[c];
+#pragma unroll
+          for (int b = 0; b < 6; ++b) {
+            uint32_t t = pl[c][b] & carry;
+            pl[c][b] ^= carry;
+            carry = t;
+          }
+        }
       }
     }
-    // bit-sliced compare: count >= mu
-    uint32_t gt = 0u, eq = 0xffffffffu;
+    if (MODE == 2) {                                 // bit-sliced compare: count >= mu
 #pragma unroll
-    for (int b = 5; b >= 0; --b) {
-      if ((mu >> b) & 1) eq &= pl[b];
-      else { gt |= eq & pl[b]; eq &= ~pl[b]; }
+      for (int c = 0; c < CW; ++c) {
+        uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+        for (int b = 5; b >= 0; --b) {
+          if ((mu >> b) & 1) eq &= pl[c][b];
+          else { gt |= eq & pl[c][b]; eq &= ~pl[c][b]; }
+        }
+        acc[c] = gt | eq;
+      }
     }
-    const int64_t widx = out_base + ri * wlast + w;
-    detect[frame * slab_words + widx] = gt | eq;
-    if (counts) {
-      uint8_t* cdst = counts + frame * slab_locs + widx * 32;
-      for (int j = 0; j < 32; ++j) {
-        int c = 0;
+    const int64_t widx = out_base + ri * W + w0;
+    uint32_t* dst = detect + frame * slab_words + widx;
+    if (CW == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(acc[0], acc[CW > 1 ? 1 : 0], acc[CW > 2 ? 2 : 0], acc[CW > 3 ? 3 : 0]);
+    else if (CW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(acc[0], acc[CW > 1 ? 1 : 0]);
+    else dst[0] = acc[0];
+    if (MODE == 2 && counts) {
 #pragma unroll
-        for (int b = 0; b < 6; ++b) c |= ((pl[b] >> j) & 1u) << b;
-        cdst[j] = (uint8_t)c;
+      for (int c = 0; c < CW; ++c) {
+        uint8_t* cdst = counts + frame * slab_locs + (widx + c) * 32;
+        for (int j = 0; j < 32; ++j) {
+          int v = 0;
+#pragma unroll
+          for (int b = 0; b < 6; ++b) v |= ((pl[c][b] >> j) & 1u) << b;
+          cdst[j] = (uint8_t)v;
+        }
       }
     }
   }
 }
 
 // ------------------------------------------------------------------------------------
-// K4 compaction: detection bitmap -> ascending flat indices.
+// K4 compaction: detection bitmap -> ascending flat indices, single pass.  Chunks of
+// kChunkWords words are taken in ticket order (atomic counter), so a chunk's predecessors
+// are always resident or done; each chunk publishes its popcount (flag A) and, once its
+// exclusive prefix is known from a decoupled look-back, its inclusive prefix (flag P).
+// The result is deterministic (positions depend only on the bitmap).
+// state[c]: bits 62-63 flag (0 none, 1 aggregate, 2 inclusive), bits 0-61 value.
 // ------------------------------------------------------------------------------------
 constexpr int kWordsPerThread = (int)(kChunkWords / kThreads);
+constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(kThreads) k_count(const uint32_t* __restrict__ det, int64_t nwords,
-                                                    long long* __restrict__ chunk_counts) {
-  __shared__ int red[kThreads / 32];
-  const int64_t base = (int64_t)blockIdx.x * kChunkWords + (int64_t)threadIdx.x * kWordsPerThread;
-  int c = 0;
-#pragma unroll
-  for (int i = 0; i < kWordsPerThread; ++i) if (base + i < nwords) c += __popc(det[base + i]);
-  for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long s = 0;
-    for (int i = 0; i < kThreads / 32; ++i) s += red[i];
-    chunk_counts[blockIdx.x] = s;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_scan(long long* __restrict__ chunk_counts, int64_t nchunks,
-                                               long long* __restrict__ d_count) {
-  __shared__ long long part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (nchunks + 1023) / 1024;
-  const int64_t b = t * per, e = b + per < nchunks ? b + per : nchunks;
-  long long s = 0;
-  for (int64_t i = b; i < e; ++i) s += chunk_counts[i];
-  part[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    long long run = 0;
-    for (int i = 0; i < 1024; ++i) { long long v = part[i]; part[i] = run; run += v; }
-    *d_count = run;
-  }
-  __syncthreads();
-  long long run = part[t];
-  for (int64_t i = b; i < e; ++i) { long long v = chunk_counts[i]; chunk_counts[i] = run; run += v; }
-}
-
-__global__ void __launch_bounds__(kThreads) k_write(const uint32_t* __restrict__ det, int64_t nwords,
-                                                    const long long* __restrict__ chunk_off,
-                                                    long long* __restrict__ idx, int64_t capacity) {
+__global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict__ det, int64_t nwords,
+                                                      int64_t nchunks, unsigned long long* state,
+                                                      unsigned int* ticket, long long* __restrict__ idx,
+                                                      int64_t capacity, long long* __restrict__ d_count) {
+  __shared__ int s_chunk;
+  __shared__ long long s_prefix;
   __shared__ int wsum[kThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t base = (int64_t)blockIdx.x * kChunkWords + (int64_t)tid * kWordsPerThread;
+  if (tid == 0) s_chunk = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t chunk = s_chunk;
+  const int64_t base = chunk * kChunkWords + (int64_t)tid * kWordsPerThread;
   uint32_t w[kWordsPerThread];
   int c = 0;
 #pragma unroll
@@ -789,15 +836,54 @@ __global__ void __launch_bounds__(kThreads) k_write(const uint32_t* __restrict__
     c += __popc(w[i]);
   }
   int incl = c;
+#pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     int v = __shfl_up_sync(0xffffffffu, incl, off);
     if (lane >= off) incl += v;
   }
   if (lane == 31) wsum[warp] = incl;
   __syncthreads();
-  int wbase = 0;
-  for (int i = 0; i < warp; ++i) wbase += wsum[i];
-  long long pos = chunk_off[blockIdx.x] + wbase + incl - c;
+  int wbase = 0, total = 0;
+  for (int i = 0; i < kThreads / 32; ++i) {
+    if (i < warp) wbase += wsum[i];
+    total += wsum[i];
+  }
+  if (warp == 0) {                                 // warp-parallel decoupled look-back
+    volatile unsigned long long* vs = state;
+    long long excl = 0;
+    if (chunk == 0) {
+      if (lane == 0) atomicExch(&state[0], kFlagP | (unsigned long long)total);
+    } else {
+      if (lane == 0) atomicExch(&state[chunk], kFlagA | (unsigned long long)total);
+      int64_t top = chunk - 1;                       // window: predecessors top, top-1, ...
+      while (true) {
+        const int64_t j = top - lane;
+        const unsigned long long v = j >= 0 ? vs[j] : (2ull << 62);
+        const unsigned long long f = v & ~kValMask;
+        const unsigned pmask = __ballot_sync(0xffffffffu, f == kFlagP);
+        const unsigned zmask = __ballot_sync(0xffffffffu, f == 0);
+        const int plane = pmask ? __ffs(pmask) - 1 : 31;
+        const unsigned need = plane == 31 ? 0xffffffffu : ((2u << plane) - 1u);
+        if (zmask & need) continue;                  // a predecessor has not published yet
+        long long val = lane <= plane ? (long long)(v & kValMask) : 0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
+        excl += val;
+        if (pmask) break;
+        top -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&state[chunk], kFlagP | (unsigned long long)(excl + total));
+      }
+    }
+    if (lane == 0) {
+      s_prefix = excl;
+      if (chunk == nchunks - 1) *d_count = excl + total;
+    }
+  }
+  __syncthreads();
+  long long pos = s_prefix + wbase + incl - c;
 #pragma unroll
   for (int i = 0; i < kWordsPerThread; ++i) {
     uint32_t v = w[i];
@@ -935,18 +1021,39 @@ rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l
   return RSFT_E_UNSUPPORTED;
 }
 
-rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                          uint32_t* det, uint8_t* counts, cudaStream_t st) {
+template <int CW, int MODE>
+static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                                 uint32_t* det, uint8_t* counts, cudaStream_t st) {
   const int D = p->D;
-  const int64_t nld = p->n[D - 1];
+  const int64_t W = p->n[D - 1] / 32;
   const int64_t brd = D >= 2 ? p->b[D - 2] : 1;
-  size_t smem = (size_t)p->L * p->dev.wpl * 4 + (size_t)p->L * brd * (nld / 32) * 4;
-  rsft_status s = check(cudaFuncSetAttribute(k_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  const int64_t wpl = p->dev.wpl;
+  const int64_t rowbits = brd * p->b[D - 1];
+  const int lw = (D == 3 && rowbits % 32 == 0) ? (int)(rowbits / 32) : (int)wpl;
+  size_t smem = (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (size_t)p->L * brd * W * 4 + kMaxLoops * 4;
+  auto kern = k_vote<CW, MODE>;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   dim3 grid(D == 3 ? (unsigned)(d0e - d0b) : 1u, (unsigned)batch);
-  k_vote<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, det, counts);
+  kern<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, det, counts);
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_vote launch");
+}
+
+template <int CW>
+static rsft_status launch_vote_cw(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                                  uint32_t* det, uint8_t* counts, cudaStream_t st) {
+  if (!counts && p->mu == p->L) return launch_vote_t<CW, 0>(p, bm, batch, d0b, d0e, det, counts, st);
+  if (!counts && p->mu == 1) return launch_vote_t<CW, 1>(p, bm, batch, d0b, d0e, det, counts, st);
+  return launch_vote_t<CW, 2>(p, bm, batch, d0b, d0e, det, counts, st);
+}
+
+rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                          uint32_t* det, uint8_t* counts, cudaStream_t st) {
+  const int64_t W = p->n[p->D - 1] / 32;
+  if (W % 4 == 0) return launch_vote_cw<4>(p, bm, batch, d0b, d0e, det, counts, st);
+  if (W % 2 == 0) return launch_vote_cw<2>(p, bm, batch, d0b, d0e, det, counts, st);
+  return launch_vote_cw<1>(p, bm, batch, d0b, d0e, det, counts, st);
 }
 
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
@@ -954,12 +1061,15 @@ rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, i
   const int64_t nwords = batch * ((p->ntot + 31) / 32);
   const int64_t nchunks = (nwords + kChunkWords - 1) / kChunkWords;
   if (nchunks > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;
-  k_count<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, p->dev.chunk_counts);
-  k_scan<<<1, 1024, 0, st>>>(p->dev.chunk_counts, nchunks, reinterpret_cast<long long*>(d_count));
-  k_write<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, p->dev.chunk_counts,
-                                                  reinterpret_cast<long long*>(idx), capacity);
-  p->last_launches += 3;
-  return check(cudaGetLastError(), "compaction launch");
+  unsigned long long* state = reinterpret_cast<unsigned long long*>(p->dev.chunk_counts);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(state + nchunks);
+  rsft_status s = check(cudaMemsetAsync(state, 0, (size_t)(nchunks + 1) * 8, st), "compaction state reset");
+  if (s) return s;
+  k_compact<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, nchunks, state, ticket,
+                                                   reinterpret_cast<long long*>(idx), capacity,
+                                                   reinterpret_cast<long long*>(d_count));
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_compact launch");
 }
 
 rsft_status upload_twiddles(cudaStream_t st) {

@@ -25,6 +25,7 @@ def gpu_run(plan, x_np, spectra=True, counts=True, capacity=None):
     bm = plan.execute(x, spectra=sp)
     ct = torch.empty((batch, plan.ntot), dtype=torch.uint8, device="cuda") if counts else None
     det = plan.detect(bm, counts=ct)
+    det_fast = plan.detect(bm)              # no counts: AND (mu = L) / OR (mu = 1) fast paths
     cap = capacity if capacity is not None else batch * plan.ntot
     idx, cnt = plan.compact(det, cap)
     torch.cuda.synchronize()
@@ -33,6 +34,7 @@ def gpu_run(plan, x_np, spectra=True, counts=True, capacity=None):
         "bm": bm.cpu().numpy(),
         "spectra": sp.cpu().numpy() if sp is not None else None,
         "det": det.cpu().numpy(),
+        "det_fast": det_fast.cpu().numpy(),
         "counts": ct.cpu().numpy() if ct is not None else None,
         "idx": idx.cpu().numpy()[:min(count, cap)],
         "count": count,
@@ -75,6 +77,7 @@ def check_frame(res, f, x, op, tb, loops=None, check_counts=True):
 
 def check_index_list(res, ntot, batch):
     """The compacted list equals the set bits of the detection bitmap, ascending."""
+    np.testing.assert_array_equal(res["det"], res["det_fast"])
     bits = B.bitmap_to_bool(res["det"].reshape(-1), ntot * batch)
     want = np.flatnonzero(bits).astype(np.int64)
     assert res["count"] == want.size

@@ -41,6 +41,9 @@ CASES = [
     ("1d_b64_full", (2048,), (64,), 3, dict(p_fa=1e-3), 2, "fused"),
     ("2d_fused", (128, 128), (16, 8), 6, dict(p_fa=1e-4, random_tau=True), 5, "fused"),
     ("2d_fused_mu", (128, 64), (8, 16), 7, dict(p_fa=1e-3, mu=4), 4, "fused"),
+    ("2d_fused_mu1", (128, 64), (8, 16), 3, dict(p_fa=1e-3, mu=1), 2, "fused"),
+    ("3d_split_mu1", (32, 32, 64), (4, 8, 8), 3, dict(p_fa=1e-3, mu=1), 1, "split"),
+    ("3d_split_nlast32_B32", (16, 64, 32), (4, 8, 32), 4, dict(p_fa=1e-3), 1, "split"),
     ("2d_split_rpw1", (128, 64), (16, 16), 6, dict(p_fa=1e-4), 2, "split"),
     ("2d_split_rpw2", (256, 32), (16, 8), 4, dict(p_fa=1e-4, random_tau=True), 2, "split"),
     ("3d_split", (64, 32, 32), (8, 4, 8), 8, dict(p_fa=1e-5, random_tau=True), 2, "split"),
