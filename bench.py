@@ -334,15 +334,13 @@ def bench_c5(a, wl, rank, world, dev):
     stream = torch.cuda.current_stream()
     plan = B.Plan(wl.n, wl.b, wl.loops, p_fa=wl.p_fa, noise_var=wl.noise_var, seed=wl.sched_seed,
                   mu=wl.mu, max_batch=1).bind()
+    from paper_1610_01050_b200 import shard
     L = wl.loops
-    assert L % world == 0, "loops must divide evenly over ranks"
-    lb, le = rank * L // world, (rank + 1) * L // world
+    lb, le = shard.loop_range(rank, world, L)
     n0 = wl.n[0]
-    d0b, d0e = rank * n0 // world, (rank + 1) * n0 // world
+    d0b, d0e = shard.slab_range(rank, world, n0, plan.ntot // n0)
     x = torch.from_numpy(synth.gen_batch(wl, [0])).to(dev)
     mine = plan.new_bitmaps(1, le - lb)
-    full = plan.new_bitmaps(1)
-    gath = torch.empty((world, le - lb, plan.bitmap_words), dtype=torch.int32, device=dev)
     slab_words = (d0e - d0b) * (plan.ntot // n0) // 32
     det = torch.empty((1, slab_words), dtype=torch.int32, device=dev)
 
@@ -353,12 +351,7 @@ def bench_c5(a, wl, rank, world, dev):
         n = plan.last_launch_count()
         if ev is not None:
             ev[1].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gath, mine[0])
-            full.copy_(gath.reshape(1, L, plan.bitmap_words))
-            src = full
-        else:
-            src = mine
+        src = shard.gather_loop_bitmaps(mine[0], world).reshape(1, L, plan.bitmap_words)
         plan.detect(src, dim0=(d0b, d0e), detect=det)
         n += plan.last_launch_count()
         return n

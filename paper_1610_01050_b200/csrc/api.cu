@@ -55,6 +55,9 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   for (int d = 0; d < p->D; ++d)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.h_off[d], p->hf[d].data(), sizeof(float) * p->hf[d].size(),
                                         cudaMemcpyHostToDevice, st), "upload weights"))) return s;
+  if (!p->xmask.empty() && p->ws.xmask_bytes == p->xmask.size() * 4)
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
+                                        cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
   if ((s = upload_twiddles(st))) return s;
   if ((s = cuda_check(cudaStreamSynchronize(st), "bind sync"))) return s;   // tables are host temporaries
 
@@ -85,6 +88,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.fbuf = reinterpret_cast<float2*>(base + p->ws.fbuf_off);
   pd.chunk_counts = reinterpret_cast<long long*>(base + p->ws.chunk_off);
   pd.chunk_capacity = p->ws.chunk_capacity;
+  pd.xmask = p->ws.xmask_bytes ? reinterpret_cast<const uint32_t*>(base + p->ws.xmask_off) : nullptr;
   p->d_ws = d_ws;
   p->bound = true;
   return RSFT_OK;

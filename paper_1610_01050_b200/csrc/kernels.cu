@@ -189,14 +189,30 @@ __device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* _
   for (int u = 0; u < U; ++u) v[u] = buf[u * 32 + lane];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
+    if constexpr (LP % 4 == 0) {                   // 16-B weight loads (rows are 16-B aligned)
+      const float4* wr = reinterpret_cast<const float4*>(wrow[u]);
 #pragma unroll
-    for (int l2 = 0; l2 < LP / 2; ++l2) {
-      float2 w = wr[l2];
-      mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
-      mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
-      mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
-      mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+      for (int l4 = 0; l4 < LP / 4; ++l4) {
+        float4 w = wr[l4];
+        mac(acc[4 * l4][0], w.x, v[u].x, v[u].y);
+        mac(acc[4 * l4][1], w.x, v[u].z, v[u].w);
+        mac(acc[4 * l4 + 1][0], w.y, v[u].x, v[u].y);
+        mac(acc[4 * l4 + 1][1], w.y, v[u].z, v[u].w);
+        mac(acc[4 * l4 + 2][0], w.z, v[u].x, v[u].y);
+        mac(acc[4 * l4 + 2][1], w.z, v[u].z, v[u].w);
+        mac(acc[4 * l4 + 3][0], w.w, v[u].x, v[u].y);
+        mac(acc[4 * l4 + 3][1], w.w, v[u].z, v[u].w);
+      }
+    } else {
+      const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
+#pragma unroll
+      for (int l2 = 0; l2 < LP / 2; ++l2) {
+        float2 w = wr[l2];
+        mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
+        mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
+        mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
+        mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+      }
     }
   }
 }
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)nwarps * S * U * 32);
   float2* F = reinterpret_cast<float2*>(bars + nwarps * S);
   const int fslot = nl * bouter * fstride;
-  float2* tw = F + (size_t)G * fslot;
+  float2* tw = F + (((size_t)G * fslot + 1) & ~size_t(1));   // keep rowW 16-B aligned
   float* rowW = reinterpret_cast<float*>(tw + 128);
   float4* myring = ring + (size_t)warp * S * U * 32;
   uint64_t* mybar = bars + warp * S;
@@ -455,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __
   float* rw = reinterpret_cast<float*>(sbo + kMaxLoops);
   float2* part = reinterpret_cast<float2*>(rw + (size_t)(RA + 1) * LP);
   float2* R = part + (size_t)nwarps * nl * blast;
+  float* part_scratch = reinterpret_cast<float*>(R + (size_t)nl * (blast + 1));   // h0s/h1s staging
   float4* myring = ring + (size_t)warp * S * U * 32;
   uint64_t* mybar = bars + warp * S;
   load_twiddles(tw);
@@ -462,20 +479,39 @@ __global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __
   int r0, r1 = 0;
   if (D == 3) { r0 = kappa / pd.b[1]; r1 = kappa - r0 * pd.b[1]; } else { r0 = kappa; }
   const int lga1 = D == 3 ? pd.lga[1] : 0;
-  for (int i = tid; i < (RA + 1) * LP; i += blockDim.x) {
-    int q = i / LP, l = i - q * LP;
-    float w = 0.f;
-    if (l < nl && q < RA) {
-      if (D == 3) {
-        int a0 = q >> lga1, a1 = q & (pd.a[1] - 1);
-        int s0 = r0 + pd.b[0] * a0, s1 = r1 + pd.b[1] * a1;
-        w = pd.h[0][(size_t)(l0 + l) * pd.n[0] + s0] * pd.h[1][(size_t)(l0 + l) * pd.n[1] + s1];
-      } else {
-        int s0 = r0 + pd.b[0] * q;
-        w = pd.h[0][(size_t)(l0 + l) * pd.n[0] + s0];
-      }
+  {
+    // stage this class's per-dimension weights (h0[l][r0 + B0 a0], h1[l][r1 + B1 a1]) in
+    // smem with independent loads, then form the row-weight products from smem
+    const int A0 = pd.a[0], A1 = D == 3 ? pd.a[1] : 1;
+    float* h0s = part_scratch;                       // [A0][LP]
+    float* h1s = h0s + LP * A0;                      // [A1][LP]
+    for (int i = tid; i < LP * A0; i += blockDim.x) {
+      int a0 = i / LP, l = i - a0 * LP;
+      h0s[i] = l < nl ? pd.h[0][(size_t)(l0 + l) * pd.n[0] + r0 + pd.b[0] * a0] : 0.f;
     }
-    rw[i] = w;
+    if (D == 3)
+      for (int i = tid; i < LP * A1; i += blockDim.x) {
+        int a1 = i / LP, l = i - a1 * LP;
+        h1s[i] = l < nl ? pd.h[1][(size_t)(l0 + l) * pd.n[1] + r1 + pd.b[1] * a1] : 0.f;
+      }
+    __syncthreads();
+    // rw[q][l] = h0[a0(q)][l] * h1[a1(q)][l], two loops per item (LP is even)
+    for (int i = tid; i < (RA + 1) * (LP / 2); i += blockDim.x) {
+      const int q = i / (LP / 2), l = 2 * (i - q * (LP / 2));
+      float2 w = make_float2(0.f, 0.f);
+      if (q < RA) {
+        if (D == 3) {
+          const int a0 = q >> lga1, a1 = q & (A1 - 1);
+          const float2 x0 = *reinterpret_cast<const float2*>(h0s + a0 * LP + l);
+          const float2 x1 = *reinterpret_cast<const float2*>(h1s + a1 * LP + l);
+          w = make_float2(x0.x * x1.x, x0.y * x1.y);
+        } else {
+          w = *reinterpret_cast<const float2*>(h0s + q * LP + l);
+        }
+      }
+      *reinterpret_cast<float2*>(rw + (size_t)q * LP + l) = w;
+    }
+    __syncthreads();
   }
   {                                                 // zero this frame's bitmap words (K2 ORs bits)
     const int64_t words = (int64_t)nl * pd.wpl;
@@ -702,23 +738,55 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
   }
   for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
   __syncthreads();
-  // E: warp per (l, w); lane j owns location 32 w + j of the last dim
-  for (int it = warp; it < L * W; it += nwarps) {
-    const int l = it / W, w = it - l * W;
-    const LoopDev& lp = pd.loops[l];
-    int base = 0;                                    // bit offset of k_pre's slab in bm[l]
-    if (D == 3) {
-      int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-      base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+  if (pd.xmask) {
+    // E[l][krd][w] = OR over the set bits k of row pattern (k_pre, krd) of X[l][k][w]
+    // (X: plan-constant masks of the last-dim buckets).  Per lane, ~popcount iterations.
+    const int lgW = __ffs(W) - 1;
+    for (int l = 0; l < L; ++l) {
+      int base = 0;
+      if (D == 3) {
+        int kpre = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+        base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+      }
+      const uint32_t* b = bm + (size_t)l * lw;
+      const uint32_t* X = pd.xmask + (size_t)l * blast * W;
+      for (int j = tid; j < brd * W; j += blockDim.x) {
+        const int krd = j >> lgW, w = j & (W - 1);
+        const int f0 = base + krd * blast;
+        uint64_t pat;
+        if (blast <= 32) {
+          pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
+        } else {                                     // blast == 64: two aligned words
+          pat = (uint64_t)b[f0 >> 5] | ((uint64_t)b[(f0 >> 5) + 1] << 32);
+        }
+        uint32_t e = 0;
+        while (pat) {
+          const int k = __ffsll((long long)pat) - 1;
+          pat &= pat - 1;
+          e |= __ldg(X + (size_t)k * W + w);
+        }
+        E[((size_t)l * brd + krd) * W + w] = e;
+      }
     }
-    const int ilast = (w << 5) + lane;
-    const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
-    const uint32_t* b = bm + (size_t)l * lw;
-    for (int krd = 0; krd < brd; ++krd) {
-      int flat = base + krd * blast + klast;
-      uint32_t bit = (b[flat >> 5] >> (flat & 31)) & 1u;
-      uint32_t word = __ballot_sync(0xffffffffu, bit);
-      if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+  } else {
+    // E via ballots: warp per (l, w); lane j owns location 32 w + j of the last dim
+    for (int it = warp; it < L * W; it += nwarps) {
+      const int l = it / W, w = it - l * W;
+      const LoopDev& lp = pd.loops[l];
+      int base = 0;
+      if (D == 3) {
+        int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+        base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+      }
+      const int ilast = (w << 5) + lane;
+      const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
+      const uint32_t* b = bm + (size_t)l * lw;
+      for (int krd = 0; krd < brd; ++krd) {
+        int flat = base + krd * blast + klast;
+        uint32_t bit = (b[flat >> 5] >> (flat & 31)) & 1u;
+        uint32_t word = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+      }
     }
   }
   __syncthreads();
@@ -814,6 +882,7 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
 // state[c]: bits 62-63 flag (0 none, 1 aggregate, 2 inclusive), bits 0-61 value.
 // ------------------------------------------------------------------------------------
 constexpr int kWordsPerThread = (int)(kChunkWords / kThreads);
+constexpr int kStageIdx = 2048;          // indices staged per chunk for coalesced writes
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict__ det, int64_t nwords,
@@ -823,6 +892,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict
   __shared__ int s_chunk;
   __shared__ long long s_prefix;
   __shared__ int wsum[kThreads / 32];
+  __shared__ long long s_idx[kStageIdx];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_chunk = (int)atomicAdd(ticket, 1u);
   __syncthreads();
@@ -830,11 +900,18 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict
   const int64_t base = chunk * kChunkWords + (int64_t)tid * kWordsPerThread;
   uint32_t w[kWordsPerThread];
   int c = 0;
+  if (base + kWordsPerThread <= nwords && ((reinterpret_cast<uintptr_t>(det + base) & 15) == 0)) {
 #pragma unroll
-  for (int i = 0; i < kWordsPerThread; ++i) {
-    w[i] = base + i < nwords ? det[base + i] : 0u;
-    c += __popc(w[i]);
+    for (int i = 0; i < kWordsPerThread; i += 4) {
+      uint4 v = *reinterpret_cast<const uint4*>(det + base + i);
+      w[i] = v.x; w[i + 1] = v.y; w[i + 2] = v.z; w[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kWordsPerThread; ++i) w[i] = base + i < nwords ? det[base + i] : 0u;
   }
+#pragma unroll
+  for (int i = 0; i < kWordsPerThread; ++i) c += __popc(w[i]);
   int incl = c;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -883,15 +960,33 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict
     }
   }
   __syncthreads();
-  long long pos = s_prefix + wbase + incl - c;
+  // indices: staged in smem and written coalesced when the chunk's count fits
+  const long long cbase = s_prefix;
+  if (total <= kStageIdx) {
+    int lp = wbase + incl - c;
 #pragma unroll
-  for (int i = 0; i < kWordsPerThread; ++i) {
-    uint32_t v = w[i];
-    while (v) {
-      int bit = __ffs(v) - 1;
-      v &= v - 1;
-      if (pos < capacity) idx[pos] = (long long)(base + i) * 32 + bit;
-      ++pos;
+    for (int i = 0; i < kWordsPerThread; ++i) {
+      uint32_t v = w[i];
+      while (v) {
+        int bit = __ffs(v) - 1;
+        v &= v - 1;
+        s_idx[lp++] = (long long)(base + i) * 32 + bit;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < total; i += blockDim.x)
+      if (cbase + i < capacity) idx[cbase + i] = s_idx[i];
+  } else {
+    long long pos = cbase + wbase + incl - c;
+#pragma unroll
+    for (int i = 0; i < kWordsPerThread; ++i) {
+      uint32_t v = w[i];
+      while (v) {
+        int bit = __ffs(v) - 1;
+        v &= v - 1;
+        if (pos < capacity) idx[pos] = (long long)(base + i) * 32 + bit;
+        ++pos;
+      }
     }
   }
 }

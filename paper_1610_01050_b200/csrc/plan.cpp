@@ -127,6 +127,24 @@ rsft_status rebuild_tables(rsft_plan_s* p) {
       p->beta[l] *= ss;              // beta = ||Wbar P_sigma w||^2 (Eq. alpha_beta)
     }
   }
+  // Vote expansion masks (identity I1, Def. 3): bit j of X[l][k][w] is set iff location
+  // i = 32 w + j of the last dimension maps to bucket k = floor(B [sigma i]_N / N).
+  {
+    const int ld = D - 1;
+    const int64_t n = p->n[ld], b = p->b[ld], W = n / 32;
+    const size_t bytes = (size_t)L * b * W * 4;
+    p->xmask.clear();
+    if (bytes <= kMaxXmaskBytes) {
+      p->xmask.assign((size_t)L * b * W, 0u);
+      for (int l = 0; l < L; ++l) {
+        const int64_t s = p->sigma[l * D + ld];
+        for (int64_t i = 0; i < n; ++i) {
+          const int64_t k = (int64_t)(((__int128)s * i) % n) * b / n;
+          p->xmask[((size_t)l * b + k) * W + (i >> 5)] |= 1u << (i & 31);
+        }
+      }
+    }
+  }
   for (int l = 0; l < L; ++l)        // Eq. tpd with P~_fa = P_fa per loop (L8)
     p->gamma[l] = p->P.gamma_override > 0 ? p->P.gamma_override
                                           : p->P.noise_var * p->beta[l] * std::log(1.0 / p->P.p_fa);
@@ -156,6 +174,12 @@ void layout_workspace(rsft_plan_s* p) {
   int64_t chunks = (p->P.max_batch * dw + kChunkWords - 1) / kChunkWords;
   w.chunk_capacity = chunks;
   w.chunk_off = off; off = align256(off + sizeof(long long) * (size_t)(chunks + 2));
+  {
+    const int64_t n = p->n[p->D - 1], b = p->b[p->D - 1];
+    w.xmask_bytes = (size_t)p->L * b * (n / 32) * 4;
+    if (w.xmask_bytes > kMaxXmaskBytes) w.xmask_bytes = 0;
+  }
+  w.xmask_off = off; off = align256(off + w.xmask_bytes);
   w.total = off;
 }
 
@@ -168,7 +192,7 @@ size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
   int64_t groups = p->D == 1 ? (nseg < 8 ? nseg : 8) : 1;
   int64_t n0 = p->D == 2 ? p->n[0] : 1;
   size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
-  size_t fbytes = (size_t)groups * nl * bouter * (blast + 1) * 8 + 128 * 8;
+  size_t fbytes = (((size_t)groups * nl * bouter * (blast + 1) + 1) & ~size_t(1)) * 8 + 128 * 8;
   return ring + fbytes + (size_t)(n0 + 1) * lpad * 4;
 }
 
@@ -178,8 +202,9 @@ size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
   int64_t ra = 1;
   for (int d = 0; d + 1 < p->D; ++d) ra *= p->a[d];
   size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
+  int64_t a0 = p->a[0], a1 = p->D == 3 ? p->a[1] : 1;
   return ring + 128 * 8 + kMaxLoops * 4 + (size_t)(ra + 1) * lpad * 4 + (size_t)nwarps * nl * blast * 8 +
-         (size_t)nl * (blast + 1) * 8;
+         (size_t)nl * (blast + 1) * 8 + (size_t)lpad * (a0 + a1) * 4;
 }
 
 int resolve_mode(const rsft_plan_s* p, int64_t batch) {

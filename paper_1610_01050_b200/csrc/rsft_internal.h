@@ -15,7 +15,7 @@ namespace rsft {
 constexpr int kMaxDim = 3;
 constexpr int kMaxLoops = 32;
 constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
-constexpr int64_t kChunkWords = 2048;  // compaction chunk: words of the detection bitmap
+constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detection bitmap
 constexpr int kThreads = 256;          // CTA size of every kernel
 constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
 constexpr int kU = 4;                  // 512 B row slots per ring stage
@@ -49,10 +49,13 @@ struct PlanDev {
   float2* fbuf;                    // split mode intermediate [batch][L][B_tot]
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
+  const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
 };
 
+constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
+
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, total;
+  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, xmask_off, xmask_bytes, total;
   int64_t chunk_capacity;
 };
 
@@ -68,6 +71,7 @@ struct rsft_plan_s {
   std::vector<double> hd[3];                      // fp64 weights [L][N_d]
   std::vector<float> hf[3];                       // fp32 weights [L][N_d]
   std::vector<double> beta, gamma;                // [L]
+  std::vector<uint32_t> xmask;                    // [L][B_last][N_last/32] (may be empty)
   rsft::Workspace ws{};
   // binding
   bool bound = false;

@@ -1,0 +1,84 @@
+"""World-size-2 gloo tests (CPU) of the multi-GPU host logic: frame / loop / slab sharding
+and the all-gather of per-loop bitmaps before voting (BASELINE configs[4]).
+The per-rank first-stage bitmaps come from the oracle (CPU), so the test checks that the
+sharded pipeline reassembles exactly the single-process result."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import rsft_ref as R
+import synth
+from paper_1610_01050_b200 import shard
+
+
+def pack(c):
+    """bool bucket mask -> uint32 words (bit k of word w = flat bucket 32 w + k)."""
+    bits = np.asarray(c, dtype=np.uint8).ravel()
+    pad = (-bits.size) % 32
+    bits = np.concatenate([bits, np.zeros(pad, np.uint8)])
+    return np.packbits(bits, bitorder="little").view(np.uint32).astype(np.int64).astype(np.int32)
+
+
+def unpack(words, n):
+    return np.unpackbits(np.asarray(words, dtype=np.int32).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, b, L = (32, 16, 64), (4, 4, 8), 4
+        p = R.Params(n=n, b=b, loops=L, p_fa=1e-3, seed=17)
+        tb = R.make_tables(p)
+        wl = synth.Workload("mg", n, b, L, 1e-3, 1.0, (3, 6), (5.0, 20.0), 1, data_seed=4)
+        x = synth.gen_frame(wl, 0)
+        lb, le = shard.loop_range(rank, world, L)
+        local = torch.from_numpy(np.stack([pack(R.first_stage(x, p, tb, l).c) for l in range(lb, le)]))
+        full = shard.gather_loop_bitmaps(local, world)
+        cs = [unpack(full[l].numpy(), int(np.prod(b))).reshape(b) for l in range(L)]
+        d0b, d0e = shard.slab_range(rank, world, n[0], n[1] * n[2])
+        abar = R.accumulate(cs, p, tb)
+        mine = (abar >= p.mu)[d0b:d0e]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (d0b, d0e, mine))
+        if rank == 0:
+            ref = R.rsft_run(x, p, tb)
+            det = np.zeros(n, dtype=bool)
+            for bb, ee, m in gathered:
+                det[bb:ee] = m
+            ret["ok"] = bool(np.array_equal(det, ref.detect))
+            ret["bits_ok"] = all(np.array_equal(cs[l], ref.stages[l].c) for l in range(L))
+            ret["frames"] = [shard.frame_range(r, world, 4096) for r in range(world)]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_loop_shard_allgather_vote():
+    world = 2
+    with mp.Manager() as mgr:
+        ret = mgr.dict()
+        mp.spawn(_worker, args=(world, free_port(), ret), nprocs=world, join=True)
+        assert ret["bits_ok"] and ret["ok"]
+        assert ret["frames"] == [(0, 2048), (2048, 4096)]
+
+
+def test_shard_ranges_partition():
+    for world in (1, 2, 4, 8):
+        assert [shard.loop_range(r, world, 16) for r in range(world)] == [(16 // world * r, 16 // world * (r + 1)) for r in range(world)]
+        sl = [shard.slab_range(r, world, 2048, 512 * 64) for r in range(world)]
+        assert sl[0][0] == 0 and sl[-1][1] == 2048 and all(sl[i][1] == sl[i + 1][0] for i in range(world - 1))
+    with pytest.raises(ValueError):
+        shard.loop_range(0, 3, 16)
