@@ -6,8 +6,8 @@ as a fraction of the B200 peak, at 1/2/4/8 GPUs).
                     [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...         (one rank per GPU, NCCL)
 
-A step is one pass of the whole hot path (execute = fused fold+FFT+threshold, detect = vote,
-compact = sorted index list) over one batch of synthetic frames resident in HBM.  Default
+A step is one pass of the whole hot path (execute = fused fold+FFT+threshold; detect_compact =
+vote + second stage + sorted index list) over one batch of synthetic frames resident in HBM.  Default
 workload: c4 (BASELINE configs[3]: 1024x256 complex64 frames, B=32x16, L=6, P_fa=1e-6),
 4096 frames per GPU (weak scaling: frames shard across GPUs, no collective in the data path).
 `--workload c5_cube` runs the single 512 MiB cube with its L=16 loops sharded across ranks
@@ -224,9 +224,7 @@ def main_gpu(a):
         n = plan.last_launch_count()
         if events is not None:
             events[1].record(stream)
-        plan.detect(bm, detect=det)
-        n += plan.last_launch_count()
-        plan.compact(det, cap, idx=idx, count=cnt)
+        plan.detect_compact(bm, cap, detect=det, idx=idx, count=cnt)
         n += plan.last_launch_count()
         return n
 

@@ -155,6 +155,14 @@ rsft_status rsft_detect(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t bat
 rsft_status rsft_compact(rsft_plan_t plan, const uint32_t* d_detect, int64_t batch,
                          int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);
 
+/* Fused second stage + compaction (full dim-0 range): the same detection bitmap as
+ * rsft_detect and the same index list / count as rsft_compact, computed in one kernel when
+ * a vote region fits (regions taken in ticket order, decoupled look-back), else as the two
+ * passes.  Errors: E_ARG, E_STATE, E_WORKSPACE, E_CUDA. */
+rsft_status rsft_detect_compact(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t batch,
+                                uint32_t* d_detect, int64_t* d_idx, int64_t capacity,
+                                int64_t* d_count, void* stream);
+
 /* End-to-end convenience call on HOST buffers (blocking: synchronises `stream`):
  * copies h_x (complex64 [batch][N...], pinned recommended) into d_scratch, runs execute,
  * detect and compact, and copies the count and min(count, capacity) indices back.

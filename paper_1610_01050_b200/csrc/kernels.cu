@@ -173,8 +173,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
   while (!ok) {
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    // suspend-time hint (ns): the warp sleeps until the phase flips instead of spinning
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
   }
 }
 
@@ -705,11 +706,51 @@ __global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, int l0, int 
 // prefix = i0 for D == 3 (k_pre = M_l,0(i0)); D <= 2: one CTA per frame.
 // smem: bm [L][lw] (this CTA's slice of each loop's bitmap) | E [L][B_rd][W] | sig_rd [L]
 // ------------------------------------------------------------------------------------
-template <int CW, int MODE>      // CW words per item (1, 2, 4); MODE 0: AND, 1: OR, 2: counters
+constexpr int kStageIdx = 2048;          // indices staged per CTA for coalesced writes
+
+// Block-wide exclusive scan of one int per thread; returns the prefix, *total = sum.
+__device__ __forceinline__ int block_excl_scan(int c, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0, t = 0;
+  for (int i = 0; i < nw; ++i) {
+    if (i < warp) wbase += wsum[i];
+    t += wsum[i];
+  }
+  *total = t;
+  return wbase + incl - c;
+}
+
+// ------------------------------------------------------------------------------------
+// K3 vote (+ optional fused compaction): one CTA per region (frame, prefix).  Reverse
+// mapping + accumulation + second stage (Alg. 1 l.11-14; Def. 4; Eq. a_i
+// P:416-417), evaluated through identity I1 (Props. 3-4): abar[i] = sum_l
+// c_l[M_l(i)] with M_l separable per dimension.  Word-parallel: for the row dim rd = D-2
+// and the last dim ld = D-1,
+//   E[l][k_rd][w] = 32-location mask {j : c_l[k_pre, k_rd, M_l,ld(32 w + j)] = 1},
+// so each (row, word) item costs one shared load per loop plus an AND (mu = L), OR
+// (mu = 1) or a bit-sliced counter add and compare (L10).  prefix = i0 for D == 3
+// (k_pre = M_l,0(i0)); D <= 2: one region per frame.
+// KMAX > 0: also store this region's detection count (rstate[region]) for the offset scan
+// of rsft_detect_compact (no look-back; k_region_scan + k_region_write follow).
+// smem: bm [L][lw] | E [L][B_rd][W] | sig_rd [32] | X [L][B_last][W]
+// ------------------------------------------------------------------------------------
+template <int CW, int MODE, int KMAX>
 __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
                                                    int64_t d0b, int64_t d0e, int lw,
-                                                   uint32_t* __restrict__ detect, uint8_t* __restrict__ counts) {
+                                                   uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
+                                                   unsigned long long* rstate, unsigned int* ticket,
+                                                   long long* __restrict__ idx, int64_t capacity,
+                                                   long long* __restrict__ d_count, int64_t nregions) {
   extern __shared__ __align__(16) uint32_t vsm[];
+  __shared__ int wsum[kThreads / 32];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
   const int ld = D - 1;
   const int nld = pd.n[ld], lga_ld = pd.lga[ld];
@@ -718,10 +759,11 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
   const int blast = pd.blast;
   uint32_t* bm = vsm;
   uint32_t* E = bm + (((size_t)L * lw + 3) & ~size_t(3));   // 16-B aligned for uint4 loads
-  int* sig_rd = reinterpret_cast<int*>(E + (size_t)L * brd * W);
-  const int64_t frame = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int64_t i0 = d0b + blockIdx.x;               // prefix (D == 3)
+  int* sig_rd = reinterpret_cast<int*>(E + (((size_t)L * brd * W + 3) & ~size_t(3)));
+  uint32_t* Xs = reinterpret_cast<uint32_t*>(sig_rd + kMaxLoops);   // [L][B_last][W] masks
+  const int tid = threadIdx.x;
+  const int64_t frame = blockIdx.y, prefix = blockIdx.x;
+  const int64_t i0 = d0b + prefix;                  // prefix (D == 3)
 
   // this CTA's slice of every loop's first-stage bitmap
   const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
@@ -737,6 +779,15 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
     bm[i] = src[(size_t)l * wpl + start + w];
   }
   for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
+  if (pd.xmask) {
+    const int nx = L * blast * W;
+    if ((nx & 3) == 0) {
+      for (int i = tid; i < (nx >> 2); i += blockDim.x)
+        reinterpret_cast<uint4*>(Xs)[i] = __ldg(reinterpret_cast<const uint4*>(pd.xmask) + i);
+    } else {
+      for (int i = tid; i < nx; i += blockDim.x) Xs[i] = __ldg(pd.xmask + i);
+    }
+  }
   __syncthreads();
   if (pd.xmask) {
     // E[l][krd][w] = OR over the set bits k of row pattern (k_pre, krd) of X[l][k][w]
@@ -749,27 +800,29 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
         base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
       }
       const uint32_t* b = bm + (size_t)l * lw;
-      const uint32_t* X = pd.xmask + (size_t)l * blast * W;
+      const uint32_t* X = Xs + (size_t)l * blast * W;
       for (int j = tid; j < brd * W; j += blockDim.x) {
         const int krd = j >> lgW, w = j & (W - 1);
         const int f0 = base + krd * blast;
-        uint64_t pat;
-        if (blast <= 32) {
-          pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
-        } else {                                     // blast == 64: two aligned words
-          pat = (uint64_t)b[f0 >> 5] | ((uint64_t)b[(f0 >> 5) + 1] << 32);
-        }
         uint32_t e = 0;
-        while (pat) {
-          const int k = __ffsll((long long)pat) - 1;
-          pat &= pat - 1;
-          e |= __ldg(X + (size_t)k * W + w);
+        if (blast <= 32) {
+          uint32_t pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
+          while (pat) {
+            const int k = __ffs(pat) - 1;
+            pat &= pat - 1;
+            e |= X[k * W + w];
+          }
+        } else {                                     // blast == 64: two aligned words
+          uint32_t lo = b[f0 >> 5], hi = b[(f0 >> 5) + 1];
+          while (lo) { const int k = __ffs(lo) - 1; lo &= lo - 1; e |= X[k * W + w]; }
+          while (hi) { const int k = __ffs(hi) + 31; hi &= hi - 1; e |= X[k * W + w]; }
         }
         E[((size_t)l * brd + krd) * W + w] = e;
       }
     }
   } else {
     // E via ballots: warp per (l, w); lane j owns location 32 w + j of the last dim
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int it = warp; it < L * W; it += nwarps) {
       const int l = it / W, w = it - l * W;
       const LoopDev& lp = pd.loops[l];
@@ -801,11 +854,12 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
   const int chunks = W / CW;
   const int64_t nitems = (rend - rbeg) * chunks;
   const int mu = pd.mu;
-  for (int64_t it = tid; it < nitems; it += blockDim.x) {
+
+  // one item = CW consecutive detection words of one row
+  auto vote_item = [&](int64_t it, uint32_t (&acc)[CW]) {
     const int64_t ri = it / chunks;
     const int w0 = (int)(it - ri * chunks) * CW;
     const int64_t row = rbeg + ri;
-    uint32_t acc[CW];
     uint32_t pl[CW][6];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
@@ -814,7 +868,8 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
       for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
     }
     for (int l = 0; l < L; ++l) {
-      const int krd = D >= 2 ? (int)(((int64_t)sig_rd[l] * row) & (nrd - 1)) >> lga_rd : 0;
+      // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
+      const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
       const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
       uint32_t m[CW];
       if (CW == 4) {
@@ -826,9 +881,10 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
       } else {
         m[0] = e[0];
       }
+      uint32_t any = 0;
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        if (MODE == 0) acc[c] &= m[c];
+        if (MODE == 0) { acc[c] &= m[c]; any |= acc[c]; }
         else if (MODE == 1) acc[c] |= m[c];
         else {
           uint32_t carry = m[c];
@@ -840,6 +896,7 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
           }
         }
       }
+      if (MODE == 0 && any == 0) break;              // unanimity already impossible
     }
     if (MODE == 2) {                                 // bit-sliced compare: count >= mu
 #pragma unroll
@@ -870,6 +927,132 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
         }
       }
     }
+  };
+
+  int cnt = 0;
+  for (int64_t it = tid; it < nitems; it += blockDim.x) {
+    uint32_t acc[CW];
+    vote_item(it, acc);
+    if (KMAX > 0) {
+#pragma unroll
+      for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+    }
+  }
+  if (KMAX > 0) {                                    // this region's detection count
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if ((tid & 31) == 0) wsum[tid >> 5] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      long long t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
+      rstate[frame * gridDim.x + prefix] = (unsigned long long)t;
+    }
+  }
+}
+
+// Exclusive scan of the per-region detection counts (one CTA); total -> *d_count.
+__global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __restrict__ counts, int64_t n,
+                                                      long long* __restrict__ d_count) {
+  __shared__ long long part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = t * per, e = b + per < n ? b + per : n;
+  long long s = 0;
+  for (int64_t i = b; i < e; ++i) s += (long long)counts[i];
+  // block exclusive scan of part[] (Hillis-Steele in shared memory)
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    long long v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  long long run = part[t] - s;
+  if (t == 1023) *d_count = part[t];
+  for (int64_t i = b; i < e; ++i) { long long v = (long long)counts[i]; counts[i] = (unsigned long long)run; run += v; }
+}
+
+// One CTA per region: load up to 8 tiles of 4 words per thread at once (all loads in
+// flight), scan in (tile, thread) order = word order with one barrier, write ascending
+// indices at the region's offset (staged in smem for coalesced stores).
+constexpr int kWT = 8;                     // tiles per pass
+
+__global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __restrict__ det, int64_t rwords,
+                                                           const unsigned long long* __restrict__ offsets,
+                                                           long long* __restrict__ idx, int64_t capacity) {
+  __shared__ int wsk[kWT * 32];
+  __shared__ long long s_idx[kStageIdx];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t r = blockIdx.x;
+  const uint32_t* src = det + r * rwords;
+  long long run = (long long)offsets[r];
+  const bool vec = (rwords & 3) == 0;
+  const int64_t tile = 4 * (int64_t)blockDim.x;
+  for (int64_t p0 = 0; p0 < rwords; p0 += kWT * tile) {
+    uint32_t w[kWT][4];
+#pragma unroll
+    for (int k = 0; k < kWT; ++k) {
+      const int64_t w0 = p0 + k * tile + 4 * (int64_t)tid;
+      if (vec && w0 + 3 < rwords) {
+        uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + w0));
+        w[k][0] = v.x; w[k][1] = v.y; w[k][2] = v.z; w[k][3] = v.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[k][c] = w0 + c < rwords ? src[w0 + c] : 0u;
+      }
+    }
+    int cnt[kWT], incl[kWT];
+#pragma unroll
+    for (int k = 0; k < kWT; ++k) {
+      cnt[k] = __popc(w[k][0]) + __popc(w[k][1]) + __popc(w[k][2]) + __popc(w[k][3]);
+      incl[k] = cnt[k];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl[k], off);
+        if (lane >= off) incl[k] += v;
+      }
+      if (lane == 31) wsk[k * 32 + warp] = incl[k];
+    }
+    __syncthreads();
+    int total = 0;
+    int off_k[kWT];
+#pragma unroll
+    for (int k = 0; k < kWT; ++k) {
+      int before = 0, rt = 0;
+      for (int w2 = 0; w2 < nw; ++w2) {
+        const int v = wsk[k * 32 + w2];
+        if (w2 < warp) before += v;
+        rt += v;
+      }
+      off_k[k] = total + before + incl[k] - cnt[k];
+      total += rt;
+    }
+    const bool staged = total <= kStageIdx;
+#pragma unroll
+    for (int k = 0; k < kWT; ++k) {
+      const int64_t w0 = p0 + k * tile + 4 * (int64_t)tid;
+      int lp = off_k[k];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v = w[k][c];
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          const long long g = (r * rwords + w0 + c) * 32 + bit;
+          if (staged) s_idx[lp] = g;
+          else if (run + lp < capacity) idx[run + lp] = g;
+          ++lp;
+        }
+      }
+    }
+    __syncthreads();
+    if (staged)
+      for (int i = tid; i < total; i += blockDim.x)
+        if (run + i < capacity) idx[run + i] = s_idx[i];
+    run += total;
+    __syncthreads();
   }
 }
 
@@ -882,7 +1065,6 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
 // state[c]: bits 62-63 flag (0 none, 1 aggregate, 2 inclusive), bits 0-61 value.
 // ------------------------------------------------------------------------------------
 constexpr int kWordsPerThread = (int)(kChunkWords / kThreads);
-constexpr int kStageIdx = 2048;          // indices staged per chunk for coalesced writes
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict__ det, int64_t nwords,
@@ -1116,39 +1298,75 @@ rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l
   return RSFT_E_UNSUPPORTED;
 }
 
-template <int CW, int MODE>
+static int64_t vote_regions_per_frame(const rsft_plan_s* p, int64_t d0b, int64_t d0e) {
+  return p->D == 3 ? d0e - d0b : 1;
+}
+
+template <int CW, int MODE, int KMAX>
 static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                                 uint32_t* det, uint8_t* counts, cudaStream_t st) {
+                                 uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
+                                 int64_t* d_count, cudaStream_t st) {
   const int D = p->D;
   const int64_t W = p->n[D - 1] / 32;
   const int64_t brd = D >= 2 ? p->b[D - 2] : 1;
   const int64_t wpl = p->dev.wpl;
   const int64_t rowbits = brd * p->b[D - 1];
   const int lw = (D == 3 && rowbits % 32 == 0) ? (int)(rowbits / 32) : (int)wpl;
-  size_t smem = (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (size_t)p->L * brd * W * 4 + kMaxLoops * 4;
-  auto kern = k_vote<CW, MODE>;
+  size_t smem = (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (((size_t)p->L * brd * W + 3) & ~size_t(3)) * 4 +
+                kMaxLoops * 4 + p->ws.xmask_bytes;
+  auto kern = k_vote<CW, MODE, KMAX>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
-  dim3 grid(D == 3 ? (unsigned)(d0e - d0b) : 1u, (unsigned)batch);
-  kern<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, det, counts);
+  const int64_t np = vote_regions_per_frame(p, d0b, d0e);
+  const int64_t nregions = np * batch;
+  unsigned long long* rstate = p->dev.region_state;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(rstate + nregions);
+  if (KMAX > 0 && nregions > p->dev.region_capacity) return RSFT_E_WORKSPACE;
+  dim3 grid((unsigned)np, (unsigned)batch);
+  kern<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, det, counts, rstate, ticket,
+                                     reinterpret_cast<long long*>(idx), capacity,
+                                     reinterpret_cast<long long*>(d_count), nregions);
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_vote launch");
 }
 
-template <int CW>
+template <int CW, int KMAX>
+static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                                    uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
+                                    int64_t* d_count, cudaStream_t st) {
+  if (!counts && p->mu == p->L) return launch_vote_t<CW, 0, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+  if (!counts && p->mu == 1) return launch_vote_t<CW, 1, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+  return launch_vote_t<CW, 2, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+}
+
+template <int KMAX>
 static rsft_status launch_vote_cw(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                                  uint32_t* det, uint8_t* counts, cudaStream_t st) {
-  if (!counts && p->mu == p->L) return launch_vote_t<CW, 0>(p, bm, batch, d0b, d0e, det, counts, st);
-  if (!counts && p->mu == 1) return launch_vote_t<CW, 1>(p, bm, batch, d0b, d0e, det, counts, st);
-  return launch_vote_t<CW, 2>(p, bm, batch, d0b, d0e, det, counts, st);
+                                  uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
+                                  int64_t* d_count, cudaStream_t st) {
+  const int64_t W = p->n[p->D - 1] / 32;
+  if (W % 4 == 0) return launch_vote_mode<4, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+  if (W % 2 == 0) return launch_vote_mode<2, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+  return launch_vote_mode<1, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
 }
 
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st) {
-  const int64_t W = p->n[p->D - 1] / 32;
-  if (W % 4 == 0) return launch_vote_cw<4>(p, bm, batch, d0b, d0e, det, counts, st);
-  if (W % 2 == 0) return launch_vote_cw<2>(p, bm, batch, d0b, d0e, det, counts, st);
-  return launch_vote_cw<1>(p, bm, batch, d0b, d0e, det, counts, st);
+  return launch_vote_cw<0>(p, bm, batch, d0b, d0e, det, counts, nullptr, 0, nullptr, st);
+}
+
+rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
+                                  int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st) {
+  const int64_t n0 = p->n[0];
+  rsft_status s = launch_vote_cw<1>(p, bm, batch, 0, n0, det, nullptr, nullptr, 0, nullptr, st);
+  if (s) return s;
+  const int64_t np = vote_regions_per_frame(p, 0, n0);
+  const int64_t nregions = np * batch;
+  const int64_t rwords = ((p->ntot + 31) / 32) / np;
+  k_region_scan<<<1, 1024, 0, st>>>(p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count));
+  k_region_write<<<(unsigned)nregions, kThreads, 0, st>>>(det, rwords, p->dev.region_state,
+                                                          reinterpret_cast<long long*>(idx), capacity);
+  p->last_launches += 2;
+  return check(cudaGetLastError(), "region scan/write launch");
 }
 
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,

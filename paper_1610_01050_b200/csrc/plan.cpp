@@ -180,6 +180,8 @@ void layout_workspace(rsft_plan_s* p) {
     if (w.xmask_bytes > kMaxXmaskBytes) w.xmask_bytes = 0;
   }
   w.xmask_off = off; off = align256(off + w.xmask_bytes);
+  w.region_capacity = p->P.max_batch * (p->D == 3 ? p->n[0] : 1) + 2;
+  w.region_off = off; off = align256(off + 8 * (size_t)w.region_capacity);
   w.total = off;
 }
 

@@ -50,12 +50,15 @@ struct PlanDev {
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
   const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
+  unsigned long long* region_state; // fused vote+compaction look-back state (+ ticket)
+  int64_t region_capacity;
 };
 
 constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, xmask_off, xmask_bytes, total;
+  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, xmask_off, xmask_bytes, region_off, total;
+  int64_t region_capacity;
   int64_t chunk_capacity;
 };
 

@@ -68,6 +68,8 @@ def lib():
         "rsft_execute": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
         "rsft_detect": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
         "rsft_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
+        "rsft_detect_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
+                                          c_void_p]),
         "rsft_host_scratch_bytes": (c_size_t, [c_void_p, c_int64, c_int64]),
         "rsft_run_host": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, P(c_int64), c_void_p,
                                     c_size_t, c_void_p]),
@@ -86,6 +88,7 @@ def lib():
 EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsft_set_schedule",
             "rsft_get_schedule", "rsft_get_thresholds", "rsft_get_window", "rsft_get_info",
             "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_detect", "rsft_compact",
+            "rsft_detect_compact",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
             "rsft_last_error"]
 
@@ -250,6 +253,22 @@ class Plan:
         _check(lib().rsft_compact(self._h, c_void_p(detect.data_ptr()), batch, c_void_p(idx.data_ptr()),
                                   capacity, c_void_p(count.data_ptr()), _stream_handle(stream)))
         return idx, count
+
+    def detect_compact(self, bitmaps, capacity, detect=None, idx=None, count=None, stream=None):
+        """Second stage + compaction in one call (full range): (detect, idx, count)."""
+        import torch
+        self._need_bind()
+        batch = bitmaps.shape[0]
+        if detect is None:
+            detect = torch.empty((batch, self.detect_words), dtype=torch.int32, device=self.device)
+        if idx is None:
+            idx = torch.empty(max(capacity, 1), dtype=torch.int64, device=self.device)
+        if count is None:
+            count = torch.empty(1, dtype=torch.int64, device=self.device)
+        _check(lib().rsft_detect_compact(self._h, c_void_p(bitmaps.data_ptr()), batch, c_void_p(detect.data_ptr()),
+                                         c_void_p(idx.data_ptr()), capacity, c_void_p(count.data_ptr()),
+                                         _stream_handle(stream)))
+        return detect, idx, count
 
     def host_scratch_bytes(self, batch, capacity):
         return lib().rsft_host_scratch_bytes(self._h, batch, capacity)
