@@ -107,8 +107,8 @@ __device__ __forceinline__ void mac(float2& acc, float w, float vx, float vy) {
 // mod B_last/2 share residues and are summed with xor shuffles.  After the call lanes
 // < max(B_last/2,1) hold residue sums for residues 2*lane + e (e < min(B_last,2)).
 template <int LP>
-__device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float* __restrict__ hlast,
-                                               int l0, int nl, int nlast, int col, int blast) {
+__device__ __forceinline__ void colweight(float2 (&acc)[LP][2], const float* __restrict__ hlast,
+                                          int l0, int nl, int nlast, int col) {
 #pragma unroll
   for (int l = 0; l < LP; ++l) {
     float2 hc = make_float2(0.f, 0.f);
@@ -116,6 +116,10 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
     acc[l][0].x *= hc.x; acc[l][0].y *= hc.x;
     acc[l][1].x *= hc.y; acc[l][1].y *= hc.y;
   }
+}
+
+template <int LP>
+__device__ __forceinline__ void lane_fold(float2 (&acc)[LP][2], int blast) {
   for (int off = blast >= 2 ? blast / 2 : 1; off < 32; off <<= 1) {
 #pragma unroll
     for (int l = 0; l < LP; ++l)
@@ -129,6 +133,13 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
 #pragma unroll
     for (int l = 0; l < LP; ++l) acc[l][0] = cadd(acc[l][0], acc[l][1]);
   }
+}
+
+template <int LP>
+__device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float* __restrict__ hlast,
+                                               int l0, int nl, int nlast, int col, int blast) {
+  colweight<LP>(acc, hlast, l0, nl, nlast, col);
+  lane_fold<LP>(acc, blast);
 }
 
 // ------------------------------------------------------------------------------------
@@ -304,11 +315,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
     for (int j = 0; j < S - 1; ++j) issue_next();
   int c_st = 0;
   uint32_t c_ph = 0;
+  float2 racc[LP][2];                              // per-lane residue sums of one class
   for (int64_t fi = 0; fi < nfr; ++fi) {
     const int64_t frame = blockIdx.x + fi * gridDim.x;
     for (int unit = 0; unit < units; ++unit) {
       if (D == 2) {
         const int kappa = warp + (unit >> lg_spt) * nwarps, seg = unit & (spt - 1);
+        if (seg == 0) {
+#pragma unroll
+          for (int l = 0; l < LP; ++l) racc[l][0] = racc[l][1] = make_float2(0.f, 0.f);
+        }
         float2 acc[LP][2];
 #pragma unroll
         for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
@@ -323,16 +339,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
           __syncwarp();
           if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
         }
-        colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane, blast);
-        if (lane < fold_lanes) {
-          float2* slot = F + kappa * fstride + 2 * lane;
+        // column weights per segment; the lanes' residues are the same for every segment,
+        // so segments accumulate per lane and the cross-lane fold runs once per class
+        colweight<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane);
 #pragma unroll
-          for (int l = 0; l < LP; ++l)
-            if (l < nl)
-              for (int e = 0; e < fold_e; ++e) {
-                float2* dst = slot + (size_t)l * bouter * fstride + e;
-                *dst = seg == 0 ? acc[l][e] : cadd(*dst, acc[l][e]);
-              }
+        for (int l = 0; l < LP; ++l) {
+          racc[l][0] = cadd(racc[l][0], acc[l][0]);
+          racc[l][1] = cadd(racc[l][1], acc[l][1]);
+        }
+        if (seg == spt - 1) {
+          lane_fold<LP>(racc, blast);
+          if (lane < fold_lanes) {
+            float2* slot = F + kappa * fstride + 2 * lane;
+#pragma unroll
+            for (int l = 0; l < LP; ++l)
+              if (l < nl)
+                for (int e = 0; e < fold_e; ++e) slot[(size_t)l * bouter * fstride + e] = racc[l][e];
+          }
         }
       } else {
         const int g = warp + unit * nwarps;
@@ -458,7 +481,7 @@ template <int LP, int U>
 __global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
                                                          int l0, int nl, uint32_t* __restrict__ bitmaps) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int S = kStages;
+  constexpr int S = kStagesSplit;
   const int D = pd.D;
   const int kappa = blockIdx.x;
   const int64_t frame = blockIdx.y;
@@ -1210,13 +1233,13 @@ static rsft_status make_map(CUtensorMap* m, const void* base, int rank, const cu
 
 // Map for the fold kernels: D >= 2 -> [N_last][B_o][A_o][planes] (B_o, A_o of the innermost
 // outer dim, planes = batch (D == 2) or batch * N_0 (D == 3)); D == 1 -> [64][N/64][batch].
-static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, CUtensorMap* m) {
+static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, CUtensorMap* m, int u) {
   const int D = p->D;
   const uint64_t e = 8;
   if (D == 1) {
     cuuint64_t dims[3] = {64, (cuuint64_t)(p->n[0] / 64), (cuuint64_t)batch};
     cuuint64_t str[2] = {64 * e, (cuuint64_t)p->n[0] * e};
-    cuuint32_t box[3] = {64, (cuuint32_t)kU, 1};
+    cuuint32_t box[3] = {64, (cuuint32_t)u, 1};
     return make_map(m, d_x, 3, dims, str, box);
   }
   const int64_t nl = p->n[D - 1], no = p->n[D - 2], bo = p->b[D - 2], ao = p->a[D - 2];
@@ -1224,7 +1247,7 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
   const int64_t rpw = nl >= 64 ? 1 : 64 / nl;
   cuuint64_t dims[4] = {(cuuint64_t)nl, (cuuint64_t)bo, (cuuint64_t)ao, (cuuint64_t)planes};
   cuuint64_t str[3] = {(cuuint64_t)(nl * e), (cuuint64_t)(bo * nl * e), (cuuint64_t)(no * nl * e)};
-  cuuint32_t box[4] = {(cuuint32_t)(nl >= 64 ? 64 : nl), 1, (cuuint32_t)(kU * rpw), 1};
+  cuuint32_t box[4] = {(cuuint32_t)(nl >= 64 ? 64 : nl), 1, (cuuint32_t)(u * rpw), 1};
   return make_map(m, d_x, 4, dims, str, box);
 }
 
@@ -1234,7 +1257,7 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
   auto kern = k_fused<LP, kU>;
   const size_t smem = fused_smem_bytes(p, nl, LP);
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, &tmap);
+  rsft_status s = fold_map(p, d_x, batch, &tmap, kU);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
@@ -1252,12 +1275,12 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
 template <int LP>
 static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                   uint32_t* bm, void* spectra, cudaStream_t st) {
-  auto kern = k_split_fold<LP, kU>;
+  auto kern = k_split_fold<LP, kUSplit>;
   const int D = p->D;
   const int64_t blast = p->b[D - 1];
   const size_t smem = split_smem_bytes(p, nl, LP);
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, &tmap);
+  rsft_status s = fold_map(p, d_x, batch, &tmap, kUSplit);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;

@@ -203,7 +203,7 @@ size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
   int64_t blast = p->b[p->D - 1];
   int64_t ra = 1;
   for (int d = 0; d + 1 < p->D; ++d) ra *= p->a[d];
-  size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
+  size_t ring = (size_t)nwarps * kStagesSplit * kUSplit * 512 + (size_t)nwarps * kStagesSplit * 8;
   int64_t a0 = p->a[0], a1 = p->D == 3 ? p->a[1] : 1;
   return ring + 128 * 8 + kMaxLoops * 4 + (size_t)(ra + 1) * lpad * 4 + (size_t)nwarps * nl * blast * 8 +
          (size_t)nl * (blast + 1) * 8 + (size_t)lpad * (a0 + a1) * 4;

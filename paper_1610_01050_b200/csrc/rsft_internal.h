@@ -19,6 +19,8 @@ constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detecti
 constexpr int kThreads = 256;          // CTA size of every kernel
 constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
 constexpr int kU = 4;                  // 512 B row slots per ring stage
+constexpr int kStagesSplit = 2;        // split-mode fold: 2 stages of ...
+constexpr int kUSplit = 8;             // ... 8 slots (4 KiB TMA boxes)
 
 // Per-loop device record: schedule + threshold (Def. 1; Eq. tpd).
 struct LoopDev {
