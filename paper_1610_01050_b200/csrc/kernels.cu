@@ -90,6 +90,34 @@ __device__ __noinline__ void fft_axis(float2* A, const View v, int a, const floa
   }
 }
 
+// Stage-parallel radix-2 DIT along one axis with a closed-form line decomposition:
+// the axis has 2^lgn points `sa` apart (bit-reversed input, natural output); line r of
+// nlines starts at (r >> sh) * hs + (r & ((1 << sh) - 1)) * ls.  One barrier per stage.
+__device__ __noinline__ void fft_axis_fast(float2* A, int lgn, int sa, int nlines, int sh, int hs, int ls,
+                                           const float2* __restrict__ tw) {
+  if (lgn == 0) return;
+  const int nbf = nlines << (lgn - 1);
+  const int lmask = (1 << sh) - 1;
+  for (int s = 1; s <= lgn; ++s) {
+    const int hm = (1 << (s - 1)) - 1;
+    const int gm = (1 << (lgn - s)) - 1;
+    const int half = 1 << (s - 1);
+    for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
+      const int j = bf & hm;
+      const int g = (bf >> (s - 1)) & gm;
+      const int r = bf >> (lgn - 1);
+      const int off = (r >> sh) * hs + (r & lmask) * ls;
+      float2* e0 = A + off + ((g << s) + j) * sa;
+      float2* e1 = e0 + half * sa;
+      const float2 u = *e0;
+      const float2 t = cmul(tw[j << (7 - s)], *e1);
+      *e0 = cadd(u, t);
+      *e1 = csub(u, t);
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void load_twiddles(float2* tw) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
 }
@@ -442,13 +470,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
       }
     }
     {
-      View vw;
-      vw.k = 3;
-      vw.n[0] = nl; vw.lg[0] = 0; vw.st[0] = bouter * fstride;
-      vw.n[1] = bouter; vw.lg[1] = D == 2 ? pd.lgb[0] : 0; vw.st[1] = fstride;
-      vw.n[2] = blast; vw.lg[2] = pd.lgb[D - 1]; vw.st[2] = 1;
-      fft_axis(F, vw, 2, tw);
-      if (D == 2) fft_axis(F, vw, 1, tw);
+      // F is [nl][bouter][fstride]: last-dim lines r = (l, bo) start at r * fstride; dim-0
+      // lines r = (l, k_last) start at (r >> lg B_last) * bouter * fstride + (r & (B_last-1))
+      const int lgbl = pd.lgb[D - 1];
+      fft_axis_fast(F, lgbl, 1, nl * bouter, 0, fstride, 0, tw);
+      if (D == 2) fft_axis_fast(F, pd.lgb[0], fstride, nl * blast, lgbl, bouter * fstride, 1, tw);
     }
     // |fhat|^2 > gamma_l -> ballot -> bitmap words (Alg. 1 l.10)
     const int wpl = pd.wpl;
