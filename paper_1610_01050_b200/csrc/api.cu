@@ -57,6 +57,18 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   for (int d = 0; d < p->D; ++d)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.h_off[d], p->hf[d].data(), sizeof(float) * p->hf[d].size(),
                                         cudaMemcpyHostToDevice, st), "upload weights"))) return s;
+  static thread_local std::vector<float> ht;
+  for (int d = 0; d + 1 < p->D; ++d) {            // ht[r][a][l] = h[l][r + B a] (class-major)
+    const int64_t n = p->n[d], b = p->b[d], a = n / b, L = p->L;
+    ht.assign((size_t)L * n, 0.f);
+    for (int64_t l = 0; l < L; ++l)
+      for (int64_t sidx = 0; sidx < n; ++sidx) ht[((sidx % b) * a + sidx / b) * L + l] = p->hf[d][l * n + sidx];
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.ht_off[d], ht.data(), sizeof(float) * ht.size(),
+                                        cudaMemcpyHostToDevice, st), "upload class-major weights"))) return s;
+  }
+  if (p->ws.cnt_capacity)
+    if ((s = cuda_check(cudaMemsetAsync(base + p->ws.cnt_off, 0, 4 * (size_t)p->ws.cnt_capacity, st), "zero counters")))
+      return s;
   if (!p->xmask.empty() && p->ws.xmask_bytes == p->xmask.size() * 4)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
                                         cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
@@ -75,6 +87,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
     pd.lgn[d] = ilog2i(n); pd.lgb[d] = ilog2i(b); pd.lga[d] = ilog2i(n / b);
     pd.shift[d] = (d < p->D && b < n) ? 1 : 0;
     pd.h[d] = d < p->D ? reinterpret_cast<const float*>(base + p->ws.h_off[d]) : nullptr;
+    pd.ht[d] = d + 1 < p->D ? reinterpret_cast<const float*>(base + p->ws.ht_off[d]) : nullptr;
   }
   pd.ntot = p->ntot;
   pd.btot = p->btot;
@@ -88,6 +101,10 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.aouter = (int32_t)aouter;
   pd.loops = reinterpret_cast<const LoopDev*>(base + p->ws.loops_off);
   pd.fbuf = reinterpret_cast<float2*>(base + p->ws.fbuf_off);
+  pd.parts = reinterpret_cast<float2*>(base + p->ws.parts_off);
+  pd.parts_capacity = (int64_t)(p->ws.parts_bytes / 8);
+  pd.class_cnt = reinterpret_cast<unsigned*>(base + p->ws.cnt_off);
+  pd.class_capacity = p->ws.cnt_capacity;
   pd.chunk_counts = reinterpret_cast<long long*>(base + p->ws.chunk_off);
   pd.chunk_capacity = p->ws.chunk_capacity;
   pd.xmask = p->ws.xmask_bytes ? reinterpret_cast<const uint32_t*>(base + p->ws.xmask_off) : nullptr;

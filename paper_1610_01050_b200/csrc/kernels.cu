@@ -122,12 +122,10 @@ __device__ __forceinline__ void load_twiddles(float2* tw) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
 }
 
-// acc += w * v for a complex pair v: one complex x real MAC as a single packed
-// fma.rn.f32x2 (SASS: FFMA2 R, R.F32, R.F32x2, R.F32x2 on sm_100a).
+// acc += w * v for a complex pair v: one complex x real MAC as a single packed FMA
+// (__ffma2_rn -> SASS FFMA2 R, R.F32, R.F32x2, R.F32x2 on sm_100a).
 __device__ __forceinline__ void mac(float2& acc, float w, float vx, float vy) {
-  asm("{\n\t.reg .b64 a, ww, v;\n\tmov.b64 a, {%0,%1};\n\tmov.b64 ww, {%2,%2};\n\t"
-      "mov.b64 v, {%3,%4};\n\tfma.rn.f32x2 a, ww, v, a;\n\tmov.b64 {%0,%1}, a;\n\t}"
-      : "+f"(acc.x), "+f"(acc.y) : "f"(w), "f"(vx), "f"(vy));
+  acc = __ffma2_rn(make_float2(w, w), make_float2(vx, vy), acc);
 }
 
 // Column weights + lane fold.  Lane owns columns c = base + 2*lane_col + e (e = 0,1); its
@@ -147,19 +145,30 @@ __device__ __forceinline__ void colweight(float2 (&acc)[LP][2], const float* __r
 }
 
 template <int LP>
+__device__ __forceinline__ void colweight_plain(float2 (&acc)[LP][2], const float* hl, int nlast, int col) {
+#pragma unroll
+  for (int l = 0; l < LP; ++l) {
+    const float2 hc = *reinterpret_cast<const float2*>(hl + (size_t)l * nlast + col);
+    acc[l][0].x *= hc.x; acc[l][0].y *= hc.x;
+    acc[l][1].x *= hc.y; acc[l][1].y *= hc.y;
+  }
+}
+
+template <int LP>
 __device__ __forceinline__ void lane_fold(float2 (&acc)[LP][2], int blast) {
   for (int off = blast >= 2 ? blast / 2 : 1; off < 32; off <<= 1) {
 #pragma unroll
     for (int l = 0; l < LP; ++l)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        acc[l][e].x += __shfl_xor_sync(0xffffffffu, acc[l][e].x, off);
-        acc[l][e].y += __shfl_xor_sync(0xffffffffu, acc[l][e].y, off);
+        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, acc[l][e].x, off),
+                                     __shfl_xor_sync(0xffffffffu, acc[l][e].y, off));
+        acc[l][e] = __fadd2_rn(acc[l][e], o);
       }
   }
   if (blast == 1) {
 #pragma unroll
-    for (int l = 0; l < LP; ++l) acc[l][0] = cadd(acc[l][0], acc[l][1]);
+    for (int l = 0; l < LP; ++l) acc[l][0] = __fadd2_rn(acc[l][0], acc[l][1]);
   }
 }
 
@@ -252,6 +261,30 @@ __device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* _
         mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
         mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
         mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+      }
+    }
+  }
+}
+
+// fold_group with per-row weights formed on the fly: w[l] = h0v[l] * wrow[u][l] (D == 3,
+// more loops than two accumulator sets fit in registers).
+template <int LP, int U>
+__device__ __forceinline__ void fold_group_prod(float2 (&acc)[LP][2], const float4* __restrict__ buf, int lane,
+                                                const float* const (&wrow)[U], const float (&h0v)[LP]) {
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = buf[u * 32 + lane];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float4* wr = reinterpret_cast<const float4*>(wrow[u]);
+#pragma unroll
+    for (int l4 = 0; l4 < LP / 4; ++l4) {
+      const float4 w = wr[l4];
+      const float wv[4] = {w.x * h0v[4 * l4], w.y * h0v[4 * l4 + 1], w.z * h0v[4 * l4 + 2], w.w * h0v[4 * l4 + 3]};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mac(acc[4 * l4 + i][0], wv[i], v[u].x, v[u].y);
+        mac(acc[4 * l4 + i][1], wv[i], v[u].z, v[u].w);
       }
     }
   }
@@ -496,247 +529,358 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
 }
 
 // ------------------------------------------------------------------------------------
-// Split mode, kernel 1: one CTA per (outer residue class kappa, frame); D in {2, 3}.
-// Rows of the class are streamed per warp through the TMA ring (rows of N_last < 64
-// complex are packed 64/N_last per 512 B slot).
-// smem: ring [nwarps][S][U][32] | bars | tw[128] | sbo[32] | rw [RA+1][LP] |
-//       part [nwarps][nl][blast] | R [nl][blast+1]
-// Output fbuf[frame][l][Bo(l)][k_last]: last-dim FFT done, all half twiddles applied.
+// Split mode, kernel 1: persistent, per-WARP work units (frame, outer residue class kappa,
+// dim-0 chunk c); D in {2, 3}.  Unit u of warp gw = blockIdx.x * nwarps + warp is
+// gw + i * (gridDim.x * nwarps).  Each warp streams its unit's rows through its own TMA ring
+// (RPW = 64/N_last rows of N_last < 64 complex packed per 512 B slot); lane 0 issues boxes
+// S-1 ahead across unit boundaries, so HBM keeps streaming with no CTA barrier anywhere.
+// Row weights: D == 2 -> h0[a0][l] (staged per unit); D == 3 -> h0[a0][l] h1[a1][l] (I3),
+// applied in two levels (a1 rows with h1, then each a0 group with h0).  Output: the residue sums R[frame][l][kappa][r_last] (identity I2:
+// the class of every sample is fixed by its residues) BEFORE the per-loop residue -> bucket
+// relabelling and half-bucket twiddles, which k_split_fft applies.  With several chunks
+// per class each warp writes its chunk partial and the class's last warp to finish sums the
+// partials in chunk order (deterministic) into R.  The sums are linear in x, so partial sums
+// of dim-0 slabs (a0_base, a0_count) add up to the whole frame's (variant B).
 // ------------------------------------------------------------------------------------
-template <int LP, int U>
-__global__ void __launch_bounds__(kThreads, 2) k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
-                                                         int l0, int nl, uint32_t* __restrict__ bitmaps) {
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int LP, int U, int RPW>
+__global__ void __launch_bounds__(kThreadsSplit, LP >= 24 ? 1 : kCtasSplit)
+k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch,
+             int a0_base, int a0_count, int lg_chunk, float2* __restrict__ R, uint32_t* __restrict__ zero_bm,
+             int64_t zero_words) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int S = kStagesSplit;
+  constexpr int BR = U * RPW;                        // run rows per TMA box
+  constexpr int LPR = 32 / RPW;                      // lanes per row
   const int D = pd.D;
-  const int kappa = blockIdx.x;
-  const int64_t frame = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int blast = pd.blast, nlast = pd.nlast;
-  const int RA = pd.aouter;
-  float4* ring = reinterpret_cast<float4*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)nwarps * S * U * 32);
-  float2* tw = reinterpret_cast<float2*>(bars + nwarps * S);
-  int* sbo = reinterpret_cast<int*>(tw + 128);       // [32] outer bucket per loop
-  float* rw = reinterpret_cast<float*>(sbo + kMaxLoops);
-  float2* part = reinterpret_cast<float2*>(rw + (size_t)(RA + 1) * LP);
-  float2* R = part + (size_t)nwarps * nl * blast;
-  float* part_scratch = reinterpret_cast<float*>(R + (size_t)nl * (blast + 1));   // h0s/h1s staging
-  float4* myring = ring + (size_t)warp * S * U * 32;
-  uint64_t* mybar = bars + warp * S;
-  load_twiddles(tw);
-
-  int r0, r1 = 0;
-  if (D == 3) { r0 = kappa / pd.b[1]; r1 = kappa - r0 * pd.b[1]; } else { r0 = kappa; }
-  const int lga1 = D == 3 ? pd.lga[1] : 0;
-  {
-    // stage this class's per-dimension weights (h0[l][r0 + B0 a0], h1[l][r1 + B1 a1]) in
-    // smem with independent loads, then form the row-weight products from smem
-    const int A0 = pd.a[0], A1 = D == 3 ? pd.a[1] : 1;
-    float* h0s = part_scratch;                       // [A0][LP]
-    float* h1s = h0s + LP * A0;                      // [A1][LP]
-    for (int i = tid; i < LP * A0; i += blockDim.x) {
-      int a0 = i / LP, l = i - a0 * LP;
-      h0s[i] = l < nl ? pd.h[0][(size_t)(l0 + l) * pd.n[0] + r0 + pd.b[0] * a0] : 0.f;
-    }
-    if (D == 3)
-      for (int i = tid; i < LP * A1; i += blockDim.x) {
-        int a1 = i / LP, l = i - a1 * LP;
-        h1s[i] = l < nl ? pd.h[1][(size_t)(l0 + l) * pd.n[1] + r1 + pd.b[1] * a1] : 0.f;
-      }
-    __syncthreads();
-    // rw[q][l] = h0[a0(q)][l] * h1[a1(q)][l], two loops per item (LP is even)
-    for (int i = tid; i < (RA + 1) * (LP / 2); i += blockDim.x) {
-      const int q = i / (LP / 2), l = 2 * (i - q * (LP / 2));
-      float2 w = make_float2(0.f, 0.f);
-      if (q < RA) {
-        if (D == 3) {
-          const int a0 = q >> lga1, a1 = q & (A1 - 1);
-          const float2 x0 = *reinterpret_cast<const float2*>(h0s + a0 * LP + l);
-          const float2 x1 = *reinterpret_cast<const float2*>(h1s + a1 * LP + l);
-          w = make_float2(x0.x * x1.x, x0.y * x1.y);
-        } else {
-          w = *reinterpret_cast<const float2*>(h0s + q * LP + l);
-        }
-      }
-      *reinterpret_cast<float2*>(rw + (size_t)q * LP + l) = w;
-    }
-    __syncthreads();
-  }
-  {                                                 // zero this frame's bitmap words (K2 ORs bits)
-    const int64_t words = (int64_t)nl * pd.wpl;
-    uint32_t* bm = bitmaps + frame * words;
-    for (int64_t w = (int64_t)kappa * blockDim.x + tid; w < words; w += (int64_t)gridDim.x * blockDim.x) bm[w] = 0u;
-  }
-  for (int i = tid; i < nwarps * nl * blast; i += blockDim.x) part[i] = make_float2(0.f, 0.f);
-  if (lane == 0) {
-    for (int st = 0; st < S; ++st) mbar_init(&mybar[st], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const int nseg = nlast >= 64 ? nlast >> 6 : 1;
-  const int rpw = nlast >= 64 ? 1 : 64 / nlast;      // rows per 512 B slot
-  const int lpr = 32 / rpw;                          // lanes per row
-  const int lane_row = lane / lpr, lane_c4 = lane - lane_row * lpr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane_row = lane / LPR, lane_c4 = lane - lane_row * LPR;
+  const int blast = pd.blast, nlast = pd.nlast, bouter = pd.bouter;
+  const int B0 = pd.b[0], B1 = D == 3 ? pd.b[1] : 1;
+  const int lgb1 = D == 3 ? pd.lgb[1] : 0;
+  const int A0 = pd.a[0], A1 = D == 3 ? pd.a[1] : 1;
+  const int nchunk = 1 << lg_chunk;
+  const int A0c = a0_count >> lg_chunk;              // dim-0 residue rows per unit
+  const int nseg = RPW == 1 ? nlast >> 6 : 1;
   const int fold_lanes = blast >= 2 ? blast / 2 : 1;
   const int fold_e = blast >= 2 ? 2 : 1;
-  // Row blocks: BR = U * rpw consecutive values of the innermost outer index a_run
-  // (a1 for D == 3, a0 for D == 2) per TMA box; a_outer = a0 for D == 3.
-  const int BR = U * rpw;
-  const int AR = D == 3 ? pd.a[1] : pd.a[0];
-  const int nb_run = (AR + BR - 1) / BR;
-  const int nblk = (D == 3 ? pd.a[0] : 1) * nb_run;
-  const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
+  const int AR = D == 3 ? A1 : A0c;                  // run length: a1 (D == 3) or the chunk's a0
+  const int nb_run = AR > BR ? AR / BR : 1;
+  const int per_a0 = D == 3 ? A0c : 1;               // a0 groups per segment
+  const int plane_stride = a0_count * B0;            // dim-0 planes per frame in this launch
 
-  // warp -> (segments, block subset): wps warps share a segment, interleaving its blocks
-  int seg_start, seg_step, wsub, wps;
-  if (nseg >= nwarps) { seg_start = warp; seg_step = nwarps; wsub = 0; wps = 1; }
-  else {
-    wps = nwarps / nseg;
-    seg_start = warp < wps * nseg ? warp % nseg : nseg;
-    seg_step = nseg;
-    wsub = warp / nseg;
+  const SplitWarpLayout wl = split_warp_layout(D, LP, nl, A0c, A1, blast, nseg, RPW);
+  unsigned char* wbase = smem + (size_t)warp * wl.total;
+  float4* ring = reinterpret_cast<float4*>(wbase + wl.ring);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + wl.bars);
+  float* hsb = reinterpret_cast<float*>(wbase + wl.hs);
+  const int hs_f = wl.hs_stride / 4;                 // floats per hs buffer
+  float2* slot = reinterpret_cast<float2*>(wbase + wl.slot);
+
+  const int64_t TW = (int64_t)gridDim.x * nwarps;
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t nunits = (batch * bouter) << lg_chunk;
+  const int64_t my_units = nunits > gw ? (nunits - 1 - gw) / TW + 1 : 0;
+
+  // k_split_fft ORs bits into the bitmaps: zero them first (stream order)
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < zero_words; w += (int64_t)gridDim.x * blockDim.x)
+    zero_bm[w] = 0u;
+
+  // column weights h_last[l0 + l][col] for the whole launch in shared memory (if small):
+  // rows l >= nl are zero (padded loops)
+  const float* hl_smem = nullptr;
+  if ((size_t)LP * nlast * 4 <= kSplitHlastBytes) {
+    float* t = reinterpret_cast<float*>(smem + (size_t)nwarps * wl.total);
+    for (int i = threadIdx.x; i < LP * nlast; i += blockDim.x) {
+      const int l = i / nlast, c = i - l * nlast;
+      t[i] = l < nl ? pd.h[D - 1][(size_t)(l0 + l) * nlast + c] : 0.f;
+    }
+    __syncthreads();
+    hl_smem = t;
   }
-  const int nsegw = seg_start < nseg ? (nseg - 1 - seg_start) / seg_step + 1 : 0;
-  const int ngrp = wsub < nblk ? (nblk - 1 - wsub) / wps + 1 : 0;   // my blocks per segment
-  const int64_t total = (int64_t)nsegw * ngrp;
+  // zero the parts of the weight tables cp.async never writes: padded loops and pad rows
+  for (int i = lane; i < 2 * hs_f; i += 32) hsb[i] = 0.f;
 
-  // producer cursor (lane 0): (segment index, block ao/rb), advanced without divisions
-  int p_si = 0, p_k = 0, p_ao = wsub / nb_run, p_rb = wsub - (wsub / nb_run) * nb_run, p_st = 0;
-  int64_t p_left = total;
-  auto issue_next = [&]() {
-    if (p_left <= 0) return;
-    --p_left;
-    const int seg = seg_start + p_si * seg_step;
-    mbar_expect_tx(&mybar[p_st], (uint32_t)U * 512u);
-    float4* dst = myring + (size_t)p_st * U * 32;
-    if (D == 3)
-      tma_load_4d(dst, tmap_ptr, seg * 64, r1, p_rb * BR, (int)(frame * pd.n[0] + r0 + pd.b[0] * p_ao), &mybar[p_st]);
-    else
-      tma_load_4d(dst, tmap_ptr, seg * 64, r0, p_rb * BR, (int)frame, &mybar[p_st]);
-    if (++p_st == S) p_st = 0;
-    if (++p_k == ngrp) {
-      p_k = 0;
-      ++p_si;
-      p_ao = wsub / nb_run;
-      p_rb = wsub - p_ao * nb_run;
-    } else {
-      p_rb += wps;
-      while (p_rb >= nb_run) { p_rb -= nb_run; ++p_ao; }
+  struct Unit { int frame, kappa, r0, r1, chunk; };
+  auto decode = [&](int64_t ui) {
+    const int64_t u = gw + ui * TW;
+    Unit t;
+#if RSFT_SPLIT_ORDER
+    const int64_t ncls = batch * bouter;
+    t.chunk = (int)(u / ncls);
+    const int64_t cu = u - (int64_t)t.chunk * ncls;
+#else
+    t.chunk = (int)(u & (nchunk - 1));
+    const int64_t cu = u >> lg_chunk;
+#endif
+    t.frame = (int)(cu / bouter);
+    t.kappa = (int)(cu - (int64_t)t.frame * bouter);
+    t.r0 = t.kappa >> lgb1;
+    t.r1 = t.kappa & (B1 - 1);
+    return t;
+  };
+  // stage h0[l0 + l][(a0_base + chunk A0c + a) B0 + r0] (a < A0c) [and h1[l0 + l][r1 + B1 a1]]
+  // from the class-major tables into hs with an LP row stride (cp.async, waited per unit)
+  auto stage = [&](const Unit& t, float* h) {
+    const float* s0 = pd.ht[0] + ((size_t)t.r0 * A0 + a0_base + t.chunk * A0c) * pd.L + l0;
+    for (int i = lane; i < A0c * nl; i += 32) {
+      const int a = i / nl, l = i - a * nl;
+      cp_async4(h + a * LP + l, s0 + (size_t)a * pd.L + l);
+    }
+    if (D == 3) {
+      const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + l0;
+      float* h1 = h + A0c * LP;
+      for (int i = lane; i < A1 * nl; i += 32) {
+        const int a = i / nl, l = i - a * nl;
+        cp_async4(h1 + a * LP + l, s1 + (size_t)a * pd.L + l);
+      }
     }
   };
 
+  if (lane == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // producer cursor (lane 0): box coordinates advanced incrementally, unit by unit
+  int64_t p_ui = 0;
+  int p_st = 0, p_rb = 0, p_a0l = 0, p_seg = 0;
+  int p_c0 = 0, p_c1 = 0, p_c2 = 0, p_c3 = 0, p_c2b = 0, p_c3b = 0;
+  auto p_unit = [&]() {
+    const Unit t = decode(p_ui);
+    p_c0 = 0;
+    p_c1 = D == 3 ? t.r1 : t.r0;
+    p_c2b = D == 3 ? 0 : t.chunk * A0c;
+    p_c3b = D == 3 ? t.frame * plane_stride + t.r0 + B0 * t.chunk * A0c : t.frame;
+    p_c2 = p_c2b;
+    p_c3 = p_c3b;
+    p_rb = p_a0l = p_seg = 0;
+  };
+  if (my_units > 0) p_unit();
+  const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
+  auto issue_next = [&]() {
+    if (p_ui >= my_units) return;
+    mbar_expect_tx(&bars[p_st], (uint32_t)U * 512u);
+    tma_load_4d(ring + (size_t)p_st * U * 32, tmap_ptr, p_c0, p_c1, p_c2, p_c3, &bars[p_st]);
+    if (++p_st == S) p_st = 0;
+    if (++p_rb < nb_run) { p_c2 += BR; return; }
+    p_rb = 0;
+    p_c2 = p_c2b;
+    if (++p_a0l < per_a0) { p_c3 += B0; return; }
+    p_a0l = 0;
+    p_c3 = p_c3b;
+    if (++p_seg < nseg) { p_c0 += 64; return; }
+    if (++p_ui < my_units) p_unit();
+  };
+#if !RSFT_NO_TMA
   if (lane == 0)
     for (int j = 0; j < S - 1; ++j) issue_next();
+#endif
+  if (my_units > 0) stage(decode(0), hsb);
+
   int c_st = 0;
   uint32_t c_ph = 0;
-  for (int si = 0; si < nsegw; ++si) {
-    const int seg = seg_start + si * seg_step;
+  const float* __restrict__ hlast = pd.h[D - 1];
+  for (int64_t ui = 0; ui < my_units; ++ui) {
+    const Unit t = decode(ui);
+    float* hcur = hsb + (ui & 1) * hs_f;
+    cp_async_wait_all();
+    __syncwarp();
+    if (ui + 1 < my_units) stage(decode(ui + 1), hsb + ((ui + 1) & 1) * hs_f);
     float2 acc[LP][2];
+    for (int seg = 0; seg < nseg; ++seg) {
 #pragma unroll
-    for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-    int ao = wsub / nb_run, rb = wsub - (wsub / nb_run) * nb_run;
-    for (int k = 0; k < ngrp; ++k) {
-      if (lane == 0) issue_next();
-      mbar_wait(&mybar[c_st], c_ph);
-      const float* wrow[U];
+      for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
+      for (int a0l = 0; a0l < per_a0; ++a0l) {
+        // D == 3: rows (a0, a1) carry h0[a0][l] h1[a1][l] (I3).  LP <= 16: fold the a1 rows
+        // with h1 into `inn`, then acc += h0[a0] * inn (two-level, +1/A1 FMAs); LP > 16: the
+        // product weight is formed per row (registers do not hold two accumulator sets).
+        // D == 2: rows a0 of the chunk carry h0[a0][l] directly.
+        const float* wb = hcur + ((D == 3 ? A0c : 0) + lane_row) * LP;
+        if (D == 3 && LP <= 16) {
+          float2 inn[LP][2];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int arun = rb * BR + u * rpw + lane_row;
-        wrow[u] = rw + (size_t)(arun < AR ? ao * AR + arun : RA) * LP;
-      }
-      fold_group<LP, U>(acc, myring + (size_t)c_st * U * 32, lane, wrow);
-      __syncwarp();
-      if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
-      rb += wps;
-      while (rb >= nb_run) { rb -= nb_run; ++ao; }
-    }
-    colweight_fold<LP>(acc, pd.h[D - 1], l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
-    if (lane < fold_lanes) {
+          for (int l = 0; l < LP; ++l) inn[l][0] = inn[l][1] = make_float2(0.f, 0.f);
+          for (int rb = 0; rb < nb_run; ++rb, wb += BR * LP) {
+#if !RSFT_NO_TMA
+            if (lane == 0) issue_next();
+            mbar_wait(&bars[c_st], c_ph);
+#endif
+            const float* wrow[U];
 #pragma unroll
-      for (int l = 0; l < LP; ++l)
-        if (l < nl)
-          for (int e = 0; e < fold_e; ++e) {
-            float2* dst = part + ((size_t)warp * nl + l) * blast + 2 * lane + e;
-            *dst = cadd(*dst, acc[l][e]);
+            for (int u = 0; u < U; ++u) wrow[u] = wb + u * RPW * LP;
+            fold_group<LP, U>(inn, ring + (size_t)c_st * U * 32, lane, wrow);
+            __syncwarp();
+            if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
           }
+          const float2* h0r = reinterpret_cast<const float2*>(hcur + a0l * LP);
+#pragma unroll
+          for (int l2 = 0; l2 < LP / 2; ++l2) {
+            const float2 w = h0r[l2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              acc[2 * l2][e] = __ffma2_rn(make_float2(w.x, w.x), inn[2 * l2][e], acc[2 * l2][e]);
+              acc[2 * l2 + 1][e] = __ffma2_rn(make_float2(w.y, w.y), inn[2 * l2 + 1][e], acc[2 * l2 + 1][e]);
+            }
+          }
+        } else {
+          float h0v[LP];
+#pragma unroll
+          for (int l = 0; l < LP; ++l) h0v[l] = D == 3 ? hcur[a0l * LP + l] : 1.f;
+          for (int rb = 0; rb < nb_run; ++rb, wb += BR * LP) {
+#if !RSFT_NO_TMA
+            if (lane == 0) issue_next();
+            mbar_wait(&bars[c_st], c_ph);
+#endif
+            const float* wrow[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) wrow[u] = wb + u * RPW * LP;
+            if constexpr (LP % 4 == 0) {
+              if (D == 3) fold_group_prod<LP, U>(acc, ring + (size_t)c_st * U * 32, lane, wrow, h0v);
+              else fold_group<LP, U>(acc, ring + (size_t)c_st * U * 32, lane, wrow);
+            } else
+              fold_group<LP, U>(acc, ring + (size_t)c_st * U * 32, lane, wrow);
+            __syncwarp();
+            if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
+          }
+        }
+      }
+      // column weights of this segment + cross-lane residue fold
+      if (hl_smem) {
+        colweight_plain<LP>(acc, hl_smem, nlast, seg * 64 + 2 * lane_c4);
+        lane_fold<LP>(acc, blast);
+      } else {
+        colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
+      }
+      if (nseg > 1 && lane < fold_lanes) {
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          if (l < nl)
+            for (int e = 0; e < fold_e; ++e) {
+              float2* d = slot + l * blast + 2 * lane + e;
+              float2 v = acc[l][e];
+              if (seg > 0) v = cadd(*d, v);
+              if (seg + 1 < nseg) *d = v; else acc[l][e] = v;
+            }
+      }
     }
-  }
-  __syncthreads();
-  // combine warps (fixed order), residue -> bucket with all half twiddles (I3, L1), written
-  // bit-reversed along the last dim; outer bucket index Bo(l) of this class per loop.
-  const int rstride = blast + 1;
-  const int lgbl = pd.lgb[D - 1];
-  for (int i = tid; i < nl * blast; i += blockDim.x) {
-    int l = i >> lgbl, r = i & (blast - 1);
-    float2 sum = make_float2(0.f, 0.f);
-    for (int w = 0; w < nwarps; ++w) sum = cadd(sum, part[((size_t)w * nl + l) * blast + r]);
-    const LoopDev& lp = pd.loops[l0 + l];
-    const int dl = D - 1;
-    int bl = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
-    if (pd.shift[dl]) sum = cmul(sum, tw[bl << (6 - lgbl)]);
-    int b0 = (lp.sinv[0] * (r0 - lp.tau[0])) & (pd.b[0] - 1);
-    if (pd.shift[0]) sum = cmul(sum, tw[b0 << (6 - pd.lgb[0])]);
-    int bo = b0;
-    if (D == 3) {
-      int b1 = (lp.sinv[1] * (r1 - lp.tau[1])) & (pd.b[1] - 1);
-      if (pd.shift[1]) sum = cmul(sum, tw[b1 << (6 - pd.lgb[1])]);
-      bo = b0 * pd.b[1] + b1;
+    // acc (lanes < fold_lanes) holds this unit's residue sums: to R, or to the chunk partials
+    const int64_t cu = (int64_t)t.frame * bouter + t.kappa;
+    if (nchunk == 1) {
+      if (lane < fold_lanes) {
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          if (l < nl)
+            for (int e = 0; e < fold_e; ++e)
+              R[(((size_t)t.frame * nl + l) * bouter + t.kappa) * blast + 2 * lane + e] = acc[l][e];
+      }
+    } else {
+      if (lane < fold_lanes) {
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          if (l < nl)
+            for (int e = 0; e < fold_e; ++e)
+              pd.parts[((((size_t)t.frame * nl + l) * bouter + t.kappa) * nchunk + t.chunk) * blast + 2 * lane + e] =
+                  acc[l][e];
+      }
+      // publish: warp barrier (orders the lanes' stores before lane 0's) + a release RMW at
+      // gpu scope; the class's last warp acquires and sums the partials in chunk order
+      __syncwarp();
+      unsigned old = 0;
+      if (lane == 0)
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(pd.class_cnt + cu) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old == (unsigned)nchunk - 1) {             // last chunk of this class: combine in order
+        __syncwarp();                                // lanes ordered after lane 0's acquire
+        for (int i = lane; i < nl * blast; i += 32) {
+          const int l = i / blast, r = i - l * blast;
+          const float2* src = pd.parts + (((size_t)t.frame * nl + l) * bouter + t.kappa) * nchunk * blast + r;
+          float2 part[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) part[c] = c < nchunk ? __ldcg(src + (size_t)c * blast) : make_float2(0.f, 0.f);
+          float2 sum = part[0];
+#pragma unroll
+          for (int c = 1; c < 8; ++c) if (c < nchunk) sum = cadd(sum, part[c]);
+          for (int c = 8; c < nchunk; ++c) sum = cadd(sum, __ldcg(src + (size_t)c * blast));
+          R[(((size_t)t.frame * nl + l) * bouter + t.kappa) * blast + r] = sum;
+        }
+        if (lane == 0) pd.class_cnt[cu] = 0u;        // ready for the next launch
+      }
     }
-    if (r == 0) sbo[l] = bo;
-    R[(size_t)l * rstride + brev(bl, lgbl)] = sum;
-  }
-  __syncthreads();
-  {
-    View vw;
-    vw.k = 2;
-    vw.n[0] = nl; vw.lg[0] = 0; vw.st[0] = rstride;
-    vw.n[1] = blast; vw.lg[1] = lgbl; vw.st[1] = 1;
-    fft_axis(R, vw, 1, tw);
-  }
-  for (int i = tid; i < nl * blast; i += blockDim.x) {
-    int l = i >> lgbl, k = i & (blast - 1);
-    pd.fbuf[(((size_t)frame * nl + l) * pd.bouter + sbo[l]) * blast + k] = R[(size_t)l * rstride + k];
   }
 }
 
-// Split mode, kernel 2: one CTA per (loop, k_last, frame): FFT over the outer dims, power,
-// NP threshold, bitmap bits (atomicOr), optional spectra.
-__global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, int l0, int nl,
+// Split mode, kernel 2: one CTA per (loop, k_last, frame).  From the residue sums R:
+// last-dim DFT at k_last with the relabelling b = sigma^{-1}(r - tau) mod B and the
+// half-bucket twiddle merged into one factor per residue, e^{-j pi b (2 k + 1) / B} (I3, L1),
+// outer relabelling + half twiddles, outer-dims FFT in smem (forward, unnormalised, L7),
+// |.|^2 > gamma_l -> bitmap bits (atomicOr; words zeroed by the fold kernel or the caller),
+// optional spectra.  Alg. 1 l.9-10; Eq. tpd.
+// smem: tw[128] | twl[B_last] | V [B0][B1 + 1]
+__global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, const float2* __restrict__ R, int rl0,
+                                                        int rnl, int l0, int nl,
                                                         uint32_t* __restrict__ bitmaps,
                                                         float2* __restrict__ spectra) {
   extern __shared__ float4 smem_f4[];
   float2* tw = reinterpret_cast<float2*>(smem_f4);
-  float2* V = tw + 128;
+  float2* twl = tw + 128;
+  float2* V = twl + kMaxB;
   const int D = pd.D;
-  const int blast = pd.blast;
-  const int l = blockIdx.x / blast, kl = blockIdx.x - l * blast;
+  const int blast = pd.blast, lgbl = pd.lgb[D - 1];
+  const int l = blockIdx.x / blast, kl = blockIdx.x - l * blast;   // l relative to l0
   const int64_t frame = blockIdx.y;
   const int tid = threadIdx.x;
   const int b0 = pd.b[0], b1 = D == 3 ? pd.b[1] : 1;
   const int vstride = b1 + 1;                        // padded rows [B0][B1+1]
-  const float2* src = pd.fbuf + (((size_t)frame * nl + l) * pd.bouter) * blast + kl;
   const int lgb0 = pd.lgb[0], lgb1 = D == 3 ? pd.lgb[1] : 0;
+  const LoopDev& lp = pd.loops[l0 + l];
+  // R holds loops [rl0, rl0 + rnl) of the plan
+  const float2* src = R + (((size_t)frame * rnl + (l0 + l - rl0)) * pd.bouter) * blast;
   load_twiddles(tw);
-  for (int o = tid; o < pd.bouter; o += blockDim.x) {
-    int o0 = o >> lgb1, o1 = o & (b1 - 1);
-    V[brev(o0, lgb0) * vstride + brev(o1, lgb1)] = src[(size_t)o * blast];
+  __syncthreads();
+  const int dl = D - 1;
+  for (int r = tid; r < blast; r += blockDim.x) {
+    const int b = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
+    float2 t;
+    if (pd.shift[dl]) t = tw[((b * (2 * kl + 1)) & (2 * blast - 1)) << (6 - lgbl)];
+    else t = tw[((b * kl) & (blast - 1)) << (7 - lgbl)];
+    twl[r] = t;
   }
   __syncthreads();
-  {
-    View vw;
-    vw.k = 3;
-    vw.n[0] = 1; vw.lg[0] = 0; vw.st[0] = 0;
-    vw.n[1] = b0; vw.lg[1] = lgb0; vw.st[1] = vstride;
-    vw.n[2] = b1; vw.lg[2] = lgb1; vw.st[2] = 1;
-    if (D == 3) fft_axis(V, vw, 2, tw);
-    fft_axis(V, vw, 1, tw);
+  for (int o = tid; o < pd.bouter; o += blockDim.x) {
+    const float2* row = src + (size_t)o * blast;
+    float2 v = make_float2(0.f, 0.f);
+    for (int r = 0; r < blast; r += 2) {
+      if (blast >= 2) {
+        const float4 q = *reinterpret_cast<const float4*>(row + r);
+        v = cadd(v, cmul(make_float2(q.x, q.y), twl[r]));
+        v = cadd(v, cmul(make_float2(q.z, q.w), twl[r + 1]));
+      } else {
+        v = cmul(row[0], twl[0]);
+      }
+    }
+    const int o0 = o >> lgb1, o1 = o & (b1 - 1);
+    int bb0 = (lp.sinv[0] * (o0 - lp.tau[0])) & (b0 - 1);
+    if (pd.shift[0]) v = cmul(v, tw[bb0 << (6 - lgb0)]);
+    int bb1 = 0;
+    if (D == 3) {
+      bb1 = (lp.sinv[1] * (o1 - lp.tau[1])) & (b1 - 1);
+      if (pd.shift[1]) v = cmul(v, tw[bb1 << (6 - lgb1)]);
+    }
+    V[brev(bb0, lgb0) * vstride + brev(bb1, lgb1)] = v;
   }
-  const float gamma = pd.loops[l0 + l].gamma;
+  __syncthreads();
+  if (D == 3) fft_axis_fast(V, lgb1, 1, b0, 0, vstride, 0, tw);
+  fft_axis_fast(V, lgb0, vstride, b1, lgb1, 0, 1, tw);
+  const float gamma = lp.gamma;
   uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
   for (int o = tid; o < pd.bouter; o += blockDim.x) {
-    int o0 = o / b1, o1 = o - o0 * b1;
+    int o0 = o >> lgb1, o1 = o & (b1 - 1);
     float2 v = V[o0 * vstride + o1];
     int64_t k = (int64_t)o * blast + kl;
     if (v.x * v.x + v.y * v.y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
@@ -1258,8 +1402,9 @@ static rsft_status make_map(CUtensorMap* m, const void* base, int rank, const cu
 }
 
 // Map for the fold kernels: D >= 2 -> [N_last][B_o][A_o][planes] (B_o, A_o of the innermost
-// outer dim, planes = batch (D == 2) or batch * N_0 (D == 3)); D == 1 -> [64][N/64][batch].
-static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, CUtensorMap* m, int u) {
+// outer dim, planes = batch (D == 2) or batch * n0 (D == 3)); D == 1 -> [64][N/64][batch].
+// n0 = dim-0 extent of one frame in this launch (N_0, or a slab's length for variant B).
+static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, int64_t n0, CUtensorMap* m, int u) {
   const int D = p->D;
   const uint64_t e = 8;
   if (D == 1) {
@@ -1268,8 +1413,8 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
     cuuint32_t box[3] = {64, (cuuint32_t)u, 1};
     return make_map(m, d_x, 3, dims, str, box);
   }
-  const int64_t nl = p->n[D - 1], no = p->n[D - 2], bo = p->b[D - 2], ao = p->a[D - 2];
-  const int64_t planes = D == 3 ? batch * p->n[0] : batch;
+  const int64_t nl = p->n[D - 1], no = D == 3 ? p->n[D - 2] : n0, bo = p->b[D - 2], ao = no / bo;
+  const int64_t planes = D == 3 ? batch * n0 : batch;
   const int64_t rpw = nl >= 64 ? 1 : 64 / nl;
   cuuint64_t dims[4] = {(cuuint64_t)nl, (cuuint64_t)bo, (cuuint64_t)ao, (cuuint64_t)planes};
   cuuint64_t str[3] = {(cuuint64_t)(nl * e), (cuuint64_t)(bo * nl * e), (cuuint64_t)(no * nl * e)};
@@ -1283,7 +1428,7 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
   auto kern = k_fused<LP, kU>;
   const size_t smem = fused_smem_bytes(p, nl, LP);
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, &tmap, kU);
+  rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, kU);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
@@ -1298,31 +1443,66 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
   return check(cudaGetLastError(), "k_fused launch");
 }
 
+// Split-mode fold of dim-0 rows [a0_base*B0, (a0_base + a0_count)*B0) of `batch` frames
+// into residue sums R [batch][nl][B_outer][B_last]; zeroes zero_words bitmap words.
 template <int LP>
-static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
-                                  uint32_t* bm, void* spectra, cudaStream_t st) {
-  auto kern = k_split_fold<LP, kUSplit>;
-  const int D = p->D;
-  const int64_t blast = p->b[D - 1];
-  const size_t smem = split_smem_bytes(p, nl, LP);
+static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
+                                       int64_t a0_base, int64_t a0_count, float2* R, uint32_t* zero_bm,
+                                       int64_t zero_words, cudaStream_t st) {
+  auto kern = p->n[p->D - 1] >= 64 ? k_split_fold<LP, kUSplit, 1> : k_split_fold<LP, kUSplit, 2>;
+  const int64_t bouter = p->dev.bouter, blast = p->b[p->D - 1];
+  int lg = split_lg_chunks(p, batch, nl, a0_count, (int64_t)p->num_sms * (kThreadsSplit / 32) * (LP >= 24 ? 1 : kCtasSplit));
+  while (lg > 0 && ((batch * bouter) << lg) * nl * blast > p->dev.parts_capacity) --lg;
+  if (lg > 0 && batch * bouter > p->dev.class_capacity) lg = 0;
+  // more chunks if the per-warp weight tables do not fit (smaller dim-0 chunk per unit)
+  const int64_t amin = p->D == 3 ? 1 : (int64_t)kUSplit * (p->n[p->D - 1] >= 64 ? 1 : 64 / p->n[p->D - 1]);
+  while (split_smem_bytes(p, nl, LP, a0_count >> lg) > 227 * 1024 && (a0_count >> (lg + 1)) >= amin &&
+         ((batch * bouter) << (lg + 1)) * nl * blast <= p->dev.parts_capacity && batch * bouter <= p->dev.class_capacity)
+    ++lg;
+  const size_t smem = split_smem_bytes(p, nl, LP, a0_count >> lg);
+  if (smem > 227 * 1024) { set_error("k_split_fold: tables beyond shared memory"); return RSFT_E_UNSUPPORTED; }
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, &tmap, kUSplit);
+  rsft_status s = fold_map(p, d_x, batch, a0_count * p->b[0], &tmap, kUSplit);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
-  dim3 grid((unsigned)p->dev.bouter, (unsigned)batch);
-  kern<<<grid, kThreads, smem, st>>>(p->dev, tmap, l0, nl, bm);
-  p->last_launches += 1;
-  s = check(cudaGetLastError(), "k_split_fold launch");
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreadsSplit, smem), "occupancy");
   if (s) return s;
+  if (nb < 1) { set_error("k_split_fold: zero occupancy"); return RSFT_E_UNSUPPORTED; }
+  const int64_t wunits = (batch * bouter) << lg;
+  int64_t grid = (int64_t)nb * p->num_sms;
+  const int64_t need = (wunits + kThreadsSplit / 32 - 1) / (kThreadsSplit / 32);
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, kThreadsSplit, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg, R,
+                                                    zero_bm, zero_words);
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_split_fold launch");
+}
+
+// Residue sums R (holding loops [rl0, rl0 + rnl)) -> bitmaps / spectra of loops [l0, l0 + nl).
+static rsft_status launch_split_fft(rsft_plan_s* p, const float2* R, int rl0, int rnl, int64_t batch, int l0,
+                                    int nl, uint32_t* bm, void* spectra, cudaStream_t st) {
+  const int D = p->D;
+  const int64_t blast = p->b[D - 1];
   const int64_t b1 = D == 3 ? p->b[1] : 1;
-  size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
-  s = check(cudaFuncSetAttribute(k_split_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), "smem attr");
+  size_t smem2 = (128 + kMaxB) * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
+  rsft_status s = check(cudaFuncSetAttribute(k_split_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2),
+                        "smem attr");
   if (s) return s;
   dim3 grid2((unsigned)(nl * blast), (unsigned)batch);
-  k_split_fft<<<grid2, kThreads, smem2, st>>>(p->dev, l0, nl, bm, reinterpret_cast<float2*>(spectra));
+  k_split_fft<<<grid2, kThreads, smem2, st>>>(p->dev, R, rl0, rnl, l0, nl, bm, reinterpret_cast<float2*>(spectra));
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_fft launch");
+}
+
+template <int LP>
+static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
+                                  uint32_t* bm, void* spectra, cudaStream_t st) {
+  rsft_status s = launch_split_fold_t<LP>(p, d_x, batch, l0, nl, 0, p->a[0], p->dev.fbuf, bm,
+                                          batch * nl * (int64_t)p->dev.wpl, st);
+  if (s) return s;
+  return launch_split_fft(p, p->dev.fbuf, l0, nl, batch, l0, nl, bm, spectra, st);
 }
 
 #define RSFT_DISPATCH_LP(FN, LPV, ...)                   \

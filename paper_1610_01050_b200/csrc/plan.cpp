@@ -3,6 +3,7 @@
 //
 // Independent of the oracle (oracle/rsft_ref.py, NumPy): same definitions, written again.
 // Citations: P:<line> = /root/reference/PAPER.md; Lnn = DESIGN.md readings.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -168,8 +169,29 @@ void layout_workspace(rsft_plan_s* p) {
     w.h_off[d] = off;
     if (d < p->D) off = align256(off + sizeof(float) * (size_t)p->L * p->n[d]);
   }
+  for (int d = 0; d < 3; ++d) {                    // class-major copies for the split fold
+    w.ht_off[d] = off;
+    if (d + 1 < p->D) off = align256(off + sizeof(float) * (size_t)p->L * p->n[d]);
+  }
   w.fbuf_off = off;
   if (p->D >= 2) off = align256(off + (size_t)p->P.max_batch * p->L * p->btot * 8);
+  // split mode: per-chunk partials, sized for the chunking of batch = 1 (the most chunks;
+  // launches with more frames use fewer chunks and must fit, else fall back to fewer)
+  w.parts_off = off;
+  w.parts_bytes = 0;
+  w.cnt_capacity = 0;
+  if (p->D >= 2) {
+    const int64_t bouter = p->btot / p->b[p->D - 1];
+    int64_t best = 0;
+    for (int64_t b = 1; b <= p->P.max_batch && b <= 64; b *= 2) {
+      int lg = split_lg_chunks(p, b, p->L, p->a[0], (int64_t)148 * (kThreadsSplit / 32) * kCtasSplit);
+      if (lg > 0) best = std::max(best, (b * bouter << lg) * p->L * p->b[p->D - 1]);
+    }
+    w.parts_bytes = (size_t)best * 8;
+    off = align256(off + w.parts_bytes);
+    w.cnt_capacity = p->P.max_batch * bouter;
+  }
+  w.cnt_off = off; off = align256(off + 4 * (size_t)w.cnt_capacity);
   int64_t dw = (p->ntot + 31) / 32;
   int64_t chunks = (p->P.max_batch * dw + kChunkWords - 1) / kChunkWords;
   w.chunk_capacity = chunks;
@@ -198,15 +220,40 @@ size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
   return ring + fbytes + (size_t)(n0 + 1) * lpad * 4;
 }
 
-size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
-  const int nwarps = kThreads / 32;
-  int64_t blast = p->b[p->D - 1];
-  int64_t ra = 1;
-  for (int d = 0; d + 1 < p->D; ++d) ra *= p->a[d];
-  size_t ring = (size_t)nwarps * kStagesSplit * kUSplit * 512 + (size_t)nwarps * kStagesSplit * 8;
-  int64_t a0 = p->a[0], a1 = p->D == 3 ? p->a[1] : 1;
-  return ring + 128 * 8 + kMaxLoops * 4 + (size_t)(ra + 1) * lpad * 4 + (size_t)nwarps * nl * blast * 8 +
-         (size_t)nl * (blast + 1) * 8 + (size_t)lpad * (a0 + a1) * 4;
+size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c) {
+  const int D = p->D;
+  const int64_t nlast = p->n[D - 1];
+  const int nseg = nlast >= 64 ? (int)(nlast / 64) : 1;
+  SplitWarpLayout w = split_warp_layout(D, lpad, nl, (int)a0c, D == 3 ? (int)p->a[1] : 1, (int)p->b[D - 1], nseg,
+                                        nlast >= 64 ? 1 : (int)(64 / nlast));
+  const size_t hl = (size_t)lpad * nlast * 4;
+  return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0);
+}
+
+// Split-mode work units are (frame, outer residue class, dim-0 chunk) per WARP.  Chunk the
+// dim-0 rows (2^lg chunks) until there are >= kSplitUnitsPerWarp units per resident warp
+// with < 5 % tail loss, keeping >= 32 rows per unit (D == 2: a chunk holds >= 1 TMA box).
+int split_lg_chunks(const rsft_plan_s* p, int64_t batch, int nl, int64_t a0_count, int64_t warps_total) {
+  const int D = p->D;
+  const int64_t nlast = p->n[D - 1];
+  const int64_t bouter = p->btot / p->b[D - 1];
+  const int64_t a1 = D == 3 ? p->a[1] : 1;
+  const int64_t nseg = nlast >= 64 ? nlast / 64 : 1;
+  const int64_t rpw = nlast >= 64 ? 1 : 64 / nlast;
+  const int64_t amin = D == 3 ? 1 : kUSplit * rpw;
+  int best = 0;
+  double best_eff = -1.0;
+  for (int lg = 0; (a0_count >> lg) >= 1; ++lg) {
+    const int64_t a0c = a0_count >> lg;
+    if (lg > 0 && (a0c < amin || a0c * a1 * nseg * (nlast >= 64 ? 1 : 1) < 32)) break;
+    if (lg > 0 && (a0c << lg) != a0_count) break;
+    const double n = (double)(batch * bouter << lg) / (double)warps_total;
+    const double eff = n / std::ceil(n);
+    if (n >= kSplitUnitsPerWarp && eff >= 0.95) return lg;
+    if (eff > best_eff + 0.02) { best_eff = eff; best = lg; }
+  }
+  (void)nl;
+  return best;
 }
 
 int resolve_mode(const rsft_plan_s* p, int64_t batch) {
@@ -214,7 +261,9 @@ int resolve_mode(const rsft_plan_s* p, int64_t batch) {
   const int lp = loop_pad(p->L);
   bool fused_ok = p->D <= 2 && nlast >= 64 && p->btot <= 8 * kThreads &&
                   fused_smem_bytes(p, p->L, lp) <= 110 * 1024;
-  bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp) <= 220 * 1024;
+  // split mode chunks dim 0 as far as needed to fit the per-warp tables (launch_split_fold_t)
+  const int64_t amin = p->D == 3 ? 1 : std::min<int64_t>(p->a[0], (int64_t)kUSplit * (nlast >= 64 ? 1 : 64 / nlast));
+  bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp, amin) <= 220 * 1024;
   int m = p->P.mode;
   if (m == RSFT_MODE_FUSED) return fused_ok ? RSFT_MODE_FUSED : -1;
   if (m == RSFT_MODE_SPLIT) return split_ok ? RSFT_MODE_SPLIT : -1;

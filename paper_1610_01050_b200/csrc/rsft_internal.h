@@ -19,8 +19,61 @@ constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detecti
 constexpr int kThreads = 256;          // CTA size of every kernel
 constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
 constexpr int kU = 4;                  // 512 B row slots per ring stage
-constexpr int kStagesSplit = 2;        // split-mode fold: 2 stages of ...
-constexpr int kUSplit = 8;             // ... 8 slots (4 KiB TMA boxes)
+#ifndef RSFT_NO_TMA
+#define RSFT_NO_TMA 0
+#endif
+#ifndef RSFT_SPLIT_ORDER
+#define RSFT_SPLIT_ORDER 1
+#endif
+#ifndef RSFT_NO_FOLD_COMPUTE
+#define RSFT_NO_FOLD_COMPUTE 0
+#endif
+#ifndef RSFT_SPLIT_STAGES
+#define RSFT_SPLIT_STAGES 3
+#endif
+#ifndef RSFT_SPLIT_U
+#define RSFT_SPLIT_U 8
+#endif
+#ifndef RSFT_SPLIT_THREADS
+#define RSFT_SPLIT_THREADS 256
+#endif
+#ifndef RSFT_SPLIT_CTAS
+#define RSFT_SPLIT_CTAS 1
+#endif
+constexpr int kStagesSplit = RSFT_SPLIT_STAGES;   // split-mode fold: per-warp ring depth of ...
+constexpr int kUSplit = RSFT_SPLIT_U;             // ... U-slot (U x 512 B) TMA boxes
+constexpr int kThreadsSplit = RSFT_SPLIT_THREADS; // threads per CTA ...
+constexpr int kCtasSplit = RSFT_SPLIT_CTAS;       // ... and CTAs per SM the kernel is built for
+constexpr int kSplitUnitsPerWarp = 4;
+constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in smem up to this size             // chunking target: >= this many units per warp
+
+#ifdef __CUDACC__
+#define RSFT_HD __host__ __device__
+#else
+#define RSFT_HD
+#endif
+
+// Per-warp shared-memory carve-up of the split-mode fold (byte offsets inside a warp's
+// region): TMA ring, its mbarriers, double-buffered staged weights hs and the segment slot.
+// D == 2: hs rows = the chunk's a0 rows (row weights h0), zero-padded to a whole box;
+// D == 3: hs = A0c h0 rows + A1 h1 rows (zero-padded to a whole box).
+struct SplitWarpLayout {
+  int ring, bars, hs, hs_stride, slot, total;
+};
+RSFT_HD inline int split_pad_rows(int rows, int br) { return rows < br ? br : rows; }
+RSFT_HD inline SplitWarpLayout split_warp_layout(int D, int lpad, int nl, int a0c, int a1, int blast, int nseg,
+                                                 int rpw) {
+  SplitWarpLayout w;
+  const int br = kUSplit * rpw;
+  int off = 0;
+  w.ring = off; off += kStagesSplit * kUSplit * 512;
+  w.bars = off; off += ((kStagesSplit * 8 + 15) / 16) * 16;
+  const int hs_rows = D == 3 ? a0c + split_pad_rows(a1, br) : split_pad_rows(a0c, br);
+  w.hs = off; w.hs_stride = ((hs_rows * lpad * 4 + 15) / 16) * 16; off += 2 * w.hs_stride;
+  w.slot = off; off += nseg > 1 ? nl * blast * 8 : 0;
+  w.total = ((off + 127) / 128) * 128;
+  return w;
+}
 
 // Per-loop device record: schedule + threshold (Def. 1; Eq. tpd).
 struct LoopDev {
@@ -48,7 +101,12 @@ struct PlanDev {
   int32_t aouter;                  // prod_{d<D-1} A_d (rows per outer residue class)
   const LoopDev* loops;            // [L]
   const float* h[kMaxDim];         // [L][N_d] fp32 weight tables h_{l,d}[s] (I3)
-  float2* fbuf;                    // split mode intermediate [batch][L][B_tot]
+  float2* fbuf;                    // split mode residue sums [batch][L][B_tot] (k_split_fold -> k_split_fft)
+  const float* ht[kMaxDim];        // d < D-1: class-major weights [B_d][A_d][L], ht[r][a][l] = h[l][r + B_d a]
+  float2* parts;                   // split mode per-chunk partial residue sums
+  int64_t parts_capacity;          // float2 elements
+  unsigned* class_cnt;             // split mode per-(frame, class) chunk counters (0 between launches)
+  int64_t class_capacity;
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
   const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
@@ -59,9 +117,10 @@ struct PlanDev {
 constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], fbuf_off, chunk_off, xmask_off, xmask_bytes, region_off, total;
+  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], parts_off, parts_bytes, cnt_off, fbuf_off, chunk_off, xmask_off, xmask_bytes, region_off, total;
   int64_t region_capacity;
   int64_t chunk_capacity;
+  int64_t cnt_capacity;
 };
 
 }  // namespace rsft
@@ -94,6 +153,7 @@ void layout_workspace(rsft_plan_s* p);
 int resolve_mode(const rsft_plan_s* p, int64_t batch);
 int loop_pad(int nl);
 size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
-size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
+size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c);
+int split_lg_chunks(const rsft_plan_s* p, int64_t batch, int nl, int64_t a0_count, int64_t warps_total);
 void set_error(const std::string& s);
 }  // namespace rsft

@@ -14,7 +14,7 @@ from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_uin
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librsft.so")
+LIB_PATH = os.environ.get("RSFT_LIB") or os.path.join(HERE, "librsft.so")   # RSFT_LIB: tuning variants
 
 WIN = {"rect": 0, "hann": 1, "cheb": 2}
 MODE = {"auto": 0, "fused": 1, "split": 2}
