@@ -66,9 +66,6 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.ht_off[d], ht.data(), sizeof(float) * ht.size(),
                                         cudaMemcpyHostToDevice, st), "upload class-major weights"))) return s;
   }
-  if (p->ws.cnt_capacity)
-    if ((s = cuda_check(cudaMemsetAsync(base + p->ws.cnt_off, 0, 4 * (size_t)p->ws.cnt_capacity, st), "zero counters")))
-      return s;
   if (!p->xmask.empty() && p->ws.xmask_bytes == p->xmask.size() * 4)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
                                         cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
@@ -101,10 +98,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.aouter = (int32_t)aouter;
   pd.loops = reinterpret_cast<const LoopDev*>(base + p->ws.loops_off);
   pd.fbuf = reinterpret_cast<float2*>(base + p->ws.fbuf_off);
-  pd.parts = reinterpret_cast<float2*>(base + p->ws.parts_off);
-  pd.parts_capacity = (int64_t)(p->ws.parts_bytes / 8);
-  pd.class_cnt = reinterpret_cast<unsigned*>(base + p->ws.cnt_off);
-  pd.class_capacity = p->ws.cnt_capacity;
+  pd.fbuf_capacity = (int64_t)(p->ws.fbuf_bytes / 8);
   pd.chunk_counts = reinterpret_cast<long long*>(base + p->ws.chunk_off);
   pd.chunk_capacity = p->ws.chunk_capacity;
   pd.xmask = p->ws.xmask_bytes ? reinterpret_cast<const uint32_t*>(base + p->ws.xmask_off) : nullptr;

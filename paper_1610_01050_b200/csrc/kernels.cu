@@ -217,6 +217,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, uint64_t tmap, int c0, in
                :: "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
 }
 
+// expect_tx + 4-D tensor-map load issued by lane 0 only, through predicates: every lane runs
+// the producer cursor (warp-uniform values), so there is no divergent branch per box.
+__device__ __forceinline__ void tma_load_4d_lane0(int lane, void* dst, uint64_t tmap, int c0, int c1, int c2, int c3,
+                                                  uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t"
+               "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%7], %8;\n\t"
+               "@p cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%1], [%2, {%3, %4, %5, %6}], [%7];\n\t}"
+               :: "r"(lane), "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)),
+                  "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
@@ -230,7 +243,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // One row group: U row-loads of 32 float4 (512 B) per warp, already in the stage buffer.
 // acc[l] += w_row[l] * x for each row.  Rows past the end of a class are zero-filled by
 // the TMA (out-of-bounds box rows) and carry the zero weight row, so they add nothing.
-template <int LP, int U>
+template <int LP, int U, bool INIT = false>
 __device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* __restrict__ buf, int lane,
                                            const float* const (&wrow)[U]) {
   float4 v[U];
@@ -242,25 +255,35 @@ __device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* _
       const float4* wr = reinterpret_cast<const float4*>(wrow[u]);
 #pragma unroll
       for (int l4 = 0; l4 < LP / 4; ++l4) {
-        float4 w = wr[l4];
-        mac(acc[4 * l4][0], w.x, v[u].x, v[u].y);
-        mac(acc[4 * l4][1], w.x, v[u].z, v[u].w);
-        mac(acc[4 * l4 + 1][0], w.y, v[u].x, v[u].y);
-        mac(acc[4 * l4 + 1][1], w.y, v[u].z, v[u].w);
-        mac(acc[4 * l4 + 2][0], w.z, v[u].x, v[u].y);
-        mac(acc[4 * l4 + 2][1], w.z, v[u].z, v[u].w);
-        mac(acc[4 * l4 + 3][0], w.w, v[u].x, v[u].y);
-        mac(acc[4 * l4 + 3][1], w.w, v[u].z, v[u].w);
+        const float4 w = wr[l4];
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (INIT && u == 0) {                    // first row of the group: acc = w * v
+            acc[4 * l4 + i][0] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].x, v[u].y));
+            acc[4 * l4 + i][1] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].z, v[u].w));
+          } else {
+            mac(acc[4 * l4 + i][0], wv[i], v[u].x, v[u].y);
+            mac(acc[4 * l4 + i][1], wv[i], v[u].z, v[u].w);
+          }
+        }
       }
     } else {
       const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
 #pragma unroll
       for (int l2 = 0; l2 < LP / 2; ++l2) {
-        float2 w = wr[l2];
-        mac(acc[2 * l2][0], w.x, v[u].x, v[u].y);
-        mac(acc[2 * l2][1], w.x, v[u].z, v[u].w);
-        mac(acc[2 * l2 + 1][0], w.y, v[u].x, v[u].y);
-        mac(acc[2 * l2 + 1][1], w.y, v[u].z, v[u].w);
+        const float2 w = wr[l2];
+        const float wv[2] = {w.x, w.y};
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (INIT && u == 0) {
+            acc[2 * l2 + i][0] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].x, v[u].y));
+            acc[2 * l2 + i][1] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].z, v[u].w));
+          } else {
+            mac(acc[2 * l2 + i][0], wv[i], v[u].x, v[u].y);
+            mac(acc[2 * l2 + i][1], wv[i], v[u].z, v[u].w);
+          }
+        }
       }
     }
   }
@@ -602,6 +625,10 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
     __syncthreads();
     hl_smem = t;
   }
+  float2* tws = reinterpret_cast<float2*>(smem + (size_t)nwarps * wl.total +
+                                         ((size_t)LP * nlast * 4 <= kSplitHlastBytes ? (size_t)LP * nlast * 4 : 0));
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = c_tw128[i];
+  __syncthreads();
   // zero the parts of the weight tables cp.async never writes: padded loops and pad rows
   for (int i = lane; i < 2 * hs_f; i += 32) hsb[i] = 0.f;
 
@@ -663,10 +690,10 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   };
   if (my_units > 0) p_unit();
   const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
-  auto issue_next = [&]() {
+  auto issue_next = [&]() {                         // run by all lanes; lane 0 issues
     if (p_ui >= my_units) return;
-    mbar_expect_tx(&bars[p_st], (uint32_t)U * 512u);
-    tma_load_4d(ring + (size_t)p_st * U * 32, tmap_ptr, p_c0, p_c1, p_c2, p_c3, &bars[p_st]);
+    tma_load_4d_lane0(lane, ring + (size_t)p_st * U * 32, tmap_ptr, p_c0, p_c1, p_c2, p_c3, &bars[p_st],
+                      (uint32_t)U * 512u);
     if (++p_st == S) p_st = 0;
     if (++p_rb < nb_run) { p_c2 += BR; return; }
     p_rb = 0;
@@ -678,8 +705,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
     if (++p_ui < my_units) p_unit();
   };
 #if !RSFT_NO_TMA
-  if (lane == 0)
-    for (int j = 0; j < S - 1; ++j) issue_next();
+  for (int j = 0; j < S - 1; ++j) issue_next();
 #endif
   if (my_units > 0) stage(decode(0), hsb);
 
@@ -703,12 +729,23 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
         // D == 2: rows a0 of the chunk carry h0[a0][l] directly.
         const float* wb = hcur + ((D == 3 ? A0c : 0) + lane_row) * LP;
         if (D == 3 && LP <= 16) {
-          float2 inn[LP][2];
-#pragma unroll
-          for (int l = 0; l < LP; ++l) inn[l][0] = inn[l][1] = make_float2(0.f, 0.f);
-          for (int rb = 0; rb < nb_run; ++rb, wb += BR * LP) {
+          float2 inn[LP][2];                         // set by the first box (INIT)
+          {                                          // box 0 peeled: inn = h1 x (no zero fill)
 #if !RSFT_NO_TMA
-            if (lane == 0) issue_next();
+            issue_next();
+            mbar_wait(&bars[c_st], c_ph);
+#endif
+            const float* wrow[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) wrow[u] = wb + u * RPW * LP;
+            fold_group<LP, U, true>(inn, ring + (size_t)c_st * U * 32, lane, wrow);
+            __syncwarp();
+            if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
+            wb += BR * LP;
+          }
+          for (int rb = 1; rb < nb_run; ++rb, wb += BR * LP) {
+#if !RSFT_NO_TMA
+            issue_next();
             mbar_wait(&bars[c_st], c_ph);
 #endif
             const float* wrow[U];
@@ -734,7 +771,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
           for (int l = 0; l < LP; ++l) h0v[l] = D == 3 ? hcur[a0l * LP + l] : 1.f;
           for (int rb = 0; rb < nb_run; ++rb, wb += BR * LP) {
 #if !RSFT_NO_TMA
-            if (lane == 0) issue_next();
+            issue_next();
             mbar_wait(&bars[c_st], c_ph);
 #endif
             const float* wrow[U];
@@ -750,122 +787,83 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
           }
         }
       }
-      // column weights of this segment + cross-lane residue fold
+      // column weights of this segment + cross-lane residue fold -> slot[l][r] (segments add)
       if (hl_smem) {
         colweight_plain<LP>(acc, hl_smem, nlast, seg * 64 + 2 * lane_c4);
         lane_fold<LP>(acc, blast);
       } else {
         colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
       }
-      if (nseg > 1 && lane < fold_lanes) {
+      if (lane < fold_lanes) {
 #pragma unroll
         for (int l = 0; l < LP; ++l)
           if (l < nl)
             for (int e = 0; e < fold_e; ++e) {
               float2* d = slot + l * blast + 2 * lane + e;
-              float2 v = acc[l][e];
-              if (seg > 0) v = cadd(*d, v);
-              if (seg + 1 < nseg) *d = v; else acc[l][e] = v;
+              *d = seg == 0 ? acc[l][e] : cadd(*d, acc[l][e]);
             }
       }
     }
-    // acc (lanes < fold_lanes) holds this unit's residue sums: to R, or to the chunk partials
-    const int64_t cu = (int64_t)t.frame * bouter + t.kappa;
-    if (nchunk == 1) {
-      if (lane < fold_lanes) {
-#pragma unroll
-        for (int l = 0; l < LP; ++l)
-          if (l < nl)
-            for (int e = 0; e < fold_e; ++e)
-              R[(((size_t)t.frame * nl + l) * bouter + t.kappa) * blast + 2 * lane + e] = acc[l][e];
-      }
-    } else {
-      if (lane < fold_lanes) {
-#pragma unroll
-        for (int l = 0; l < LP; ++l)
-          if (l < nl)
-            for (int e = 0; e < fold_e; ++e)
-              pd.parts[((((size_t)t.frame * nl + l) * bouter + t.kappa) * nchunk + t.chunk) * blast + 2 * lane + e] =
-                  acc[l][e];
-      }
-      // publish: warp barrier (orders the lanes' stores before lane 0's) + a release RMW at
-      // gpu scope; the class's last warp acquires and sums the partials in chunk order
-      __syncwarp();
-      unsigned old = 0;
-      if (lane == 0)
-        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(pd.class_cnt + cu) : "memory");
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == (unsigned)nchunk - 1) {             // last chunk of this class: combine in order
-        __syncwarp();                                // lanes ordered after lane 0's acquire
-        for (int i = lane; i < nl * blast; i += 32) {
-          const int l = i / blast, r = i - l * blast;
-          const float2* src = pd.parts + (((size_t)t.frame * nl + l) * bouter + t.kappa) * nchunk * blast + r;
-          float2 part[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) part[c] = c < nchunk ? __ldcg(src + (size_t)c * blast) : make_float2(0.f, 0.f);
-          float2 sum = part[0];
-#pragma unroll
-          for (int c = 1; c < 8; ++c) if (c < nchunk) sum = cadd(sum, part[c]);
-          for (int c = 8; c < nchunk; ++c) sum = cadd(sum, __ldcg(src + (size_t)c * blast));
-          R[(((size_t)t.frame * nl + l) * bouter + t.kappa) * blast + r] = sum;
-        }
-        if (lane == 0) pd.class_cnt[cu] = 0u;        // ready for the next launch
+    __syncwarp();
+    // last-dim DFT of the unit's residue sums with the residue -> bucket relabelling and the
+    // half-bucket twiddle merged into one factor per (loop, residue, k_last) (I3, L1):
+    //   F[l][k][kappa] = sum_r slot[l][r] e^{-j pi b_l(r) (2k + 1) / B},  b_l(r) = sigma^{-1}(r - tau)
+    // (no shift when B_last = N_last: e^{-j 2 pi b k / B}).  Written per dim-0 chunk;
+    // k_split_fft adds the chunks in order (deterministic, no atomics).
+    {
+      const int dl = D - 1, lgbl = pd.lgb[dl], shl = pd.shift[dl];
+      float2* dst = R + (size_t)t.frame * nl * blast * nchunk * bouter + (size_t)t.chunk * bouter + t.kappa;
+      const int m2 = shl ? 2 * blast - 1 : blast - 1;     // twiddle index mod 2B (shift) or B
+      const int tsh = shl ? 6 - lgbl : 7 - lgbl;
+      for (int i = lane; i < nl * blast; i += 32) {
+        const int l = i >> lgbl, k = i & (blast - 1);
+        const LoopDev& lp = pd.loops[l0 + l];
+        const float2* row = slot + l * blast;
+        // twiddle index b(r) (2k + 1) mod 2B [or b(r) k mod B], b(r) = sigma^{-1} (r - tau) mod B
+        const int f = shl ? 2 * k + 1 : k;
+        int b = (lp.sinv[dl] * (0 - lp.tau[dl])) & (blast - 1);
+        const int db = lp.sinv[dl] & (blast - 1);
+        float2 v = make_float2(0.f, 0.f);
+        for (int r = 0; r < blast; ++r, b = (b + db) & (blast - 1)) v = cadd(v, cmul(row[r], tws[((b * f) & m2) << tsh]));
+        dst[(size_t)i * nchunk * bouter] = v;
       }
     }
+    __syncwarp();
   }
 }
 
-// Split mode, kernel 2: one CTA per (loop, k_last, frame).  From the residue sums R:
-// last-dim DFT at k_last with the relabelling b = sigma^{-1}(r - tau) mod B and the
-// half-bucket twiddle merged into one factor per residue, e^{-j pi b (2 k + 1) / B} (I3, L1),
-// outer relabelling + half twiddles, outer-dims FFT in smem (forward, unnormalised, L7),
-// |.|^2 > gamma_l -> bitmap bits (atomicOr; words zeroed by the fold kernel or the caller),
-// optional spectra.  Alg. 1 l.9-10; Eq. tpd.
-// smem: tw[128] | twl[B_last] | V [B0][B1 + 1]
-__global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, const float2* __restrict__ R, int rl0,
-                                                        int rnl, int l0, int nl,
-                                                        uint32_t* __restrict__ bitmaps,
-                                                        float2* __restrict__ spectra) {
+// Split mode, kernel 2: one CTA per (loop, k_last, frame).  From the folded spectra F (k_last
+// domain, one slice per dim-0 chunk): sum the chunks in order, outer relabelling
+// b_d = sigma^{-1}(r_d - tau_d) mod B_d + half twiddles e^{-j pi b_d / B_d} (I3, L1), outer-dims
+// FFT in smem (forward, unnormalised, L7), |.|^2 > gamma_l -> bitmap bits (atomicOr; words
+// zeroed by the fold kernel or the caller), optional spectra.  Alg. 1 l.9-10;
+// Eq. tpd.  F holds loops [rl0, rl0 + rnl) of the plan.
+// smem: tw[128] | V [B0][B1 + 1]
+__global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const float2* __restrict__ F, int rl0,
+                                                           int rnl, int nchunk, int l0, int nl,
+                                                           uint32_t* __restrict__ bitmaps,
+                                                           float2* __restrict__ spectra) {
   extern __shared__ float4 smem_f4[];
   float2* tw = reinterpret_cast<float2*>(smem_f4);
-  float2* twl = tw + 128;
-  float2* V = twl + kMaxB;
+  float2* V = tw + 128;
   const int D = pd.D;
   const int blast = pd.blast, lgbl = pd.lgb[D - 1];
-  const int l = blockIdx.x / blast, kl = blockIdx.x - l * blast;   // l relative to l0
+  const int l = blockIdx.x >> lgbl, kl = blockIdx.x & (blast - 1);   // l relative to l0
   const int64_t frame = blockIdx.y;
   const int tid = threadIdx.x;
   const int b0 = pd.b[0], b1 = D == 3 ? pd.b[1] : 1;
   const int vstride = b1 + 1;                        // padded rows [B0][B1+1]
   const int lgb0 = pd.lgb[0], lgb1 = D == 3 ? pd.lgb[1] : 0;
+  const int bouter = pd.bouter;
   const LoopDev& lp = pd.loops[l0 + l];
-  // R holds loops [rl0, rl0 + rnl) of the plan
-  const float2* src = R + (((size_t)frame * rnl + (l0 + l - rl0)) * pd.bouter) * blast;
+  const float2* src = F + ((((size_t)frame * rnl + (l0 + l - rl0)) * blast + kl) * nchunk) * bouter;
   load_twiddles(tw);
   __syncthreads();
-  const int dl = D - 1;
-  for (int r = tid; r < blast; r += blockDim.x) {
-    const int b = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
-    float2 t;
-    if (pd.shift[dl]) t = tw[((b * (2 * kl + 1)) & (2 * blast - 1)) << (6 - lgbl)];
-    else t = tw[((b * kl) & (blast - 1)) << (7 - lgbl)];
-    twl[r] = t;
-  }
-  __syncthreads();
-  for (int o = tid; o < pd.bouter; o += blockDim.x) {
-    const float2* row = src + (size_t)o * blast;
-    float2 v = make_float2(0.f, 0.f);
-    for (int r = 0; r < blast; r += 2) {
-      if (blast >= 2) {
-        const float4 q = *reinterpret_cast<const float4*>(row + r);
-        v = cadd(v, cmul(make_float2(q.x, q.y), twl[r]));
-        v = cadd(v, cmul(make_float2(q.z, q.w), twl[r + 1]));
-      } else {
-        v = cmul(row[0], twl[0]);
-      }
-    }
+  for (int o = tid; o < bouter; o += blockDim.x) {
+    float2 v = __ldg(src + o);
+    for (int c = 1; c < nchunk; ++c) v = cadd(v, __ldg(src + (size_t)c * bouter + o));
     const int o0 = o >> lgb1, o1 = o & (b1 - 1);
-    int bb0 = (lp.sinv[0] * (o0 - lp.tau[0])) & (b0 - 1);
+    const int bb0 = (lp.sinv[0] * (o0 - lp.tau[0])) & (b0 - 1);
     if (pd.shift[0]) v = cmul(v, tw[bb0 << (6 - lgb0)]);
     int bb1 = 0;
     if (D == 3) {
@@ -879,12 +877,24 @@ __global__ void __launch_bounds__(kThreads) k_split_fft(PlanDev pd, const float2
   fft_axis_fast(V, lgb0, vstride, b1, lgb1, 0, 1, tw);
   const float gamma = lp.gamma;
   uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
-  for (int o = tid; o < pd.bouter; o += blockDim.x) {
+  for (int o = tid; o < bouter; o += blockDim.x) {
     int o0 = o >> lgb1, o1 = o & (b1 - 1);
     float2 v = V[o0 * vstride + o1];
     int64_t k = (int64_t)o * blast + kl;
     if (v.x * v.x + v.y * v.y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
     if (spectra) spectra[((size_t)frame * nl + l) * pd.btot + k] = v;
+  }
+}
+
+// Variant B helper: sum the dim-0 chunks of the folded spectra F [L][B_last][nchunk][B_outer]
+// into the canonical partial [L][B_last][B_outer] (in chunk order).
+__global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bouter, int64_t n, float2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / bouter, o = i - row * bouter;
+    const float2* s = F + row * nchunk * bouter + o;
+    float2 v = s[0];
+    for (int c = 1; c < nchunk; ++c) v = cadd(v, s[(size_t)c * bouter]);
+    out[i] = v;
   }
 }
 
@@ -1447,17 +1457,17 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
 // into residue sums R [batch][nl][B_outer][B_last]; zeroes zero_words bitmap words.
 template <int LP>
 static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
-                                       int64_t a0_base, int64_t a0_count, float2* R, uint32_t* zero_bm,
+                                       int64_t a0_base, int64_t a0_count, int* lg_out, uint32_t* zero_bm,
                                        int64_t zero_words, cudaStream_t st) {
   auto kern = p->n[p->D - 1] >= 64 ? k_split_fold<LP, kUSplit, 1> : k_split_fold<LP, kUSplit, 2>;
-  const int64_t bouter = p->dev.bouter, blast = p->b[p->D - 1];
+  const int64_t per = (int64_t)nl * p->btot;          // folded spectrum elements per frame and chunk
   int lg = split_lg_chunks(p, batch, nl, a0_count, (int64_t)p->num_sms * (kThreadsSplit / 32) * (LP >= 24 ? 1 : kCtasSplit));
-  while (lg > 0 && ((batch * bouter) << lg) * nl * blast > p->dev.parts_capacity) --lg;
-  if (lg > 0 && batch * bouter > p->dev.class_capacity) lg = 0;
+  while (lg > 0 && (batch << lg) * per > p->dev.fbuf_capacity) --lg;
+  if (batch * per > p->dev.fbuf_capacity) { set_error("split fold: batch exceeds the workspace"); return RSFT_E_ARG; }
   // more chunks if the per-warp weight tables do not fit (smaller dim-0 chunk per unit)
   const int64_t amin = p->D == 3 ? 1 : (int64_t)kUSplit * (p->n[p->D - 1] >= 64 ? 1 : 64 / p->n[p->D - 1]);
   while (split_smem_bytes(p, nl, LP, a0_count >> lg) > 227 * 1024 && (a0_count >> (lg + 1)) >= amin &&
-         ((batch * bouter) << (lg + 1)) * nl * blast <= p->dev.parts_capacity && batch * bouter <= p->dev.class_capacity)
+         (batch << (lg + 1)) * per <= p->dev.fbuf_capacity)
     ++lg;
   const size_t smem = split_smem_bytes(p, nl, LP, a0_count >> lg);
   if (smem > 227 * 1024) { set_error("k_split_fold: tables beyond shared memory"); return RSFT_E_UNSUPPORTED; }
@@ -1470,28 +1480,30 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
   s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreadsSplit, smem), "occupancy");
   if (s) return s;
   if (nb < 1) { set_error("k_split_fold: zero occupancy"); return RSFT_E_UNSUPPORTED; }
-  const int64_t wunits = (batch * bouter) << lg;
+  const int64_t wunits = (batch * p->dev.bouter) << lg;
   int64_t grid = (int64_t)nb * p->num_sms;
   const int64_t need = (wunits + kThreadsSplit / 32 - 1) / (kThreadsSplit / 32);
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kThreadsSplit, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg, R,
-                                                    zero_bm, zero_words);
+  kern<<<(unsigned)grid, kThreadsSplit, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg,
+                                                    p->dev.fbuf, zero_bm, zero_words);
   p->last_launches += 1;
+  *lg_out = lg;
   return check(cudaGetLastError(), "k_split_fold launch");
 }
 
-// Residue sums R (holding loops [rl0, rl0 + rnl)) -> bitmaps / spectra of loops [l0, l0 + nl).
-static rsft_status launch_split_fft(rsft_plan_s* p, const float2* R, int rl0, int rnl, int64_t batch, int l0,
-                                    int nl, uint32_t* bm, void* spectra, cudaStream_t st) {
+// Folded spectra F (loops [rl0, rl0 + rnl), nchunk chunks) -> bitmaps / spectra of loops [l0, l0 + nl).
+static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, int rnl, int nchunk, int64_t batch,
+                                    int l0, int nl, uint32_t* bm, void* spectra, cudaStream_t st) {
   const int D = p->D;
   const int64_t blast = p->b[D - 1];
   const int64_t b1 = D == 3 ? p->b[1] : 1;
-  size_t smem2 = (128 + kMaxB) * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
+  size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
   rsft_status s = check(cudaFuncSetAttribute(k_split_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2),
                         "smem attr");
   if (s) return s;
   dim3 grid2((unsigned)(nl * blast), (unsigned)batch);
-  k_split_fft<<<grid2, kThreads, smem2, st>>>(p->dev, R, rl0, rnl, l0, nl, bm, reinterpret_cast<float2*>(spectra));
+  k_split_fft<<<grid2, kThreadsFft, smem2, st>>>(p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
+                                                 reinterpret_cast<float2*>(spectra));
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_fft launch");
 }
@@ -1499,10 +1511,11 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* R, int rl0, in
 template <int LP>
 static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                   uint32_t* bm, void* spectra, cudaStream_t st) {
-  rsft_status s = launch_split_fold_t<LP>(p, d_x, batch, l0, nl, 0, p->a[0], p->dev.fbuf, bm,
+  int lg = 0;
+  rsft_status s = launch_split_fold_t<LP>(p, d_x, batch, l0, nl, 0, p->a[0], &lg, bm,
                                           batch * nl * (int64_t)p->dev.wpl, st);
   if (s) return s;
-  return launch_split_fft(p, p->dev.fbuf, l0, nl, batch, l0, nl, bm, spectra, st);
+  return launch_split_fft(p, p->dev.fbuf, l0, nl, 1 << lg, batch, l0, nl, bm, spectra, st);
 }
 
 #define RSFT_DISPATCH_LP(FN, LPV, ...)                   \

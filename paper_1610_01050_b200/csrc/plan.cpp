@@ -173,25 +173,19 @@ void layout_workspace(rsft_plan_s* p) {
     w.ht_off[d] = off;
     if (d + 1 < p->D) off = align256(off + sizeof(float) * (size_t)p->L * p->n[d]);
   }
+  // split mode: folded spectra per dim-0 chunk, sized for the largest batch x chunks product
+  // the launcher can choose (batch <= max_batch; chunks from split_lg_chunks)
   w.fbuf_off = off;
-  if (p->D >= 2) off = align256(off + (size_t)p->P.max_batch * p->L * p->btot * 8);
-  // split mode: per-chunk partials, sized for the chunking of batch = 1 (the most chunks;
-  // launches with more frames use fewer chunks and must fit, else fall back to fewer)
-  w.parts_off = off;
-  w.parts_bytes = 0;
-  w.cnt_capacity = 0;
+  w.fbuf_bytes = 0;
   if (p->D >= 2) {
-    const int64_t bouter = p->btot / p->b[p->D - 1];
-    int64_t best = 0;
-    for (int64_t b = 1; b <= p->P.max_batch && b <= 64; b *= 2) {
-      int lg = split_lg_chunks(p, b, p->L, p->a[0], (int64_t)148 * (kThreadsSplit / 32) * kCtasSplit);
-      if (lg > 0) best = std::max(best, (b * bouter << lg) * p->L * p->b[p->D - 1]);
-    }
-    w.parts_bytes = (size_t)best * 8;
-    off = align256(off + w.parts_bytes);
-    w.cnt_capacity = p->P.max_batch * bouter;
+    const int64_t warps = (int64_t)148 * (kThreadsSplit / 32) * kCtasSplit;
+    int64_t best = p->P.max_batch;
+    for (int64_t b = 1; b <= std::min<int64_t>(p->P.max_batch, 64); b *= 2)
+      best = std::max(best, b << split_lg_chunks(p, b, p->L, p->a[0], warps));
+    w.fbuf_bytes = (size_t)best * p->L * p->btot * 8;
+    off = align256(off + w.fbuf_bytes);
   }
-  w.cnt_off = off; off = align256(off + 4 * (size_t)w.cnt_capacity);
+
   int64_t dw = (p->ntot + 31) / 32;
   int64_t chunks = (p->P.max_batch * dw + kChunkWords - 1) / kChunkWords;
   w.chunk_capacity = chunks;
@@ -227,7 +221,7 @@ size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c) {
   SplitWarpLayout w = split_warp_layout(D, lpad, nl, (int)a0c, D == 3 ? (int)p->a[1] : 1, (int)p->b[D - 1], nseg,
                                         nlast >= 64 ? 1 : (int)(64 / nlast));
   const size_t hl = (size_t)lpad * nlast * 4;
-  return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0);
+  return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0) + 128 * 8;
 }
 
 // Split-mode work units are (frame, outer residue class, dim-0 chunk) per WARP.  Chunk the

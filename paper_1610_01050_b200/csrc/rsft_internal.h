@@ -16,7 +16,8 @@ constexpr int kMaxDim = 3;
 constexpr int kMaxLoops = 32;
 constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
 constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detection bitmap
-constexpr int kThreads = 256;          // CTA size of every kernel
+constexpr int kThreads = 256;          // CTA size of most kernels
+constexpr int kThreadsFft = 1024;      // split-mode outer FFT: one L2 round trip per thread
 constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
 constexpr int kU = 4;                  // 512 B row slots per ring stage
 #ifndef RSFT_NO_TMA
@@ -56,7 +57,8 @@ constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in 
 // Per-warp shared-memory carve-up of the split-mode fold (byte offsets inside a warp's
 // region): TMA ring, its mbarriers, double-buffered staged weights hs and the segment slot.
 // D == 2: hs rows = the chunk's a0 rows (row weights h0), zero-padded to a whole box;
-// D == 3: hs = A0c h0 rows + A1 h1 rows (zero-padded to a whole box).
+// D == 3: hs = A0c h0 rows + A1 h1 rows (zero-padded to a whole box).  slot [nl][B_last]:
+// the unit's folded residue sums (segments accumulate there).
 struct SplitWarpLayout {
   int ring, bars, hs, hs_stride, slot, total;
 };
@@ -70,7 +72,7 @@ RSFT_HD inline SplitWarpLayout split_warp_layout(int D, int lpad, int nl, int a0
   w.bars = off; off += ((kStagesSplit * 8 + 15) / 16) * 16;
   const int hs_rows = D == 3 ? a0c + split_pad_rows(a1, br) : split_pad_rows(a0c, br);
   w.hs = off; w.hs_stride = ((hs_rows * lpad * 4 + 15) / 16) * 16; off += 2 * w.hs_stride;
-  w.slot = off; off += nseg > 1 ? nl * blast * 8 : 0;
+  w.slot = off; off += nl * blast * 8;
   w.total = ((off + 127) / 128) * 128;
   return w;
 }
@@ -101,12 +103,9 @@ struct PlanDev {
   int32_t aouter;                  // prod_{d<D-1} A_d (rows per outer residue class)
   const LoopDev* loops;            // [L]
   const float* h[kMaxDim];         // [L][N_d] fp32 weight tables h_{l,d}[s] (I3)
-  float2* fbuf;                    // split mode residue sums [batch][L][B_tot] (k_split_fold -> k_split_fft)
+  float2* fbuf;                    // split mode folded spectra [batch][L][B_last][nchunk][B_outer] (fold -> FFT)
+  int64_t fbuf_capacity;           // float2 elements
   const float* ht[kMaxDim];        // d < D-1: class-major weights [B_d][A_d][L], ht[r][a][l] = h[l][r + B_d a]
-  float2* parts;                   // split mode per-chunk partial residue sums
-  int64_t parts_capacity;          // float2 elements
-  unsigned* class_cnt;             // split mode per-(frame, class) chunk counters (0 between launches)
-  int64_t class_capacity;
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
   const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
@@ -117,10 +116,9 @@ struct PlanDev {
 constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], parts_off, parts_bytes, cnt_off, fbuf_off, chunk_off, xmask_off, xmask_bytes, region_off, total;
+  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, total;
   int64_t region_capacity;
   int64_t chunk_capacity;
-  int64_t cnt_capacity;
 };
 
 }  // namespace rsft
