@@ -30,10 +30,10 @@ constexpr int kU = 4;                  // 512 B row slots per ring stage
 #define RSFT_NO_FOLD_COMPUTE 0
 #endif
 #ifndef RSFT_SPLIT_STAGES
-#define RSFT_SPLIT_STAGES 3
+#define RSFT_SPLIT_STAGES 2
 #endif
 #ifndef RSFT_SPLIT_U
-#define RSFT_SPLIT_U 8
+#define RSFT_SPLIT_U 16
 #endif
 #ifndef RSFT_SPLIT_THREADS
 #define RSFT_SPLIT_THREADS 256
