@@ -898,17 +898,6 @@ __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bo
   }
 }
 
-// ------------------------------------------------------------------------------------
-// K3 vote: one CTA per (prefix, frame).  Reverse mapping + accumulation + second stage
-// (Alg. 1 l.11-14; Def. 4; Eq. a_i), evaluated through identity I1
-// (Props. 3-4): abar[i] = sum_l c_l[M_l(i)] with M_l separable per dimension.
-// Word-parallel: for the row dim rd = D-2 and the last dim ld = D-1,
-//   E[l][k_rd][w] = 32-location mask {j : c_l[k_pre, k_rd, M_l,ld(32 w + j)] = 1}
-// (built with one ballot per word), so each (row, word) item costs one shared load per
-// loop plus an AND (mu = L), OR (mu = 1) or a bit-sliced counter add and compare (L10).
-// prefix = i0 for D == 3 (k_pre = M_l,0(i0)); D <= 2: one CTA per frame.
-// smem: bm [L][lw] (this CTA's slice of each loop's bitmap) | E [L][B_rd][W] | sig_rd [L]
-// ------------------------------------------------------------------------------------
 constexpr int kStageIdx = 2048;          // indices staged per CTA for coalesced writes
 
 // Block-wide exclusive scan of one int per thread; returns the prefix, *total = sum.
@@ -932,80 +921,85 @@ __device__ __forceinline__ int block_excl_scan(int c, int* wsum, int* total) {
 }
 
 // ------------------------------------------------------------------------------------
-// K3 vote (+ optional fused compaction): one CTA per region (frame, prefix).  Reverse
-// mapping + accumulation + second stage (Alg. 1 l.11-14; Def. 4; Eq. a_i
-// P:416-417), evaluated through identity I1 (Props. 3-4): abar[i] = sum_l
-// c_l[M_l(i)] with M_l separable per dimension.  Word-parallel: for the row dim rd = D-2
-// and the last dim ld = D-1,
-//   E[l][k_rd][w] = 32-location mask {j : c_l[k_pre, k_rd, M_l,ld(32 w + j)] = 1},
-// so each (row, word) item costs one shared load per loop plus an AND (mu = L), OR
-// (mu = 1) or a bit-sliced counter add and compare (L10).  prefix = i0 for D == 3
-// (k_pre = M_l,0(i0)); D <= 2: one region per frame.
-// KMAX > 0: also store this region's detection count (rstate[region]) for the offset scan
-// of rsft_detect_compact (no look-back; k_region_scan + k_region_write follow).
+// K3 vote (persistent).  Reverse mapping + accumulation + second stage (Alg. 1 l.11-14,
+// P:226-229; Def. 4; Eq. a_i), evaluated through identity I1 (Props. 3-4,
+// P:437-450): abar[i] = sum_l c_l[M_l(i)] with M_l separable per dimension.  A region is
+// (frame, prefix): prefix = i0 for D == 3 (k_pre = M_l,0(i0)); one region per frame for
+// D <= 2.  Word-parallel: for the row dim rd = D-2 and the last dim ld = D-1,
+//   E[l][k_rd][w] = {j : c_l[k_pre, k_rd, M_l,ld(32 w + j)] = 1}
+// (32 locations per word: OR of the plan-constant last-dim bucket masks X[l][k][w] over the
+// set bits of the bucket row, or one ballot per word), so each (row, CW words) item costs
+// one shared load per loop plus an AND (mu = L), OR (mu = 1) or a bit-sliced counter add
+// and compare (L10).  CTAs loop over regions; COUNT also stores each region's detection
+// count (rcount[region]) for the offset scan of rsft_detect_compact.
 // smem: bm [L][lw] | E [L][B_rd][W] | sig_rd [32] | X [L][B_last][W]
 // ------------------------------------------------------------------------------------
-template <int CW, int MODE, int KMAX>
-__global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
-                                                   int64_t d0b, int64_t d0e, int lw,
+template <int CW, int MODE, bool COUNT>
+__global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
+                                                   int64_t d0b, int64_t d0e, int lw, int64_t np, int64_t nregions,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
-                                                   unsigned long long* rstate, unsigned int* ticket,
-                                                   long long* __restrict__ idx, int64_t capacity,
-                                                   long long* __restrict__ d_count, int64_t nregions) {
+                                                   unsigned long long* __restrict__ rcount) {
   extern __shared__ __align__(16) uint32_t vsm[];
   __shared__ int wsum[kThreads / 32];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
   const int ld = D - 1;
   const int nld = pd.n[ld], lga_ld = pd.lga[ld];
   const int W = nld >> 5;                            // words per row of locations
+  const int lgW = __ffs(W) - 1;
   const int brd = D >= 2 ? pd.b[D - 2] : 1;
   const int blast = pd.blast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   uint32_t* bm = vsm;
   uint32_t* E = bm + (((size_t)L * lw + 3) & ~size_t(3));   // 16-B aligned for uint4 loads
   int* sig_rd = reinterpret_cast<int*>(E + (((size_t)L * brd * W + 3) & ~size_t(3)));
-  uint32_t* Xs = reinterpret_cast<uint32_t*>(sig_rd + kMaxLoops);   // [L][B_last][W] masks
-  const int tid = threadIdx.x;
-  const int64_t frame = blockIdx.y, prefix = blockIdx.x;
-  const int64_t i0 = d0b + prefix;                  // prefix (D == 3)
-
-  // this CTA's slice of every loop's first-stage bitmap
-  const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
+  uint32_t* Xs = reinterpret_cast<uint32_t*>(sig_rd + kMaxLoops);
   const int rowbits = brd * blast;                   // bits of one k_pre slab
-  for (int i = tid; i < L * lw; i += blockDim.x) {
-    int l = i / lw, w = i - l * lw;
-    int start = 0;
-    if (D == 3 && lw < wpl) {
-      const LoopDev& lp = pd.loops[l];
-      int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-      start = (kpre * rowbits) >> 5;
-    }
-    bm[i] = src[(size_t)l * wpl + start + w];
-  }
+  const int nrd = D >= 2 ? pd.n[D - 2] : 1;
+  const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
+  const int chunks = W / CW;
+  const int mu = pd.mu;
+  const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
+  const int64_t slab_words = slab_locs >> 5;
+
   for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
-  if (pd.xmask) {
+  if (pd.xmask) {                                    // plan-constant: once per CTA
     const int nx = L * blast * W;
-    if ((nx & 3) == 0) {
+    if ((nx & 3) == 0)
       for (int i = tid; i < (nx >> 2); i += blockDim.x)
         reinterpret_cast<uint4*>(Xs)[i] = __ldg(reinterpret_cast<const uint4*>(pd.xmask) + i);
-    } else {
+    else
       for (int i = tid; i < nx; i += blockDim.x) Xs[i] = __ldg(pd.xmask + i);
-    }
   }
-  __syncthreads();
-  if (pd.xmask) {
-    // E[l][krd][w] = OR over the set bits k of row pattern (k_pre, krd) of X[l][k][w]
-    // (X: plan-constant masks of the last-dim buckets).  Per lane, ~popcount iterations.
-    const int lgW = __ffs(W) - 1;
-    for (int l = 0; l < L; ++l) {
-      int base = 0;
-      if (D == 3) {
-        int kpre = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-        base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+
+  for (int64_t region = blockIdx.x; region < nregions; region += gridDim.x) {
+    __syncthreads();                                 // previous region's E / bm readers done
+    const int64_t frame = region / np, prefix = region - frame * np;
+    const int64_t i0 = d0b + prefix;
+
+    // this region's slice of every loop's first-stage bitmap
+    const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
+    for (int i = tid; i < L * lw; i += blockDim.x) {
+      const int l = i / lw, w = i - l * lw;
+      int start = 0;
+      if (D == 3 && lw < wpl) {
+        const int kpre = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+        start = (kpre * rowbits) >> 5;
       }
-      const uint32_t* b = bm + (size_t)l * lw;
-      const uint32_t* X = Xs + (size_t)l * blast * W;
-      for (int j = tid; j < brd * W; j += blockDim.x) {
-        const int krd = j >> lgW, w = j & (W - 1);
+      bm[i] = __ldg(src + (size_t)l * wpl + start + w);
+    }
+    __syncthreads();
+    // E[l][krd][w] (all loops at once)
+    if (pd.xmask) {
+      for (int j = tid; j < L * brd * W; j += blockDim.x) {
+        const int l = j / (brd * W), rem = j - l * (brd * W);
+        const int krd = rem >> lgW, w = rem & (W - 1);
+        int base = 0;
+        if (D == 3) {
+          const int kpre = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+        }
+        const uint32_t* b = bm + (size_t)l * lw;
+        const uint32_t* X = Xs + (size_t)l * blast * W;
         const int f0 = base + krd * blast;
         uint32_t e = 0;
         if (blast <= 32) {
@@ -1020,136 +1014,129 @@ __global__ void __launch_bounds__(kThreads) k_vote(PlanDev pd, const uint32_t* _
           while (lo) { const int k = __ffs(lo) - 1; lo &= lo - 1; e |= X[k * W + w]; }
           while (hi) { const int k = __ffs(hi) + 31; hi &= hi - 1; e |= X[k * W + w]; }
         }
-        E[((size_t)l * brd + krd) * W + w] = e;
+        E[j] = e;
+      }
+    } else {                                         // ballots: warp per (l, w)
+      for (int it = warp; it < L * W; it += nwarps) {
+        const int l = it / W, w = it - l * W;
+        const LoopDev& lp = pd.loops[l];
+        int base = 0;
+        if (D == 3) {
+          const int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+        }
+        const int ilast = (w << 5) + lane;
+        const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
+        const uint32_t* b = bm + (size_t)l * lw;
+        for (int krd = 0; krd < brd; ++krd) {
+          const int flat = base + krd * blast + klast;
+          const uint32_t word = __ballot_sync(0xffffffffu, (b[flat >> 5] >> (flat & 31)) & 1u);
+          if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+        }
       }
     }
-  } else {
-    // E via ballots: warp per (l, w); lane j owns location 32 w + j of the last dim
-    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    for (int it = warp; it < L * W; it += nwarps) {
-      const int l = it / W, w = it - l * W;
-      const LoopDev& lp = pd.loops[l];
-      int base = 0;
-      if (D == 3) {
-        int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-        base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
-      }
-      const int ilast = (w << 5) + lane;
-      const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
-      const uint32_t* b = bm + (size_t)l * lw;
-      for (int krd = 0; krd < brd; ++krd) {
-        int flat = base + krd * blast + klast;
-        uint32_t bit = (b[flat >> 5] >> (flat & 31)) & 1u;
-        uint32_t word = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
-      }
-    }
-  }
-  __syncthreads();
-  int64_t rbeg, rend, out_base;
-  const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
-  const int64_t slab_words = slab_locs >> 5;
-  if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * W; }
-  else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
-  else { rbeg = 0; rend = 1; out_base = 0; }
-  const int nrd = D >= 2 ? pd.n[D - 2] : 1;
-  const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
-  const int chunks = W / CW;
-  const int64_t nitems = (rend - rbeg) * chunks;
-  const int mu = pd.mu;
+    __syncthreads();
+    int64_t rbeg, rend, out_base;
+    if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * W; }
+    else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
+    else { rbeg = 0; rend = 1; out_base = 0; }
+    const int64_t nitems = (rend - rbeg) * chunks;
 
-  // one item = CW consecutive detection words of one row
-  auto vote_item = [&](int64_t it, uint32_t (&acc)[CW]) {
-    const int64_t ri = it / chunks;
-    const int w0 = (int)(it - ri * chunks) * CW;
-    const int64_t row = rbeg + ri;
-    uint32_t pl[CW][6];
-#pragma unroll
-    for (int c = 0; c < CW; ++c) {
-      acc[c] = MODE == 0 ? 0xffffffffu : 0u;
-#pragma unroll
-      for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
-    }
-    for (int l = 0; l < L; ++l) {
-      // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
-      const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
-      const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
-      uint32_t m[CW];
-      if (CW == 4) {
-        uint4 v = *reinterpret_cast<const uint4*>(e);
-        m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y; m[CW > 2 ? 2 : 0] = v.z; m[CW > 3 ? 3 : 0] = v.w;
-      } else if (CW == 2) {
-        uint2 v = *reinterpret_cast<const uint2*>(e);
-        m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
-      } else {
-        m[0] = e[0];
-      }
-      uint32_t any = 0;
+    // one item = CW consecutive detection words of one row
+    auto vote_item = [&](int64_t it, uint32_t (&acc)[CW]) {
+      const int64_t ri = it / chunks;
+      const int w0 = (int)(it - ri * chunks) * CW;
+      const int64_t row = rbeg + ri;
+      uint32_t pl[CW][6];
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        if (MODE == 0) { acc[c] &= m[c]; any |= acc[c]; }
-        else if (MODE == 1) acc[c] |= m[c];
-        else {
-          uint32_t carry = m[c];
+        acc[c] = MODE == 0 ? 0xffffffffu : 0u;
 #pragma unroll
-          for (int b = 0; b < 6; ++b) {
-            uint32_t t = pl[c][b] & carry;
-            pl[c][b] ^= carry;
-            carry = t;
+        for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
+      }
+      for (int l = 0; l < L; ++l) {
+        // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
+        const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
+        const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
+        uint32_t m[CW];
+        if (CW == 4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(e);
+          m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y; m[CW > 2 ? 2 : 0] = v.z; m[CW > 3 ? 3 : 0] = v.w;
+        } else if (CW == 2) {
+          const uint2 v = *reinterpret_cast<const uint2*>(e);
+          m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
+        } else {
+          m[0] = e[0];
+        }
+        uint32_t any = 0;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          if (MODE == 0) { acc[c] &= m[c]; any |= acc[c]; }
+          else if (MODE == 1) acc[c] |= m[c];
+          else {
+            uint32_t carry = m[c];
+#pragma unroll
+            for (int b = 0; b < 6; ++b) {
+              const uint32_t t = pl[c][b] & carry;
+              pl[c][b] ^= carry;
+              carry = t;
+            }
+          }
+        }
+        if (MODE == 0 && any == 0) break;              // unanimity already impossible
+      }
+      if (MODE == 2) {                                 // bit-sliced compare: count >= mu
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+          for (int b = 5; b >= 0; --b) {
+            if ((mu >> b) & 1) eq &= pl[c][b];
+            else { gt |= eq & pl[c][b]; eq &= ~pl[c][b]; }
+          }
+          acc[c] = gt | eq;
+        }
+      }
+      const int64_t widx = out_base + ri * W + w0;
+      if (detect) {
+        uint32_t* dst = detect + frame * slab_words + widx;
+        if (CW == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(acc[0], acc[CW > 1 ? 1 : 0], acc[CW > 2 ? 2 : 0], acc[CW > 3 ? 3 : 0]);
+        else if (CW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(acc[0], acc[CW > 1 ? 1 : 0]);
+        else dst[0] = acc[0];
+      }
+      if (MODE == 2 && counts) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          uint8_t* cdst = counts + frame * slab_locs + (widx + c) * 32;
+          for (int j = 0; j < 32; ++j) {
+            int v = 0;
+#pragma unroll
+            for (int b = 0; b < 6; ++b) v |= ((pl[c][b] >> j) & 1u) << b;
+            cdst[j] = (uint8_t)v;
           }
         }
       }
-      if (MODE == 0 && any == 0) break;              // unanimity already impossible
-    }
-    if (MODE == 2) {                                 // bit-sliced compare: count >= mu
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        uint32_t gt = 0u, eq = 0xffffffffu;
-#pragma unroll
-        for (int b = 5; b >= 0; --b) {
-          if ((mu >> b) & 1) eq &= pl[c][b];
-          else { gt |= eq & pl[c][b]; eq &= ~pl[c][b]; }
-        }
-        acc[c] = gt | eq;
-      }
-    }
-    const int64_t widx = out_base + ri * W + w0;
-    uint32_t* dst = detect + frame * slab_words + widx;
-    if (CW == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(acc[0], acc[CW > 1 ? 1 : 0], acc[CW > 2 ? 2 : 0], acc[CW > 3 ? 3 : 0]);
-    else if (CW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(acc[0], acc[CW > 1 ? 1 : 0]);
-    else dst[0] = acc[0];
-    if (MODE == 2 && counts) {
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        uint8_t* cdst = counts + frame * slab_locs + (widx + c) * 32;
-        for (int j = 0; j < 32; ++j) {
-          int v = 0;
-#pragma unroll
-          for (int b = 0; b < 6; ++b) v |= ((pl[c][b] >> j) & 1u) << b;
-          cdst[j] = (uint8_t)v;
-        }
-      }
-    }
-  };
+    };
 
-  int cnt = 0;
-  for (int64_t it = tid; it < nitems; it += blockDim.x) {
-    uint32_t acc[CW];
-    vote_item(it, acc);
-    if (KMAX > 0) {
+    int cnt = 0;
+    for (int64_t it = tid; it < nitems; it += blockDim.x) {
+      uint32_t acc[CW];
+      vote_item(it, acc);
+      if (COUNT) {
 #pragma unroll
-      for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+        for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+      }
     }
-  }
-  if (KMAX > 0) {                                    // this region's detection count
+    if (COUNT) {                                     // this region's detection count
 #pragma unroll
-    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    if ((tid & 31) == 0) wsum[tid >> 5] = cnt;
-    __syncthreads();
-    if (tid == 0) {
-      long long t = 0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
-      rstate[frame * gridDim.x + prefix] = (unsigned long long)t;
+      for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+      if (lane == 0) wsum[warp] = cnt;
+      __syncthreads();
+      if (tid == 0) {
+        long long t = 0;
+        for (int i = 0; i < nwarps; ++i) t += wsum[i];
+        rcount[region] = (unsigned long long)t;
+      }
     }
   }
 }
@@ -1544,62 +1531,67 @@ static int64_t vote_regions_per_frame(const rsft_plan_s* p, int64_t d0b, int64_t
   return p->D == 3 ? d0e - d0b : 1;
 }
 
-template <int CW, int MODE, int KMAX>
-static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                                 uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
-                                 int64_t* d_count, cudaStream_t st) {
+// Shared memory of k_vote and the bitmap slice width lw (words per loop it loads).
+static size_t vote_smem(const rsft_plan_s* p, int* lw_out) {
   const int D = p->D;
   const int64_t W = p->n[D - 1] / 32;
   const int64_t brd = D >= 2 ? p->b[D - 2] : 1;
   const int64_t wpl = p->dev.wpl;
   const int64_t rowbits = brd * p->b[D - 1];
   const int lw = (D == 3 && rowbits % 32 == 0) ? (int)(rowbits / 32) : (int)wpl;
-  size_t smem = (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (((size_t)p->L * brd * W + 3) & ~size_t(3)) * 4 +
-                kMaxLoops * 4 + p->ws.xmask_bytes;
-  auto kern = k_vote<CW, MODE, KMAX>;
+  *lw_out = lw;
+  const size_t xw = p->dev.xmask ? (size_t)p->L * p->b[D - 1] * W : 0;
+  return (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (((size_t)p->L * brd * W + 3) & ~size_t(3)) * 4 +
+         kMaxLoops * 4 + ((xw + 3) & ~size_t(3)) * 4;
+}
+
+template <int CW, int MODE, bool COUNT>
+static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                                 uint32_t* det, uint8_t* counts, cudaStream_t st) {
+  int lw = 0;
+  const size_t smem = vote_smem(p, &lw);
+  auto kern = k_vote<CW, MODE, COUNT>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   const int64_t np = vote_regions_per_frame(p, d0b, d0e);
   const int64_t nregions = np * batch;
-  unsigned long long* rstate = p->dev.region_state;
-  unsigned int* ticket = reinterpret_cast<unsigned int*>(rstate + nregions);
-  if (KMAX > 0 && nregions > p->dev.region_capacity) return RSFT_E_WORKSPACE;
-  dim3 grid((unsigned)np, (unsigned)batch);
-  kern<<<grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, det, counts, rstate, ticket,
-                                     reinterpret_cast<long long*>(idx), capacity,
-                                     reinterpret_cast<long long*>(d_count), nregions);
+  if (COUNT && nregions > p->dev.region_capacity) return RSFT_E_WORKSPACE;
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem), "occupancy");
+  if (s) return s;
+  if (nb < 1) { set_error("k_vote: zero occupancy"); return RSFT_E_UNSUPPORTED; }
+  int64_t grid = (int64_t)nb * p->num_sms;
+  if (grid > nregions) grid = nregions;
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, np, nregions, det, counts,
+                                               p->dev.region_state);
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_vote launch");
 }
 
-template <int CW, int KMAX>
+template <bool COUNT>
 static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                                    uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
-                                    int64_t* d_count, cudaStream_t st) {
-  if (!counts && p->mu == p->L) return launch_vote_t<CW, 0, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
-  if (!counts && p->mu == 1) return launch_vote_t<CW, 1, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
-  return launch_vote_t<CW, 2, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
-}
-
-template <int KMAX>
-static rsft_status launch_vote_cw(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
-                                  uint32_t* det, uint8_t* counts, int64_t* idx, int64_t capacity,
-                                  int64_t* d_count, cudaStream_t st) {
+                                    uint32_t* det, uint8_t* counts, cudaStream_t st) {
   const int64_t W = p->n[p->D - 1] / 32;
-  if (W % 4 == 0) return launch_vote_mode<4, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
-  if (W % 2 == 0) return launch_vote_mode<2, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
-  return launch_vote_mode<1, KMAX>(p, bm, batch, d0b, d0e, det, counts, idx, capacity, d_count, st);
+  const int mode = (!counts && p->mu == p->L) ? 0 : (!counts && p->mu == 1) ? 1 : 2;
+#define RSFT_VOTE_CASE(CWV, MV) \
+  if (W % CWV == 0 && mode == MV) return launch_vote_t<CWV, MV, COUNT>(p, bm, batch, d0b, d0e, det, counts, st);
+  RSFT_VOTE_CASE(4, 0) RSFT_VOTE_CASE(4, 1) RSFT_VOTE_CASE(4, 2)
+  RSFT_VOTE_CASE(2, 0) RSFT_VOTE_CASE(2, 1) RSFT_VOTE_CASE(2, 2)
+  RSFT_VOTE_CASE(1, 0) RSFT_VOTE_CASE(1, 1) RSFT_VOTE_CASE(1, 2)
+#undef RSFT_VOTE_CASE
+  return RSFT_E_UNSUPPORTED;
 }
 
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st) {
-  return launch_vote_cw<0>(p, bm, batch, d0b, d0e, det, counts, nullptr, 0, nullptr, st);
+  return launch_vote_mode<false>(p, bm, batch, d0b, d0e, det, counts, st);
 }
 
+// vote (+ per-region counts) -> offset scan -> per-region sorted index writes
 rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                   int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st) {
   const int64_t n0 = p->n[0];
-  rsft_status s = launch_vote_cw<1>(p, bm, batch, 0, n0, det, nullptr, nullptr, 0, nullptr, st);
+  rsft_status s = launch_vote_mode<true>(p, bm, batch, 0, n0, det, nullptr, st);
   if (s) return s;
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
