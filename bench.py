@@ -324,20 +324,30 @@ def main_gpu(a):
 
 def bench_c5(a, wl, rank, world, dev):
     """Single 512 MiB cube, L=16 loops sharded over ranks, NCCL all-gather of the per-loop
-    bitmaps (2 KiB/loop), then voting on this rank's dim-0 slab (BASELINE configs[4])."""
+    bitmaps (2 KiB/loop), then voting on this rank's dim-0 slab (BASELINE configs[4]).
+    Variant B (default): each rank folds only its dim-0 slab for all loops
+    (rsft_bucketize_partial), the partial folded spectra are reduce-scattered over loops
+    (NCCL), each rank finalizes its loops (rsft_finalize).  Variant A: each rank reads the
+    whole cube for its loops (rsft_execute loop range)."""
     import torch
     import torch.distributed as dist
     from paper_1610_01050_b200 import rsft as B
+    from paper_1610_01050_b200 import shard
 
     stream = torch.cuda.current_stream()
     plan = B.Plan(wl.n, wl.b, wl.loops, p_fa=wl.p_fa, noise_var=wl.noise_var, seed=wl.sched_seed,
                   mu=wl.mu, max_batch=1).bind()
-    from paper_1610_01050_b200 import shard
     L = wl.loops
     lb, le = shard.loop_range(rank, world, L)
     n0 = wl.n[0]
     d0b, d0e = shard.slab_range(rank, world, n0, plan.ntot // n0)
-    x = torch.from_numpy(synth.gen_batch(wl, [0])).to(dev)
+    hx = synth.gen_batch(wl, [0])
+    if a.c5_variant == "B":
+        x = torch.from_numpy(np.ascontiguousarray(hx[0, d0b:d0e])).to(dev)     # this rank's slab only
+        partial = torch.empty((L, plan.btot), dtype=torch.complex64, device=dev)
+    else:
+        x = torch.from_numpy(hx).to(dev)
+    del hx
     mine = plan.new_bitmaps(1, le - lb)
     slab_words = (d0e - d0b) * (plan.ntot // n0) // 32
     det = torch.empty((1, slab_words), dtype=torch.int32, device=dev)
@@ -345,8 +355,15 @@ def bench_c5(a, wl, rank, world, dev):
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        plan.execute(x, loop_begin=lb, loop_end=le, bitmaps=mine)
-        n = plan.last_launch_count()
+        if a.c5_variant == "B":
+            plan.bucketize_partial(x, d0b, partial=partial)
+            n = plan.last_launch_count()
+            folded = shard.reduce_scatter_loops(partial, world)
+            plan.finalize(folded, loop_begin=lb, loop_end=le, bitmaps=mine[0])
+            n += plan.last_launch_count()
+        else:
+            plan.execute(x, loop_begin=lb, loop_end=le, bitmaps=mine)
+            n = plan.last_launch_count()
         if ev is not None:
             ev[1].record(stream)
         src = shard.gather_loop_bitmaps(mine[0], world).reshape(1, L, plan.bitmap_words)
@@ -380,16 +397,23 @@ def bench_c5(a, wl, rank, world, dev):
     step_ms = float(el.item()) / a.steps
     k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     peak, peak_src = load_peaks()
-    algo = 8 * plan.ntot + (le - lb) * plan.bitmap_words * 4
+    cube_bytes = 8 * plan.ntot
+    algo = (cube_bytes // world if a.c5_variant == "B" else cube_bytes) + (le - lb) * plan.bitmap_words * 4
     out = {
         "metric": METRIC, "value": 1000.0 / step_ms, "unit": "cubes/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic: 1 seeded Eq. sig_model cube",
-        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": L,
-                   "parallelism": f"loops sharded {world} ways + NCCL all-gather of bitmaps"},
+        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": L, "variant": a.c5_variant,
+                   "l2": "cube 512 MiB >> 126 MB L2 (no flush needed)",
+                   "parallelism": (f"dim-0 slabs over {world} GPU(s), partial folds reduce-scattered over loops "
+                                   f"(NCCL), loops finalized per rank, NCCL all-gather of bitmaps"
+                                   if a.c5_variant == "B" else
+                                   f"loops sharded {world} ways + NCCL all-gather of bitmaps")},
         "roofline": {"bound": "hbm", "achieved": algo / (k1 / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": algo / (k1 / 1000.0) / 1e9 / peak, "traffic": load_traffic(wl.name),
-                     "kernel": "k_split_fold + k_split_fft", "avg_launch_ms": k1, "peak_source": peak_src},
+                     "kernel": "k_split_fold + k_split_fft (first stage of this rank)",
+                     "algorithmic_bytes_per_launch": algo, "avg_launch_ms": k1,
+                     "share_of_step": k1 / step_ms, "peak_source": peak_src},
         "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None, "e2e": None,
     }
     print(json.dumps(out), flush=True)
@@ -410,6 +434,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--c5-variant", default="B", choices=["A", "B"], help="c5 multi-GPU scheme (DESIGN.md §8)")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3

@@ -135,6 +135,32 @@ rsft_status rsft_bind(rsft_plan_t plan, void* d_workspace, size_t bytes, void* s
 rsft_status rsft_execute(rsft_plan_t plan, const void* d_x, int64_t batch, int32_t loop_begin,
                          int32_t loop_end, uint32_t* d_bitmaps, void* d_spectra, void* stream);
 
+/* Slab sharding of ONE frame (SURVEY §8(e) variant B).  Pre-window, permutation, flat
+ * window and aliasing (Alg. 1 l.5-8) are linear in x (Eqs. z, l: P:272-279), so
+ * dim-0 slabs produce partial folded spectra that add up (in any order, up to fp32 rounding)
+ * to the whole frame's.  Split mode (D >= 2) only.
+ *   d_x_slab   device complex64 [dim0_len][N_1]...[N_{D-1}]: rows [dim0_offset,
+ *              dim0_offset + dim0_len) of one frame, 16-byte aligned.
+ *   dim0_offset, dim0_len: multiples of B_0, dim0_len > 0, offset + len <= N_0.
+ *   d_partial  device complex64 [L][B_last][B_tot / B_last] (all loops of the plan): the
+ *              slab's folded spectrum after the last-dim DFT (the last-dim relabelling and
+ *              half-bucket twiddle applied), indexed [l][k_last][outer residue class];
+ *              overwritten.  Sum the partials of all slabs, then call rsft_finalize.
+ * Errors: E_ARG (range, alignment, null), E_UNSUPPORTED (fused-mode plan), E_STATE, E_CUDA. */
+rsft_status rsft_bucketize_partial(rsft_plan_t plan, const void* d_x_slab, int64_t dim0_offset, int64_t dim0_len,
+                                   void* d_partial, void* stream);
+
+/* Finish the first stage of loops [loop_begin, loop_end) from summed folded spectra
+ * (Alg. 1 l.9-10): outer relabelling + half-bucket twiddles, outer-dims FFT, |.|^2 > gamma_l.
+ *   d_folded   device complex64 [loop_end-loop_begin][B_last][B_tot / B_last]: rows
+ *              loop_begin.. of the rsft_bucketize_partial layout, summed over slabs (e.g. this
+ *              rank's block after a reduce-scatter over loops).
+ *   d_bitmaps  device uint32 [loop_end-loop_begin][bitmap_words] (overwritten).
+ *   d_spectra  NULL or device complex64 [loop_end-loop_begin][B_tot].
+ * Errors: E_ARG, E_UNSUPPORTED (fused-mode plan), E_STATE, E_CUDA. */
+rsft_status rsft_finalize(rsft_plan_t plan, const void* d_folded, int32_t loop_begin, int32_t loop_end,
+                          uint32_t* d_bitmaps, void* d_spectra, void* stream);
+
 /* Reverse mapping + accumulation + second-stage test (Alg. 1 l.11-14) for locations whose
  * dim-0 index lies in [dim0_begin, dim0_end) (sharded voting; full range = [0, N_0)):
  *   d_bitmaps  device uint32 [batch][L][bitmap_words] — ALL loops of the plan.

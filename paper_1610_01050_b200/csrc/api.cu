@@ -9,6 +9,10 @@
 namespace rsft {
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                            void* spectra, cudaStream_t st);
+rsft_status launch_partial(rsft_plan_s* p, const void* d_x, int64_t off, int64_t len, void* d_partial,
+                           cudaStream_t st);
+rsft_status launch_finalize(rsft_plan_s* p, const void* d_folded, int l0, int nl, uint32_t* bm, void* spectra,
+                            cudaStream_t st);
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st);
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
@@ -120,6 +124,28 @@ rsft_status rsft_execute(rsft_plan_t p, const void* d_x, int64_t batch, int32_t 
   if (batch == 0) return RSFT_OK;
   return launch_execute(p, d_x, batch, loop_begin, loop_end - loop_begin, d_bitmaps, d_spectra,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+rsft_status rsft_bucketize_partial(rsft_plan_t p, const void* d_x_slab, int64_t off, int64_t len, void* d_partial,
+                                   void* stream) {
+  if (!p || !d_x_slab || !d_partial) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (p->D < 2 || resolve_mode(p, 1) != RSFT_MODE_SPLIT) return RSFT_E_UNSUPPORTED;
+  if (off < 0 || len <= 0 || off + len > p->n[0] || off % p->b[0] || len % p->b[0]) return RSFT_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_x_slab) & 15) || (reinterpret_cast<uintptr_t>(d_partial) & 7)) return RSFT_E_ARG;
+  p->last_launches = 0;
+  return launch_partial(p, d_x_slab, off, len, d_partial, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rsft_status rsft_finalize(rsft_plan_t p, const void* d_folded, int32_t loop_begin, int32_t loop_end,
+                          uint32_t* d_bitmaps, void* d_spectra, void* stream) {
+  if (!p || !d_folded || !d_bitmaps) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (p->D < 2 || resolve_mode(p, 1) != RSFT_MODE_SPLIT) return RSFT_E_UNSUPPORTED;
+  if (loop_begin < 0 || loop_end > p->L || loop_begin >= loop_end) return RSFT_E_ARG;
+  p->last_launches = 0;
+  return launch_finalize(p, d_folded, loop_begin, loop_end - loop_begin, d_bitmaps, d_spectra,
+                         reinterpret_cast<cudaStream_t>(stream));
 }
 
 rsft_status rsft_detect(rsft_plan_t p, const uint32_t* d_bitmaps, int64_t batch, int64_t d0b, int64_t d0e,

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <string>
 
@@ -1517,6 +1518,32 @@ static rsft_status launch_split_t(rsft_plan_s* p, const void* d_x, int64_t batch
     case 32: return FN<32>(__VA_ARGS__);                 \
     default: return RSFT_E_UNSUPPORTED;                  \
   }
+
+template <int LP>
+static rsft_status launch_partial_t(rsft_plan_s* p, const void* d_x, int64_t off, int64_t len, void* d_partial,
+                                    cudaStream_t st) {
+  int lg = 0;
+  rsft_status s = launch_split_fold_t<LP>(p, d_x, 1, 0, p->L, off / p->b[0], len / p->b[0], &lg, nullptr, 0, st);
+  if (s) return s;
+  const int64_t bouter = p->dev.bouter;
+  const int64_t n = (int64_t)p->L * p->btot;
+  k_chunk_sum<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * p->num_sms), 256, 0, st>>>(
+      p->dev.fbuf, 1 << lg, bouter, n, reinterpret_cast<float2*>(d_partial));
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_chunk_sum launch");
+}
+
+rsft_status launch_partial(rsft_plan_s* p, const void* d_x, int64_t off, int64_t len, void* d_partial,
+                           cudaStream_t st) {
+  RSFT_DISPATCH_LP(launch_partial_t, loop_pad(p->L), p, d_x, off, len, d_partial, st);
+}
+
+rsft_status launch_finalize(rsft_plan_s* p, const void* d_folded, int l0, int nl, uint32_t* bm, void* spectra,
+                            cudaStream_t st) {
+  rsft_status s = check(cudaMemsetAsync(bm, 0, (size_t)nl * p->dev.wpl * 4, st), "bitmap reset");
+  if (s) return s;
+  return launch_split_fft(p, reinterpret_cast<const float2*>(d_folded), l0, nl, 1, 1, l0, nl, bm, spectra, st);
+}
 
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                            void* spectra, cudaStream_t st) {

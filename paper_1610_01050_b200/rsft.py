@@ -66,6 +66,8 @@ def lib():
         "rsft_workspace_bytes": (c_size_t, [c_void_p]),
         "rsft_bind": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
         "rsft_execute": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+        "rsft_bucketize_partial": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+        "rsft_finalize": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
         "rsft_detect": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
         "rsft_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
         "rsft_detect_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
@@ -87,7 +89,8 @@ def lib():
 
 EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsft_set_schedule",
             "rsft_get_schedule", "rsft_get_thresholds", "rsft_get_window", "rsft_get_info",
-            "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_detect", "rsft_compact",
+            "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_bucketize_partial", "rsft_finalize",
+            "rsft_detect", "rsft_compact",
             "rsft_detect_compact",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
             "rsft_last_error"]
@@ -226,6 +229,34 @@ class Plan:
         sp = c_void_p(spectra.data_ptr()) if spectra is not None else None
         _check(lib().rsft_execute(self._h, c_void_p(x.data_ptr()), batch, loop_begin, loop_end,
                                   c_void_p(bitmaps.data_ptr()), sp, _stream_handle(stream)))
+        return bitmaps
+
+    def bucketize_partial(self, x_slab, dim0_offset, partial=None, stream=None):
+        """Folded spectrum [L, B_tot] (layout [l][k_last][outer class]) of the dim-0 slab
+        x_slab = rows [dim0_offset, dim0_offset + len) of one frame (variant B, linear in x)."""
+        import torch
+        self._need_bind()
+        assert x_slab.dtype == torch.complex64 and x_slab.is_cuda and x_slab.is_contiguous()
+        assert tuple(x_slab.shape[1:]) == self.n[1:]
+        if partial is None:
+            partial = torch.empty((self.loops, self.btot), dtype=torch.complex64, device=self.device)
+        _check(lib().rsft_bucketize_partial(self._h, c_void_p(x_slab.data_ptr()), dim0_offset, x_slab.shape[0],
+                                            c_void_p(partial.data_ptr()), _stream_handle(stream)))
+        return partial
+
+    def finalize(self, folded, loop_begin=0, loop_end=None, bitmaps=None, spectra=None, stream=None):
+        """Bitmaps [loop_end - loop_begin, words] from summed folded spectra
+        [loop_end - loop_begin, B_tot] (those loops' rows of the partial layout)."""
+        import torch
+        self._need_bind()
+        loop_end = self.loops if loop_end is None else loop_end
+        assert folded.dtype == torch.complex64 and folded.is_cuda and folded.is_contiguous()
+        assert folded.shape[0] == loop_end - loop_begin
+        if bitmaps is None:
+            bitmaps = torch.empty((loop_end - loop_begin, self.bitmap_words), dtype=torch.int32, device=self.device)
+        sp = c_void_p(spectra.data_ptr()) if spectra is not None else None
+        _check(lib().rsft_finalize(self._h, c_void_p(folded.data_ptr()), loop_begin, loop_end,
+                                   c_void_p(bitmaps.data_ptr()), sp, _stream_handle(stream)))
         return bitmaps
 
     def detect(self, bitmaps, dim0=None, detect=None, counts=None, stream=None):

@@ -2,10 +2,15 @@
 
 c4-style batches: frames are independent -> each rank owns a contiguous frame range,
 no data-path collective.
-c5-style single cube (BASELINE configs[4]): the L loops are sharded over ranks, each rank
-computes the first-stage bitmaps of its loops (rsft_execute loop range), the per-loop
-bitmaps are all-gathered over NCCL (2 KiB per loop at c5), then every rank votes on its own
-dim-0 slab of locations (rsft_detect dim0 range).
+c5-style single cube (BASELINE configs[4]): the L loops are sharded over ranks and the
+per-loop bitmaps are all-gathered over NCCL (2 KiB per loop at c5) before every rank votes on
+its own dim-0 slab of locations (rsft_detect dim0 range).
+  variant A: every rank reads the whole cube and computes the bitmaps of its loops
+             (rsft_execute loop range);
+  variant B: every rank folds only its dim-0 slab of the cube for all loops
+             (rsft_bucketize_partial; the fold is linear in x), the partial folded spectra are
+             reduce-scattered over loops (2 MiB at c5), and each rank finalizes its loops
+             (rsft_finalize) -- HBM traffic per rank drops to cube/G.
 """
 from __future__ import annotations
 
@@ -44,3 +49,24 @@ def gather_loop_bitmaps(local, world: int, group=None):
     out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     return out
+
+
+def reduce_scatter_loops(partial, world: int, group=None):
+    """Sum the slab partials [L, B_tot] over ranks and keep this rank's loop block
+    [L / world, B_tot] (loop order = rank order).  NCCL: reduce_scatter_tensor; backends
+    without it (gloo, CPU tests): all_reduce + slice."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return partial
+    L = partial.shape[0]
+    if L % world:
+        raise ValueError(f"loops={L} must divide evenly over {world} ranks")
+    rank = dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((L // world,) + tuple(partial.shape[1:]), dtype=partial.dtype, device=partial.device)
+        dist.reduce_scatter_tensor(out, partial.contiguous(), group=group)
+        return out
+    full = partial.clone()
+    dist.all_reduce(full, group=group)
+    return full[rank * L // world:(rank + 1) * L // world].contiguous()

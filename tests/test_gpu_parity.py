@@ -192,3 +192,73 @@ def test_parity_c5_full_cube():
     wl = synth.C5
     x = frames(wl, 1)
     run_case(wl_params(wl), x)
+
+
+# ----------------------------------------------------------------------------- variant B
+def _slab_run(plan, x, slabs):
+    import torch
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    folded = None
+    for a, e in slabs:
+        part = plan.bucketize_partial(xt[0, a:e].contiguous(), a)
+        folded = part.clone() if folded is None else folded + part
+    sp = torch.empty((plan.loops, plan.btot), dtype=torch.complex64, device="cuda")
+    bm = plan.finalize(folded, spectra=sp)
+    return folded, bm, sp
+
+
+@pytest.mark.parametrize("n,b,L,slabs", [
+    ((64, 32, 32), (8, 4, 8), 6, [(0, 16), (16, 40), (40, 64)]),
+    ((128, 64), (16, 16), 4, [(0, 64), (64, 128)]),
+    ((32, 16, 64), (4, 4, 8), 12, [(0, 8), (8, 12), (12, 32)]),
+])
+def test_variant_b_slab_partials(n, b, L, slabs):
+    """Slab partial folds (linear in x) summed + rsft_finalize == the whole-frame first stage:
+    buckets vs the oracle within 1e-4, bits exact outside the band; loop-sharded finalize
+    returns the matching rows."""
+    import torch
+    op = oracle_params(n, b, L, p_fa=1e-3, seed=21, random_tau=True)
+    wl = synth.Workload("vb", n, b, L, 1e-3, 1.0, (3, 8), (0.0, 20.0), 1, data_seed=12)
+    x = frames(wl, 1)
+    plan = make_plan(op, max_batch=1, mode="split").bind()
+    folded, bm, sp = _slab_run(plan, x, slabs)
+    torch.cuda.synchronize()
+    res = {"bm": bm.cpu().numpy()[None], "spectra": sp.cpu().numpy()[None], "det": None}
+    tb = R.make_tables(op)
+    ref = R.rsft_run(x[0], op, tb)
+    px = float(np.mean(np.abs(x[0].astype(np.complex128)) ** 2))
+    from paper_1610_01050_b200 import rsft as B
+    for l, st in enumerate(ref.stages):
+        cb = R.compare_buckets(res["spectra"][0, l].reshape(b), st, px)
+        assert cb["ok"], (l, cb)
+        bits = B.bitmap_to_bool(res["bm"][0, l], plan.btot).reshape(b)
+        assert R.compare_bits(bits, st)["ok"], l
+    part = plan.finalize(folded[2:L - 1].contiguous(), loop_begin=2, loop_end=L - 1)
+    np.testing.assert_array_equal(part.cpu().numpy(), bm.cpu().numpy()[2:L - 1])
+
+
+def test_variant_b_c5_full_cube():
+    """c5 at full size: 4 slabs of 512 planes (the 4-rank variant-B split) + finalize vs the
+    unsharded rsft_execute: spectra within fp32 rounding, bits equal outside the 1e-3 band."""
+    import torch
+    wl = synth.C5
+    x = frames(wl, 1)
+    op = wl_params(wl)
+    plan = make_plan(op, max_batch=1).bind()
+    xt = torch.from_numpy(x).cuda()
+    sp_full = torch.empty((1, plan.loops, plan.btot), dtype=torch.complex64, device="cuda")
+    bm_full = plan.execute(xt, spectra=sp_full)
+    del xt
+    _, bm, sp = _slab_run(plan, x, [(0, 512), (512, 1024), (1024, 1536), (1536, 2048)])
+    torch.cuda.synchronize()
+    a, f = sp.cpu().numpy().astype(np.complex128), sp_full.cpu().numpy()[0].astype(np.complex128)
+    beta, gamma = plan.thresholds()
+    px = float(np.mean(np.abs(x[0].astype(np.complex128)) ** 2))
+    floor = np.sqrt(beta * px)[:, None]
+    assert np.max(np.abs(a - f) / np.maximum(np.abs(f), floor)) < 1e-4
+    from paper_1610_01050_b200 import rsft as B
+    for l in range(plan.loops):
+        b1 = B.bitmap_to_bool(bm.cpu().numpy()[l], plan.btot)
+        b2 = B.bitmap_to_bool(bm_full.cpu().numpy()[0, l], plan.btot)
+        band = np.abs(np.abs(f[l]) ** 2 - gamma[l]) <= 1e-3 * gamma[l]
+        assert np.all((b1 == b2) | band)

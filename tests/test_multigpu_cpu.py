@@ -82,3 +82,39 @@ def test_shard_ranges_partition():
         assert sl[0][0] == 0 and sl[-1][1] == 2048 and all(sl[i][1] == sl[i + 1][0] for i in range(world - 1))
     with pytest.raises(ValueError):
         shard.loop_range(0, 3, 16)
+
+
+def _worker_b(rank, world, port, ret):
+    """Variant B host logic: each rank's slab-masked frame -> oracle folded spectra (the fold
+    is linear in x, Eqs. z, l P:272-279) -> reduce-scatter over loops -> this rank's loop rows
+    equal the unsharded frame's."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, b, L = (32, 16, 64), (4, 4, 8), 4
+        p = R.Params(n=n, b=b, loops=L, p_fa=1e-3, seed=19, random_tau=True)
+        tb = R.make_tables(p)
+        wl = synth.Workload("mgb", n, b, L, 1e-3, 1.0, (3, 6), (5.0, 20.0), 1, data_seed=6)
+        x = synth.gen_frame(wl, 0)
+        d0b, d0e = shard.slab_range(rank, world, n[0], n[1] * n[2])
+        xs = np.zeros_like(x)
+        xs[d0b:d0e] = x[d0b:d0e]
+        part = torch.from_numpy(np.stack([R.first_stage(xs, p, tb, l).fhat.ravel() for l in range(L)]))
+        mine = shard.reduce_scatter_loops(part, world)
+        lb, le = shard.loop_range(rank, world, L)
+        full = np.stack([R.first_stage(x, p, tb, l).fhat.ravel() for l in range(lb, le)])
+        err = float(np.max(np.abs(mine.numpy() - full)) / np.max(np.abs(full)))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, err)
+        if rank == 0:
+            ret["err"] = max(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_slab_partials_reduce_scatter():
+    world = 2
+    with mp.Manager() as mgr:
+        ret = mgr.dict()
+        mp.spawn(_worker_b, args=(world, free_port(), ret), nprocs=world, join=True)
+        assert ret["err"] < 1e-12
