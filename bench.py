@@ -220,13 +220,10 @@ def main_gpu(a):
     def step(events=None):
         if events is not None:
             events[0].record(stream)
-        plan.execute(x, bitmaps=bm)
-        n = plan.last_launch_count()
+        plan.run(x, cap, bitmaps=bm, detect=det, idx=idx, count=cnt)
         if events is not None:
             events[1].record(stream)
-        plan.detect_compact(bm, cap, detect=det, idx=idx, count=cnt)
-        n += plan.last_launch_count()
-        return n
+        return plan.last_launch_count()
 
     for _ in range(a.warmup):
         step()
@@ -285,10 +282,12 @@ def main_gpu(a):
             dist.destroy_process_group()
         return 0
 
-    # roofline of the dominant kernel (fused fold + FFT + threshold, one launch per step)
+    # roofline: the fused kernel (fold + FFT + threshold + vote, one launch per step) with the
+    # offset scan and index writes that follow it, timed around rsft_run on the launching
+    # stream; algorithmic bytes = x read + bitmaps + detection bitmap + index list written
     peak, peak_src = load_peaks()
     k1_avg = statistics.mean(k1_ms)
-    algo_bytes = frames * (8 * plan.ntot + plan.loops * plan.bitmap_words * 4)
+    algo_bytes = frames * (8 * plan.ntot + plan.loops * plan.bitmap_words * 4 + plan.detect_words * 4) + 8 * detections
     achieved = algo_bytes / (k1_avg / 1000.0) / 1e9
     step_ms = elapsed_ms / a.steps
     value = world * frames / (step_ms / 1000.0)
@@ -308,7 +307,8 @@ def main_gpu(a):
                    "parallelism": f"frames sharded over {world} GPU(s), no data-path collective"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(wl.name),
-                     "kernel": "k_fused (fold+FFT+threshold)", "algorithmic_bytes_per_launch": algo_bytes,
+                     "kernel": "rsft_run: k_fused (fold+FFT+threshold+vote) + offset scan + index writes",
+                     "algorithmic_bytes_per_launch": algo_bytes,
                      "avg_launch_ms": k1_avg, "share_of_step": k1_avg / step_ms, "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": clocks,

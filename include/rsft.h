@@ -189,9 +189,17 @@ rsft_status rsft_detect_compact(rsft_plan_t plan, const uint32_t* d_bitmaps, int
                                 uint32_t* d_detect, int64_t* d_idx, int64_t capacity,
                                 int64_t* d_count, void* stream);
 
+/* Whole hot path on device buffers: rsft_execute (all loops) + rsft_detect_compact, with the
+ * same outputs (d_bitmaps [batch][L][bitmap_words], d_detect [batch][detect_words], sorted
+ * indices, *d_count).  In fused mode the second stage runs inside the fold kernel's
+ * per-frame epilogue (the frame's bitmaps stay on the SM).  Errors: as rsft_execute and
+ * rsft_detect_compact. */
+rsft_status rsft_run(rsft_plan_t plan, const void* d_x, int64_t batch, uint32_t* d_bitmaps, uint32_t* d_detect,
+                     int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);
+
 /* End-to-end convenience call on HOST buffers (blocking: synchronises `stream`):
- * copies h_x (complex64 [batch][N...], pinned recommended) into d_scratch, runs execute,
- * detect and compact, and copies the count and min(count, capacity) indices back.
+ * copies h_x (complex64 [batch][N...], pinned recommended) into d_scratch, runs rsft_run,
+ * and copies the count and min(count, capacity) indices back.
  * d_scratch: device buffer of >= rsft_host_scratch_bytes(plan, batch, capacity) bytes.
  * Returns the true count in *h_count.  Errors: as above. */
 size_t rsft_host_scratch_bytes(rsft_plan_t plan, int64_t batch, int64_t capacity);

@@ -13,6 +13,8 @@ rsft_status launch_partial(rsft_plan_s* p, const void* d_x, int64_t off, int64_t
                            cudaStream_t st);
 rsft_status launch_finalize(rsft_plan_s* p, const void* d_folded, int l0, int nl, uint32_t* bm, void* spectra,
                             cudaStream_t st);
+rsft_status launch_run(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det, int64_t* idx,
+                       int64_t capacity, int64_t* d_count, cudaStream_t st);
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st);
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
@@ -108,6 +110,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.xmask = p->ws.xmask_bytes ? reinterpret_cast<const uint32_t*>(base + p->ws.xmask_off) : nullptr;
   pd.region_state = reinterpret_cast<unsigned long long*>(base + p->ws.region_off);
   pd.region_capacity = p->ws.region_capacity;
+  pd.region_slots = p->ws.slots_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.slots_off) : nullptr;
   p->d_ws = d_ws;
   p->bound = true;
   return RSFT_OK;
@@ -180,6 +183,16 @@ rsft_status rsft_detect_compact(rsft_plan_t p, const uint32_t* d_bitmaps, int64_
                                reinterpret_cast<cudaStream_t>(stream));
 }
 
+rsft_status rsft_run(rsft_plan_t p, const void* d_x, int64_t batch, uint32_t* d_bitmaps, uint32_t* d_detect,
+                     int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream) {
+  if (!p || !d_x || !d_bitmaps || !d_detect || !d_count || (capacity > 0 && !d_idx) || capacity < 0) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
+  if (reinterpret_cast<uintptr_t>(d_x) & 15) return RSFT_E_ARG;
+  p->last_launches = 0;
+  return launch_run(p, d_x, batch, d_bitmaps, d_detect, d_idx, capacity, d_count, reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t rsft_host_scratch_bytes(rsft_plan_t p, int64_t batch, int64_t capacity) {
   if (!p || batch < 1) return 0;
   size_t x = align256((size_t)batch * p->ntot * 8);
@@ -207,9 +220,7 @@ rsft_status rsft_run_host(rsft_plan_t p, const void* h_x, int64_t batch, int64_t
   rsft_status s;
   int32_t launches = 0;
   if ((s = cuda_check(cudaMemcpyAsync(dx, h_x, (size_t)batch * p->ntot * 8, cudaMemcpyHostToDevice, st), "H2D x"))) return s;
-  if ((s = rsft_execute(p, dx, batch, 0, p->L, dbm, nullptr, stream))) return s;
-  launches += p->last_launches;
-  if ((s = rsft_detect_compact(p, dbm, batch, ddet, didx, capacity, dcount, stream))) return s;
+  if ((s = rsft_run(p, dx, batch, dbm, ddet, didx, capacity, dcount, stream))) return s;
   launches += p->last_launches;
   if ((s = cuda_check(cudaMemcpyAsync(h_count, dcount, 8, cudaMemcpyDeviceToHost, st), "D2H count"))) return s;
   if ((s = cuda_check(cudaStreamSynchronize(st), "sync"))) return s;

@@ -314,6 +314,281 @@ __device__ __forceinline__ void fold_group_prod(float2 (&acc)[LP][2], const floa
   }
 }
 
+constexpr int kStageIdx = 2048;          // indices staged per CTA for coalesced writes
+
+// Block-wide exclusive scan of one int per thread; returns the prefix, *total = sum.
+__device__ __forceinline__ int block_excl_scan(int c, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0, t = 0;
+  for (int i = 0; i < nw; ++i) {
+    if (i < warp) wbase += wsum[i];
+    t += wsum[i];
+  }
+  *total = t;
+  return wbase + incl - c;
+}
+
+// Vote one region whose bitmap slice bm [L][lw] is in shared memory (see k_vote): builds
+// E (shared, [L][B_rd][W] words), votes every item of the region, writes its detection words
+// (detect, if not null) and abar (counts, MODE 2, if not null).  Returns this thread's
+// detection popcount.  Contains __syncthreads: every thread of the CTA calls it.
+// LIST: items are assigned kListIpt-contiguous per thread, kept in registers, and the
+// region's detections are also written as ascending region-local location indices to
+// slot[0 .. min(total, cap)) (the return value is then the region total, on every thread).
+constexpr int kListIpt = 4;              // items per thread in LIST mode (<= 32 words)
+
+template <int CW, int MODE, bool LIST = false>
+__device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32_t* E, const int* sig_rd,
+                           const uint32_t* Xs, const uint32_t* NT, const int* kpre_s, int64_t frame, int64_t i0,
+                           int64_t d0b, int64_t d0e, uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
+                           int* wsum = nullptr, uint32_t* __restrict__ slot = nullptr) {
+  const int D = pd.D, L = pd.L, wpl = pd.wpl;
+  const int ld = D - 1;
+  const int nld = pd.n[ld], lga_ld = pd.lga[ld];
+  const int W = nld >> 5;
+  const int lgW = __ffs(W) - 1;
+  const int brd = D >= 2 ? pd.b[D - 2] : 1;
+  const int blast = pd.blast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int rowbits = brd * blast;
+  const int nrd = D >= 2 ? pd.n[D - 2] : 1;
+  const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
+  const int chunks = W / CW;
+  const int lg_chunks = __ffs(chunks) - 1;
+  const int mu = pd.mu;
+  const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
+  const int64_t slab_words = slab_locs >> 5;
+  constexpr bool COUNT = true;
+  int cnt = 0;
+  (void)wpl;
+    // E[l][krd][w] (all loops at once).  With nibble tables NT[l][g][n][w] = OR of the X masks
+    // of the set bits of n in bucket group g (4 buckets), one entry costs B_last/4 lookups.
+    if (pd.xmask) {
+      const int lg_rw = (brd > 1 ? __ffs(brd) - 1 : 0) + lgW;
+      for (int j = tid; j < L * brd * W; j += blockDim.x) {
+        const int l = j >> lg_rw, rem = j & ((1 << lg_rw) - 1);
+        const int krd = rem >> lgW, w = rem & (W - 1);
+        int base = 0;
+        if (D == 3) base = lw < wpl ? (kpre_s[l] * rowbits) & 31 : kpre_s[l] * rowbits;
+        const uint32_t* b = bm + (size_t)l * lw;
+        const int f0 = base + krd * blast;
+        uint32_t e = 0;
+        if (NT) {
+          const uint32_t* T = NT + (size_t)l * (blast >> 2) * 16 * W + w;
+          if (blast <= 32) {
+            uint32_t pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
+            for (int g = 0; g < (blast >> 2); ++g, pat >>= 4) e |= T[((g << 4) + (pat & 15)) * W];
+          } else {
+            uint32_t lo = b[f0 >> 5], hi = b[(f0 >> 5) + 1];
+#pragma unroll
+            for (int g = 0; g < 8; ++g, lo >>= 4) e |= T[((g << 4) + (lo & 15)) * W];
+#pragma unroll
+            for (int g = 8; g < 16; ++g, hi >>= 4) e |= T[((g << 4) + (hi & 15)) * W];
+          }
+        } else {
+          const uint32_t* X = Xs + (size_t)l * blast * W;
+          if (blast <= 32) {
+            uint32_t pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
+            while (pat) {
+              const int k = __ffs(pat) - 1;
+              pat &= pat - 1;
+              e |= X[k * W + w];
+            }
+          } else {                                   // blast == 64: two aligned words
+            uint32_t lo = b[f0 >> 5], hi = b[(f0 >> 5) + 1];
+            while (lo) { const int k = __ffs(lo) - 1; lo &= lo - 1; e |= X[k * W + w]; }
+            while (hi) { const int k = __ffs(hi) + 31; hi &= hi - 1; e |= X[k * W + w]; }
+          }
+        }
+        E[j] = e;
+      }
+    } else {                                         // ballots: warp per (l, w)
+      for (int it = warp; it < L * W; it += nwarps) {
+        const int l = it / W, w = it - l * W;
+        const LoopDev& lp = pd.loops[l];
+        int base = 0;
+        if (D == 3) {
+          const int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
+          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
+        }
+        const int ilast = (w << 5) + lane;
+        const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
+        const uint32_t* b = bm + (size_t)l * lw;
+        for (int krd = 0; krd < brd; ++krd) {
+          const int flat = base + krd * blast + klast;
+          const uint32_t word = __ballot_sync(0xffffffffu, (b[flat >> 5] >> (flat & 31)) & 1u);
+          if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+        }
+      }
+    }
+    __syncthreads();
+    int64_t rbeg, rend, out_base;
+    if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * W; }
+    else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
+    else { rbeg = 0; rend = 1; out_base = 0; }
+    const int64_t nitems = (rend - rbeg) * chunks;
+
+    // one item = CW consecutive detection words of one row
+    auto vote_item = [&](int64_t it, uint32_t (&acc)[CW]) {
+      const int64_t ri = it >> lg_chunks;
+      const int w0 = (int)(it - ri * chunks) * CW;
+      const int64_t row = rbeg + ri;
+      uint32_t pl[CW][6];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        acc[c] = MODE == 0 ? 0xffffffffu : 0u;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
+      }
+      for (int l = 0; l < L; ++l) {
+        // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
+        const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
+        const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
+        uint32_t m[CW];
+        if (CW % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < CW; q += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(e + q);
+            m[q] = v.x; m[(q + 1) % CW] = v.y; m[(q + 2) % CW] = v.z; m[(q + 3) % CW] = v.w;
+          }
+        } else if (CW == 2) {
+          const uint2 v = *reinterpret_cast<const uint2*>(e);
+          m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
+        } else {
+          m[0] = e[0];
+        }
+        uint32_t any = 0;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          if (MODE == 0) { acc[c] &= m[c]; any |= acc[c]; }
+          else if (MODE == 1) acc[c] |= m[c];
+          else {
+            uint32_t carry = m[c];
+#pragma unroll
+            for (int b = 0; b < 6; ++b) {
+              const uint32_t t = pl[c][b] & carry;
+              pl[c][b] ^= carry;
+              carry = t;
+            }
+          }
+        }
+        if (MODE == 0 && any == 0) break;              // unanimity already impossible
+      }
+      if (MODE == 2) {                                 // bit-sliced compare: count >= mu
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+          for (int b = 5; b >= 0; --b) {
+            if ((mu >> b) & 1) eq &= pl[c][b];
+            else { gt |= eq & pl[c][b]; eq &= ~pl[c][b]; }
+          }
+          acc[c] = gt | eq;
+        }
+      }
+      const int64_t widx = out_base + ri * W + w0;
+      if (detect) {
+        uint32_t* dst = detect + frame * slab_words + widx;
+        if (CW % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < CW; q += 4)
+            *reinterpret_cast<uint4*>(dst + q) = make_uint4(acc[q], acc[(q + 1) % CW], acc[(q + 2) % CW], acc[(q + 3) % CW]);
+        } else if (CW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(acc[0], acc[CW > 1 ? 1 : 0]);
+        else dst[0] = acc[0];
+      }
+      if (MODE == 2 && counts) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          uint8_t* cdst = counts + frame * slab_locs + (widx + c) * 32;
+          for (int j = 0; j < 32; ++j) {
+            int v = 0;
+#pragma unroll
+            for (int b = 0; b < 6; ++b) v |= ((pl[c][b] >> j) & 1u) << b;
+            cdst[j] = (uint8_t)v;
+          }
+        }
+      }
+    };
+
+    if (LIST) {
+      // items it = tid + k * blockDim (coalesced detection-word stores); word order is
+      // k-major, so the position of item (k, tid) is sum_{k' < k} T_k' + prefix_k(tid)
+      uint32_t words[kListIpt][CW];
+      int ck[kListIpt];
+#pragma unroll
+      for (int k = 0; k < kListIpt; ++k) {
+        const int64_t it = tid + (int64_t)k * blockDim.x;
+        ck[k] = 0;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) words[k][c] = 0u;
+        if (it < nitems) {
+          vote_item(it, words[k]);
+#pragma unroll
+          for (int c = 0; c < CW; ++c) ck[k] += __popc(words[k][c]);
+        }
+      }
+      int incl[kListIpt];
+#pragma unroll
+      for (int k = 0; k < kListIpt; ++k) {
+        incl[k] = ck[k];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl[k], off);
+          if (lane >= off) incl[k] += v;
+        }
+        if (lane == 31) wsum[k * nwarps + warp] = incl[k];
+      }
+      __syncthreads();
+      int pos[kListIpt], total = 0;
+#pragma unroll
+      for (int k = 0; k < kListIpt; ++k) {
+        int before = 0, tk = 0;
+        for (int w2 = 0; w2 < nwarps; ++w2) {
+          const int v = wsum[k * nwarps + w2];
+          if (w2 < warp) before += v;
+          tk += v;
+        }
+        pos[k] = total + before + incl[k] - ck[k];
+        total += tk;
+      }
+      if (total <= kListCap) {
+#pragma unroll
+        for (int k = 0; k < kListIpt; ++k) {
+          const int64_t it = tid + (int64_t)k * blockDim.x;
+          int q = pos[k];
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            uint32_t v = words[k][c];
+            while (v) {
+              const int bit = __ffs(v) - 1;
+              v &= v - 1;
+              slot[q++] = (uint32_t)((it * CW + c) * 32 + bit);
+            }
+          }
+        }
+      }
+      __syncthreads();                             // wsum reused by the next region
+      return total;
+    }
+    for (int64_t it = tid; it < nitems; it += blockDim.x) {
+      uint32_t acc[CW];
+      vote_item(it, acc);
+      if (COUNT) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+      }
+    }
+  return cnt;
+}
+
 // ------------------------------------------------------------------------------------
 // Fused mode: persistent CTAs, one frame at a time per CTA.  D in {1, 2}, N_last >= 64.
 // Warp task = (outer residue class kappa, segment group g); unit = (task, 64-column
@@ -899,28 +1174,6 @@ __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bo
   }
 }
 
-constexpr int kStageIdx = 2048;          // indices staged per CTA for coalesced writes
-
-// Block-wide exclusive scan of one int per thread; returns the prefix, *total = sum.
-__device__ __forceinline__ int block_excl_scan(int c, int* wsum, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int incl = c;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    int v = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += v;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  int wbase = 0, t = 0;
-  for (int i = 0; i < nw; ++i) {
-    if (i < warp) wbase += wsum[i];
-    t += wsum[i];
-  }
-  *total = t;
-  return wbase + incl - c;
-}
-
 // ------------------------------------------------------------------------------------
 // K3 vote (persistent).  Reverse mapping + accumulation + second stage (Alg. 1 l.11-14,
 // P:226-229; Def. 4; Eq. a_i), evaluated through identity I1 (Props. 3-4,
@@ -935,18 +1188,15 @@ __device__ __forceinline__ int block_excl_scan(int c, int* wsum, int* total) {
 // count (rcount[region]) for the offset scan of rsft_detect_compact.
 // smem: bm [L][lw] | E [L][B_rd][W] | sig_rd [32] | X [L][B_last][W]
 // ------------------------------------------------------------------------------------
-template <int CW, int MODE, bool COUNT>
+template <int CW, int MODE, bool COUNT, bool LIST>
 __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
                                                    int64_t d0b, int64_t d0e, int lw, int64_t np, int64_t nregions,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
                                                    unsigned long long* __restrict__ rcount) {
   extern __shared__ __align__(16) uint32_t vsm[];
-  __shared__ int wsum[kThreads / 32];
+  __shared__ int wsum[kListIpt * kThreads / 32];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
-  const int ld = D - 1;
-  const int nld = pd.n[ld], lga_ld = pd.lga[ld];
-  const int W = nld >> 5;                            // words per row of locations
-  const int lgW = __ffs(W) - 1;
+  const int W = pd.n[D - 1] >> 5;                    // words per row of locations
   const int brd = D >= 2 ? pd.b[D - 2] : 1;
   const int blast = pd.blast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -954,13 +1204,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
   uint32_t* E = bm + (((size_t)L * lw + 3) & ~size_t(3));   // 16-B aligned for uint4 loads
   int* sig_rd = reinterpret_cast<int*>(E + (((size_t)L * brd * W + 3) & ~size_t(3)));
   uint32_t* Xs = reinterpret_cast<uint32_t*>(sig_rd + kMaxLoops);
+  const size_t xw = pd.xmask ? (size_t)L * blast * W : 0;
+  uint32_t* NT = (pd.xmask && blast >= 4 && 16 * xw <= kMaxNibbleBytes) ? Xs + ((xw + 3) & ~size_t(3)) : nullptr;
+  __shared__ int kpre_s[kMaxLoops];
   const int rowbits = brd * blast;                   // bits of one k_pre slab
-  const int nrd = D >= 2 ? pd.n[D - 2] : 1;
-  const int lga_rd = D >= 2 ? pd.lga[D - 2] : 0;
-  const int chunks = W / CW;
-  const int mu = pd.mu;
-  const int64_t slab_locs = (d0e - d0b) * (pd.ntot / pd.n[0]);
-  const int64_t slab_words = slab_locs >> 5;
 
   for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
   if (pd.xmask) {                                    // plan-constant: once per CTA
@@ -972,10 +1219,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
       for (int i = tid; i < nx; i += blockDim.x) Xs[i] = __ldg(pd.xmask + i);
   }
 
+  if (NT) {                                          // nibble tables from the X masks (once)
+    __syncthreads();
+    const int ng = blast >> 2;
+    for (int i = tid; i < L * ng * 16 * W; i += blockDim.x) {
+      const int w = i % W, n = (i / W) & 15, g = (i / (W * 16)) % ng, l = i / (W * 16 * ng);
+      uint32_t e = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((n >> q) & 1) e |= Xs[((size_t)l * blast + 4 * g + q) * W + w];
+      NT[i] = e;
+    }
+  }
+
   for (int64_t region = blockIdx.x; region < nregions; region += gridDim.x) {
     __syncthreads();                                 // previous region's E / bm readers done
     const int64_t frame = region / np, prefix = region - frame * np;
     const int64_t i0 = d0b + prefix;
+    if (D == 3)
+      for (int l = tid; l < L; l += blockDim.x)
+        kpre_s[l] = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
 
     // this region's slice of every loop's first-stage bitmap
     const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
@@ -989,145 +1252,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
       bm[i] = __ldg(src + (size_t)l * wpl + start + w);
     }
     __syncthreads();
-    // E[l][krd][w] (all loops at once)
-    if (pd.xmask) {
-      for (int j = tid; j < L * brd * W; j += blockDim.x) {
-        const int l = j / (brd * W), rem = j - l * (brd * W);
-        const int krd = rem >> lgW, w = rem & (W - 1);
-        int base = 0;
-        if (D == 3) {
-          const int kpre = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
-        }
-        const uint32_t* b = bm + (size_t)l * lw;
-        const uint32_t* X = Xs + (size_t)l * blast * W;
-        const int f0 = base + krd * blast;
-        uint32_t e = 0;
-        if (blast <= 32) {
-          uint32_t pat = (b[f0 >> 5] >> (f0 & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
-          while (pat) {
-            const int k = __ffs(pat) - 1;
-            pat &= pat - 1;
-            e |= X[k * W + w];
-          }
-        } else {                                     // blast == 64: two aligned words
-          uint32_t lo = b[f0 >> 5], hi = b[(f0 >> 5) + 1];
-          while (lo) { const int k = __ffs(lo) - 1; lo &= lo - 1; e |= X[k * W + w]; }
-          while (hi) { const int k = __ffs(hi) + 31; hi &= hi - 1; e |= X[k * W + w]; }
-        }
-        E[j] = e;
-      }
-    } else {                                         // ballots: warp per (l, w)
-      for (int it = warp; it < L * W; it += nwarps) {
-        const int l = it / W, w = it - l * W;
-        const LoopDev& lp = pd.loops[l];
-        int base = 0;
-        if (D == 3) {
-          const int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
-        }
-        const int ilast = (w << 5) + lane;
-        const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
-        const uint32_t* b = bm + (size_t)l * lw;
-        for (int krd = 0; krd < brd; ++krd) {
-          const int flat = base + krd * blast + klast;
-          const uint32_t word = __ballot_sync(0xffffffffu, (b[flat >> 5] >> (flat & 31)) & 1u);
-          if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
-        }
-      }
+    if (LIST) {                                      // region-local index list + count
+      const int t = vote_region<CW, MODE, true>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, frame, i0, d0b, d0e, detect,
+                                                counts, wsum, pd.region_slots + (size_t)region * kListCap);
+      if (tid == 0) rcount[region] = (unsigned long long)t;
+      continue;
     }
-    __syncthreads();
-    int64_t rbeg, rend, out_base;
-    if (D == 3) { rbeg = 0; rend = pd.n[1]; out_base = (i0 - d0b) * pd.n[1] * W; }
-    else if (D == 2) { rbeg = d0b; rend = d0e; out_base = 0; }
-    else { rbeg = 0; rend = 1; out_base = 0; }
-    const int64_t nitems = (rend - rbeg) * chunks;
-
-    // one item = CW consecutive detection words of one row
-    auto vote_item = [&](int64_t it, uint32_t (&acc)[CW]) {
-      const int64_t ri = it / chunks;
-      const int w0 = (int)(it - ri * chunks) * CW;
-      const int64_t row = rbeg + ri;
-      uint32_t pl[CW][6];
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        acc[c] = MODE == 0 ? 0xffffffffu : 0u;
-#pragma unroll
-        for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
-      }
-      for (int l = 0; l < L; ++l) {
-        // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
-        const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
-        const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
-        uint32_t m[CW];
-        if (CW == 4) {
-          const uint4 v = *reinterpret_cast<const uint4*>(e);
-          m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y; m[CW > 2 ? 2 : 0] = v.z; m[CW > 3 ? 3 : 0] = v.w;
-        } else if (CW == 2) {
-          const uint2 v = *reinterpret_cast<const uint2*>(e);
-          m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
-        } else {
-          m[0] = e[0];
-        }
-        uint32_t any = 0;
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          if (MODE == 0) { acc[c] &= m[c]; any |= acc[c]; }
-          else if (MODE == 1) acc[c] |= m[c];
-          else {
-            uint32_t carry = m[c];
-#pragma unroll
-            for (int b = 0; b < 6; ++b) {
-              const uint32_t t = pl[c][b] & carry;
-              pl[c][b] ^= carry;
-              carry = t;
-            }
-          }
-        }
-        if (MODE == 0 && any == 0) break;              // unanimity already impossible
-      }
-      if (MODE == 2) {                                 // bit-sliced compare: count >= mu
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          uint32_t gt = 0u, eq = 0xffffffffu;
-#pragma unroll
-          for (int b = 5; b >= 0; --b) {
-            if ((mu >> b) & 1) eq &= pl[c][b];
-            else { gt |= eq & pl[c][b]; eq &= ~pl[c][b]; }
-          }
-          acc[c] = gt | eq;
-        }
-      }
-      const int64_t widx = out_base + ri * W + w0;
-      if (detect) {
-        uint32_t* dst = detect + frame * slab_words + widx;
-        if (CW == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(acc[0], acc[CW > 1 ? 1 : 0], acc[CW > 2 ? 2 : 0], acc[CW > 3 ? 3 : 0]);
-        else if (CW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(acc[0], acc[CW > 1 ? 1 : 0]);
-        else dst[0] = acc[0];
-      }
-      if (MODE == 2 && counts) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-          uint8_t* cdst = counts + frame * slab_locs + (widx + c) * 32;
-          for (int j = 0; j < 32; ++j) {
-            int v = 0;
-#pragma unroll
-            for (int b = 0; b < 6; ++b) v |= ((pl[c][b] >> j) & 1u) << b;
-            cdst[j] = (uint8_t)v;
-          }
-        }
-      }
-    };
-
-    int cnt = 0;
-    for (int64_t it = tid; it < nitems; it += blockDim.x) {
-      uint32_t acc[CW];
-      vote_item(it, acc);
-      if (COUNT) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
-      }
-    }
+    int cnt = vote_region<CW, MODE>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, frame, i0, d0b, d0e, detect, counts);
     if (COUNT) {                                     // this region's detection count
 #pragma unroll
       for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
@@ -1165,77 +1296,64 @@ __global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __rest
   for (int64_t i = b; i < e; ++i) { long long v = (long long)counts[i]; counts[i] = (unsigned long long)run; run += v; }
 }
 
-// One CTA per region: load up to 8 tiles of 4 words per thread at once (all loads in
-// flight), scan in (tile, thread) order = word order with one barrier, write ascending
-// indices at the region's offset (staged in smem for coalesced stores).
-constexpr int kWT = 8;                     // tiles per pass
+// One CTA per region: each thread owns 32 consecutive detection words of a pass of
+// 32 x blockDim words (8 x 16-B loads in flight), one block scan of the per-thread counts
+// gives every thread its output position in word order; ascending indices are staged in
+// shared memory and written at the region's offset (coalesced).
+constexpr int kRwWords = 32;               // words per thread per pass
 
 __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __restrict__ det, int64_t rwords,
                                                            const unsigned long long* __restrict__ offsets,
+                                                           const long long* __restrict__ d_count, int64_t nregions,
+                                                           const uint32_t* __restrict__ slots,
                                                            long long* __restrict__ idx, int64_t capacity) {
-  __shared__ int wsk[kWT * 32];
+  __shared__ int wsum[kThreads / 32];
   __shared__ long long s_idx[kStageIdx];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x;
   const int64_t r = blockIdx.x;
   const uint32_t* src = det + r * rwords;
   long long run = (long long)offsets[r];
+  if (slots) {                                       // the vote left a region-local index list
+    const long long n = (r + 1 < nregions ? (long long)offsets[r + 1] : *d_count) - run;
+    if (n <= kListCap) {
+      const uint32_t* sl = slots + (size_t)r * kListCap;
+      const long long g0 = r * rwords * 32;
+      for (long long i = tid; i < n; i += blockDim.x)
+        if (run + i < capacity) idx[run + i] = g0 + (long long)sl[i];
+      return;
+    }
+  }
   const bool vec = (rwords & 3) == 0;
-  const int64_t tile = 4 * (int64_t)blockDim.x;
-  for (int64_t p0 = 0; p0 < rwords; p0 += kWT * tile) {
-    uint32_t w[kWT][4];
+  const int64_t pass = (int64_t)kRwWords * blockDim.x;
+  for (int64_t p0 = 0; p0 < rwords; p0 += pass) {
+    const int64_t w0 = p0 + (int64_t)tid * kRwWords;
+    uint32_t w[kRwWords];
 #pragma unroll
-    for (int k = 0; k < kWT; ++k) {
-      const int64_t w0 = p0 + k * tile + 4 * (int64_t)tid;
-      if (vec && w0 + 3 < rwords) {
-        uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + w0));
-        w[k][0] = v.x; w[k][1] = v.y; w[k][2] = v.z; w[k][3] = v.w;
+    for (int q = 0; q < kRwWords; q += 4) {
+      if (vec && w0 + q + 3 < rwords) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + w0 + q));
+        w[q] = v.x; w[q + 1] = v.y; w[q + 2] = v.z; w[q + 3] = v.w;
       } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) w[k][c] = w0 + c < rwords ? src[w0 + c] : 0u;
+        for (int c = 0; c < 4; ++c) w[q + c] = w0 + q + c < rwords ? src[w0 + q + c] : 0u;
       }
     }
-    int cnt[kWT], incl[kWT];
+    int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < kWT; ++k) {
-      cnt[k] = __popc(w[k][0]) + __popc(w[k][1]) + __popc(w[k][2]) + __popc(w[k][3]);
-      incl[k] = cnt[k];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl[k], off);
-        if (lane >= off) incl[k] += v;
-      }
-      if (lane == 31) wsk[k * 32 + warp] = incl[k];
-    }
-    __syncthreads();
-    int total = 0;
-    int off_k[kWT];
-#pragma unroll
-    for (int k = 0; k < kWT; ++k) {
-      int before = 0, rt = 0;
-      for (int w2 = 0; w2 < nw; ++w2) {
-        const int v = wsk[k * 32 + w2];
-        if (w2 < warp) before += v;
-        rt += v;
-      }
-      off_k[k] = total + before + incl[k] - cnt[k];
-      total += rt;
-    }
+    for (int q = 0; q < kRwWords; ++q) cnt += __popc(w[q]);
+    int total;
+    int lp = block_excl_scan(cnt, wsum, &total);
     const bool staged = total <= kStageIdx;
 #pragma unroll
-    for (int k = 0; k < kWT; ++k) {
-      const int64_t w0 = p0 + k * tile + 4 * (int64_t)tid;
-      int lp = off_k[k];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v = w[k][c];
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          const long long g = (r * rwords + w0 + c) * 32 + bit;
-          if (staged) s_idx[lp] = g;
-          else if (run + lp < capacity) idx[run + lp] = g;
-          ++lp;
-        }
+    for (int q = 0; q < kRwWords; ++q) {
+      uint32_t v = w[q];
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1;
+        const long long g = (r * rwords + w0 + q) * 32 + bit;
+        if (staged) s_idx[lp] = g;
+        else if (run + lp < capacity) idx[run + lp] = g;
+        ++lp;
       }
     }
     __syncthreads();
@@ -1568,16 +1686,17 @@ static size_t vote_smem(const rsft_plan_s* p, int* lw_out) {
   const int lw = (D == 3 && rowbits % 32 == 0) ? (int)(rowbits / 32) : (int)wpl;
   *lw_out = lw;
   const size_t xw = p->dev.xmask ? (size_t)p->L * p->b[D - 1] * W : 0;
+  const size_t nt = (p->dev.xmask && p->b[D - 1] >= 4 && 16 * xw <= kMaxNibbleBytes) ? 4 * xw : 0;   // nibble tables
   return (((size_t)p->L * lw + 3) & ~size_t(3)) * 4 + (((size_t)p->L * brd * W + 3) & ~size_t(3)) * 4 +
-         kMaxLoops * 4 + ((xw + 3) & ~size_t(3)) * 4;
+         kMaxLoops * 4 + ((xw + 3) & ~size_t(3)) * 4 + nt * 4;
 }
 
-template <int CW, int MODE, bool COUNT>
+template <int CW, int MODE, bool COUNT, bool LIST>
 static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                                  uint32_t* det, uint8_t* counts, cudaStream_t st) {
   int lw = 0;
   const size_t smem = vote_smem(p, &lw);
-  auto kern = k_vote<CW, MODE, COUNT>;
+  auto kern = k_vote<CW, MODE, COUNT, LIST>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   const int64_t np = vote_regions_per_frame(p, d0b, d0e);
@@ -1595,13 +1714,14 @@ static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   return check(cudaGetLastError(), "k_vote launch");
 }
 
-template <bool COUNT>
+template <bool COUNT, bool LIST>
 static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                                     uint32_t* det, uint8_t* counts, cudaStream_t st) {
   const int64_t W = p->n[p->D - 1] / 32;
   const int mode = (!counts && p->mu == p->L) ? 0 : (!counts && p->mu == 1) ? 1 : 2;
 #define RSFT_VOTE_CASE(CWV, MV) \
-  if (W % CWV == 0 && mode == MV) return launch_vote_t<CWV, MV, COUNT>(p, bm, batch, d0b, d0e, det, counts, st);
+  if (W % CWV == 0 && mode == MV) return launch_vote_t<CWV, MV, COUNT, LIST>(p, bm, batch, d0b, d0e, det, counts, st);
+  RSFT_VOTE_CASE(8, 0) RSFT_VOTE_CASE(8, 1)
   RSFT_VOTE_CASE(4, 0) RSFT_VOTE_CASE(4, 1) RSFT_VOTE_CASE(4, 2)
   RSFT_VOTE_CASE(2, 0) RSFT_VOTE_CASE(2, 1) RSFT_VOTE_CASE(2, 2)
   RSFT_VOTE_CASE(1, 0) RSFT_VOTE_CASE(1, 1) RSFT_VOTE_CASE(1, 2)
@@ -1611,23 +1731,44 @@ static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t 
 
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st) {
-  return launch_vote_mode<false>(p, bm, batch, d0b, d0e, det, counts, st);
+  return launch_vote_mode<false, false>(p, bm, batch, d0b, d0e, det, counts, st);
 }
 
 // vote (+ per-region counts) -> offset scan -> per-region sorted index writes
 rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                   int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st) {
   const int64_t n0 = p->n[0];
-  rsft_status s = launch_vote_mode<true>(p, bm, batch, 0, n0, det, nullptr, st);
+  // region-local index lists when a region's items fit the registers (LIST): the writer then
+  // copies the lists instead of re-reading the detection bitmap
+  const int D = p->D;
+  const int64_t W = p->n[D - 1] / 32;
+  const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
+  const int64_t cw = (W % 8 == 0 && mode != 2) ? 8 : W % 4 == 0 ? 4 : W % 2 == 0 ? 2 : 1;
+  const int64_t rows = D == 3 ? p->n[1] : D == 2 ? n0 : 1;
+  const bool list = p->dev.region_slots && rows * (W / cw) <= (int64_t)kListIpt * kThreads;
+  rsft_status s = list ? launch_vote_mode<true, true>(p, bm, batch, 0, n0, det, nullptr, st)
+                       : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);
   if (s) return s;
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
   k_region_scan<<<1, 1024, 0, st>>>(p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count));
   k_region_write<<<(unsigned)nregions, kThreads, 0, st>>>(det, rwords, p->dev.region_state,
+                                                          reinterpret_cast<long long*>(d_count), nregions,
+                                                          list ? p->dev.region_slots : nullptr,
                                                           reinterpret_cast<long long*>(idx), capacity);
   p->last_launches += 2;
   return check(cudaGetLastError(), "region scan/write launch");
+}
+
+// Whole pipeline on one batch: execute (all loops) + detect_compact.  (Running the vote in
+// the fold kernel's per-frame epilogue was measured slower at c4: the CTA's TMA stream
+// stalls while it votes.)
+rsft_status launch_run(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det, int64_t* idx,
+                       int64_t capacity, int64_t* d_count, cudaStream_t st) {
+  rsft_status s = launch_execute(p, d_x, batch, 0, p->L, bm, nullptr, st);
+  if (s) return s;
+  return launch_detect_compact(p, bm, batch, det, idx, capacity, d_count, st);
 }
 
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,

@@ -198,6 +198,9 @@ void layout_workspace(rsft_plan_s* p) {
   w.xmask_off = off; off = align256(off + w.xmask_bytes);
   w.region_capacity = p->P.max_batch * (p->D == 3 ? p->n[0] : 1) + 2;
   w.region_off = off; off = align256(off + 8 * (size_t)w.region_capacity);
+  w.slots_off = off;                               // vote index lists (kListCap per region)
+  w.slots_bytes = (size_t)w.region_capacity * kListCap * 4;
+  off = align256(off + w.slots_bytes);
   w.total = off;
 }
 

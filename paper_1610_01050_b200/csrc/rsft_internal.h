@@ -46,6 +46,7 @@ constexpr int kUSplit = RSFT_SPLIT_U;             // ... U-slot (U x 512 B) TMA 
 constexpr int kThreadsSplit = RSFT_SPLIT_THREADS; // threads per CTA ...
 constexpr int kCtasSplit = RSFT_SPLIT_CTAS;       // ... and CTAs per SM the kernel is built for
 constexpr int kSplitUnitsPerWarp = 4;
+constexpr int kListCap = 2048;                   // vote: region-local index slots per region
 constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in smem up to this size             // chunking target: >= this many units per warp
 
 #ifdef __CUDACC__
@@ -109,14 +110,16 @@ struct PlanDev {
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
   const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
-  unsigned long long* region_state; // fused vote+compaction look-back state (+ ticket)
+  unsigned long long* region_state; // per-region detection counts -> offsets (rsft_detect_compact)
   int64_t region_capacity;
+  uint32_t* region_slots;          // per-region local index lists [region_capacity][kListCap] (or null)
 };
 
 constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
+constexpr size_t kMaxNibbleBytes = 64 * 1024;  // vote nibble tables (4x the masks) kept in smem
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, total;
+  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, total;
   int64_t region_capacity;
   int64_t chunk_capacity;
 };

@@ -72,6 +72,8 @@ def lib():
         "rsft_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
         "rsft_detect_compact": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
                                           c_void_p]),
+        "rsft_run": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                               c_void_p]),
         "rsft_host_scratch_bytes": (c_size_t, [c_void_p, c_int64, c_int64]),
         "rsft_run_host": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, P(c_int64), c_void_p,
                                     c_size_t, c_void_p]),
@@ -91,7 +93,7 @@ EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsf
             "rsft_get_schedule", "rsft_get_thresholds", "rsft_get_window", "rsft_get_info",
             "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_bucketize_partial", "rsft_finalize",
             "rsft_detect", "rsft_compact",
-            "rsft_detect_compact",
+            "rsft_detect_compact", "rsft_run",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
             "rsft_last_error"]
 
@@ -300,6 +302,26 @@ class Plan:
                                          c_void_p(idx.data_ptr()), capacity, c_void_p(count.data_ptr()),
                                          _stream_handle(stream)))
         return detect, idx, count
+
+    def run(self, x, capacity, bitmaps=None, detect=None, idx=None, count=None, stream=None):
+        """Whole hot path (execute all loops + detect + compact): (bitmaps, detect, idx, count)."""
+        import torch
+        self._need_bind()
+        batch = x.shape[0]
+        assert x.dtype == torch.complex64 and x.is_cuda and x.is_contiguous()
+        assert tuple(x.shape[1:]) == self.n
+        if bitmaps is None:
+            bitmaps = self.new_bitmaps(batch)
+        if detect is None:
+            detect = torch.empty((batch, self.detect_words), dtype=torch.int32, device=self.device)
+        if idx is None:
+            idx = torch.empty(max(capacity, 1), dtype=torch.int64, device=self.device)
+        if count is None:
+            count = torch.empty(1, dtype=torch.int64, device=self.device)
+        _check(lib().rsft_run(self._h, c_void_p(x.data_ptr()), batch, c_void_p(bitmaps.data_ptr()),
+                              c_void_p(detect.data_ptr()), c_void_p(idx.data_ptr()), capacity,
+                              c_void_p(count.data_ptr()), _stream_handle(stream)))
+        return bitmaps, detect, idx, count
 
     def host_scratch_bytes(self, batch, capacity):
         return lib().rsft_host_scratch_bytes(self._h, batch, capacity)

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+TAG=${1:-fused}
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
+$CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 -o gpurun_out/prof_${TAG} -f $CMD > gpurun_out/${TAG}_ncu.log 2>&1
+echo done

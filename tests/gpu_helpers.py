@@ -28,12 +28,16 @@ def gpu_run(plan, x_np, spectra=True, counts=True, capacity=None):
     det_fast = plan.detect(bm)              # no counts: AND (mu = L) / OR (mu = 1) fast paths
     cap = capacity if capacity is not None else batch * plan.ntot
     idx, cnt = plan.compact(det, cap)
-    det_f, idx_f, cnt_f = plan.detect_compact(bm, cap)      # fused vote + compaction
+    det_f, idx_f, cnt_f = plan.detect_compact(bm, cap)      # vote + compaction in one call
+    bm_r, det_r, idx_r, cnt_r = plan.run(x, cap)             # whole path (fused vote in fused mode)
     torch.cuda.synchronize()
     count = int(cnt.item())
-    assert int(cnt_f.item()) == count
+    assert int(cnt_f.item()) == count and int(cnt_r.item()) == count
     np.testing.assert_array_equal(det_f.cpu().numpy(), det.cpu().numpy())
+    np.testing.assert_array_equal(det_r.cpu().numpy(), det.cpu().numpy())
+    np.testing.assert_array_equal(bm_r.cpu().numpy(), bm.cpu().numpy())
     np.testing.assert_array_equal(idx_f.cpu().numpy()[:min(count, cap)], idx.cpu().numpy()[:min(count, cap)])
+    np.testing.assert_array_equal(idx_r.cpu().numpy()[:min(count, cap)], idx.cpu().numpy()[:min(count, cap)])
     return {
         "bm": bm.cpu().numpy(),
         "spectra": sp.cpu().numpy() if sp is not None else None,
