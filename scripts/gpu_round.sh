@@ -1,5 +1,6 @@
 #!/bin/bash
-# Full GPU session: smoke, full parity, bench (+e2e, cpu baseline), launch list, ncu capture.
+# Full GPU session: smoke, full parity, bench (+e2e, cpu baseline), c5 benches, reference arm,
+# launch lists (c4, c5), ncu --set full of the dominant kernels (k_fused at c4, k_split_fold at c5).
 set -u
 mkdir -p gpurun_out
 OUT=gpurun_out
@@ -8,13 +9,16 @@ python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "
 python -m pytest tests -q -m gpu --timeout 1500 > $OUT/parity_full.log 2>&1; echo "pytest rc=$?" >> $OUT/parity_full.log
 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 python bench.py --workload c5_cube --no-cpu --no-e2e > $OUT/bench_c5.json 2> $OUT/bench_c5.err
+python bench.py --workload c5_cube --no-cpu --no-e2e --c5-variant A > $OUT/bench_c5A.json 2> $OUT/bench_c5A.err
 python bench.py --impl reference --steps 2 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+for wl in c4_batched_2d c5_cube; do
+  CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --workload $wl"
+  $CMD > $OUT/plain_$wl.log 2>&1 && \
+    ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second --clock-control none -c 60 --csv \
+      --log-file $OUT/launches_$wl.csv $CMD > $OUT/ncu_launches_$wl.log 2>&1
+done
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
-$CMD > $OUT/plain.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-$CMD > $OUT/plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 -o $OUT/prof_fused_r01 -f $CMD > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 -o $OUT/prof_k_fused -f $CMD > $OUT/ncu_full_c4.log 2>&1
 CMD5="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --workload c5_cube"
-$CMD5 > $OUT/plain5.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_c5.csv $CMD5 > $OUT/ncu_launches5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_split_fold -s 1 -c 1 -o $OUT/prof_k_split_fold -f $CMD5 > $OUT/ncu_full_c5.log 2>&1
 echo done
