@@ -207,6 +207,36 @@ rsft_status rsft_run_host(rsft_plan_t plan, const void* h_x, int64_t batch, int6
                           int64_t capacity, int64_t* h_count, void* d_scratch,
                           size_t scratch_bytes, void* stream);
 
+/* Optimal thresholds (Eq. opt; host, fp64): minimise the worst-case per-sample
+ * SNR_min for the final targets p_d / p_fa of Problem 1, using the
+ * first-stage laws of Eq. bpd and the asymptotic Normal laws of the votes of
+ * Claims 2-3; alpha_bar / beta_bar are the permutation averages of Eq.
+ * alpha_beta for this plan's windows (alpha at the Claim 1 peak bucket of the
+ * weakest sinusoid at omega, every odd sigma, tau = 0), separable over dimensions. */
+typedef struct {
+  int32_t K;               /* sparsity budget K                                        */
+  double p_d, p_fa;        /* final per-location detection / false-alarm targets       */
+  double eta_m;            /* 6-dB bandwidth of the pre-window in bins (product over dims);
+                              <= 0: measured from the plan's windows                           */
+  double eta_p;            /* Claim 3 calibration (>= 1, 1 = lower bound, Remark 3); 0: upper
+                              bound (co-existing sinusoids detected with rate 1)              */
+  double omega[3];         /* weakest sinusoid frequency per dim, in DFT bins (e.g. 64.5)      */
+  int32_t loops;           /* T; 0 => the plan's L                                             */
+} rsft_design_params;
+
+typedef struct {
+  int32_t mu;              /* optimal second-stage threshold mu* in [T]                        */
+  double snr_min, snr_min_db;   /* SNR_min* (linear, dB)                                       */
+  double pd_bar, pfa_bar;  /* first-stage rates at the optimum                                 */
+  double gamma;            /* gamma* = sigma_n^2 beta_bar ln(1 / pfa_bar) (Eq. bpd)            */
+  double alpha_bar, beta_bar, eta_m, F;   /* inputs as used; F = T K eta_m / B (Claim 3)       */
+} rsft_design_result;
+
+/* Defaults: K = 1, p_d = 0.9, p_fa = 1e-6, eta_m measured, eta_p = 1, omega = 0.5 bins, T = L. */
+void rsft_default_design_params(rsft_design_params* d);
+/* Errors: E_ARG (ranges; infeasible design, e.g. K eta_m >= B per Remark 2 P:517). Host only. */
+rsft_status rsft_design_thresholds(rsft_plan_t plan, const rsft_design_params* d, rsft_design_result* out);
+
 /* Number of kernels the last execute/detect/compact/run_host call launched. */
 int32_t rsft_last_launch_count(rsft_plan_t plan);
 

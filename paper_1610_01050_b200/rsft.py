@@ -45,6 +45,17 @@ class RsftInfo(ctypes.Structure):
 _LIB = None
 
 
+class RsftDesignParams(ctypes.Structure):
+    _fields_ = [("K", c_int32), ("p_d", c_double), ("p_fa", c_double), ("eta_m", c_double), ("eta_p", c_double),
+                ("omega", c_double * 3), ("loops", c_int32)]
+
+
+class RsftDesignResult(ctypes.Structure):
+    _fields_ = [("mu", c_int32), ("snr_min", c_double), ("snr_min_db", c_double), ("pd_bar", c_double),
+                ("pfa_bar", c_double), ("gamma", c_double), ("alpha_bar", c_double), ("beta_bar", c_double),
+                ("eta_m", c_double), ("F", c_double)]
+
+
 def lib():
     """Load librsft.so (raises if it has not been built: no fallback path exists)."""
     global _LIB
@@ -78,6 +89,8 @@ def lib():
         "rsft_run_host": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, P(c_int64), c_void_p,
                                     c_size_t, c_void_p]),
         "rsft_last_launch_count": (c_int32, [c_void_p]),
+        "rsft_default_design_params": (None, [P(RsftDesignParams)]),
+        "rsft_design_thresholds": (c_int32, [c_void_p, P(RsftDesignParams), P(RsftDesignResult)]),
         "rsft_status_string": (ctypes.c_char_p, [c_int32]),
         "rsft_last_error": (ctypes.c_char_p, []),
     }
@@ -95,6 +108,7 @@ EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsf
             "rsft_detect", "rsft_compact",
             "rsft_detect_compact", "rsft_run",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
+            "rsft_default_design_params", "rsft_design_thresholds",
             "rsft_last_error"]
 
 
@@ -338,6 +352,20 @@ class Plan:
                                    scratch.numel(), _stream_handle(stream)))
         n = min(cnt.value, capacity)
         return h_idx[:n].numpy().copy(), cnt.value
+
+    def design_thresholds(self, K, p_d=0.9, p_fa=1e-6, eta_m=0.0, eta_p=1.0, omega=None, loops=0):
+        """Optimal thresholds (Eq. opt) for this plan's windows: dict with mu,
+        snr_min(_db), pd_bar, pfa_bar, gamma, alpha_bar, beta_bar, eta_m, F.  eta_p = 0 is
+        the upper bound of Remark 3 (co-existing sinusoids detected with rate 1)."""
+        d = RsftDesignParams()
+        lib().rsft_default_design_params(ctypes.byref(d))
+        d.K, d.p_d, d.p_fa, d.eta_m, d.eta_p, d.loops = K, p_d, p_fa, eta_m, eta_p, loops
+        if omega is not None:
+            for i, v in enumerate(omega):
+                d.omega[i] = v
+        r = RsftDesignResult()
+        _check(lib().rsft_design_thresholds(self._h, ctypes.byref(d), ctypes.byref(r)))
+        return {f: getattr(r, f) for f, _ in RsftDesignResult._fields_}
 
     def last_launch_count(self):
         return int(lib().rsft_last_launch_count(self._h))
