@@ -347,7 +347,8 @@ constexpr int kListIpt = 4;              // items per thread in LIST mode (<= 32
 
 template <int CW, int MODE, bool LIST = false>
 __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32_t* E, const int* sig_rd,
-                           const uint32_t* Xs, const uint32_t* NT, const int* kpre_s, int64_t frame, int64_t i0,
+                           const uint32_t* Xs, const uint32_t* NT, const int* kpre_s, const int* sig_ld,
+                           int64_t frame, int64_t i0,
                            int64_t d0b, int64_t d0e, uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
                            int* wsum = nullptr, uint32_t* __restrict__ slot = nullptr) {
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
@@ -410,23 +411,25 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
         }
         E[j] = e;
       }
-    } else {                                         // ballots: warp per (l, w)
-      for (int it = warp; it < L * W; it += nwarps) {
-        const int l = it / W, w = it - l * W;
-        const LoopDev& lp = pd.loops[l];
+    } else {                                         // no masks (too large): thread per E word
+      const int lg_rw = (brd > 1 ? __ffs(brd) - 1 : 0) + lgW;
+      for (int j = tid; j < L * brd * W; j += blockDim.x) {
+        const int l = j >> lg_rw, rem = j & ((1 << lg_rw) - 1);
+        const int krd = rem >> lgW, w = rem & (W - 1);
         int base = 0;
-        if (D == 3) {
-          const int kpre = (int)(((int64_t)lp.sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
-          base = lw < wpl ? (kpre * rowbits) & 31 : kpre * rowbits;
-        }
-        const int ilast = (w << 5) + lane;
-        const int klast = (int)(((int64_t)lp.sig[ld] * ilast) & (nld - 1)) >> lga_ld;
+        if (D == 3) base = lw < wpl ? (kpre_s[l] * rowbits) & 31 : kpre_s[l] * rowbits;
         const uint32_t* b = bm + (size_t)l * lw;
-        for (int krd = 0; krd < brd; ++krd) {
-          const int flat = base + krd * blast + klast;
-          const uint32_t word = __ballot_sync(0xffffffffu, (b[flat >> 5] >> (flat & 31)) & 1u);
-          if (lane == 0) E[((size_t)l * brd + krd) * W + w] = word;
+        const uint32_t sg = (uint32_t)sig_ld[l];
+        uint32_t m = (sg * (uint32_t)(w << 5)) & (uint32_t)(nld - 1);   // [sigma i]_N, i = 32 w
+        const int f0 = base + krd * blast;
+        uint32_t e = 0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {                 // M_l(i) = floor(B [sigma i]_N / N) (Def. 3)
+          const int flat = f0 + (int)(m >> lga_ld);
+          e |= ((b[flat >> 5] >> (flat & 31)) & 1u) << q;
+          m = (m + sg) & (uint32_t)(nld - 1);
         }
+        E[j] = e;
       }
     }
     __syncthreads();
@@ -518,7 +521,7 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
       }
     };
 
-    if (LIST) {
+    if constexpr (LIST) {
       // items it = tid + k * blockDim (coalesced detection-word stores); word order is
       // k-major, so the position of item (k, tid) is sum_{k' < k} T_k' + prefix_k(tid)
       uint32_t words[kListIpt][CW];
@@ -578,12 +581,14 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
       __syncthreads();                             // wsum reused by the next region
       return total;
     }
-    for (int64_t it = tid; it < nitems; it += blockDim.x) {
-      uint32_t acc[CW];
-      vote_item(it, acc);
-      if (COUNT) {
+    if constexpr (!LIST) {
+      for (int64_t it = tid; it < nitems; it += blockDim.x) {
+        uint32_t acc[CW];
+        vote_item(it, acc);
+        if (COUNT) {
 #pragma unroll
-        for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+          for (int c = 0; c < CW; ++c) cnt += __popc(acc[c]);
+        }
       }
     }
   return cnt;
@@ -1207,9 +1212,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
   const size_t xw = pd.xmask ? (size_t)L * blast * W : 0;
   uint32_t* NT = (pd.xmask && blast >= 4 && 16 * xw <= kMaxNibbleBytes) ? Xs + ((xw + 3) & ~size_t(3)) : nullptr;
   __shared__ int kpre_s[kMaxLoops];
+  __shared__ int sig_ld[kMaxLoops];                  // last-dim sigma per loop
   const int rowbits = brd * blast;                   // bits of one k_pre slab
 
-  for (int l = tid; l < L; l += blockDim.x) sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
+  for (int l = tid; l < L; l += blockDim.x) {
+    sig_rd[l] = D >= 2 ? pd.loops[l].sig[D - 2] : 0;
+    sig_ld[l] = pd.loops[l].sig[D - 1];
+  }
   if (pd.xmask) {                                    // plan-constant: once per CTA
     const int nx = L * blast * W;
     if ((nx & 3) == 0)
@@ -1253,12 +1262,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
     }
     __syncthreads();
     if (LIST) {                                      // region-local index list + count
-      const int t = vote_region<CW, MODE, true>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, frame, i0, d0b, d0e, detect,
-                                                counts, wsum, pd.region_slots + (size_t)region * kListCap);
+      const int t = vote_region<CW, MODE, true>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, sig_ld, frame, i0, d0b, d0e,
+                                                detect, counts, wsum, pd.region_slots + (size_t)region * kListCap);
       if (tid == 0) rcount[region] = (unsigned long long)t;
       continue;
     }
-    int cnt = vote_region<CW, MODE>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, frame, i0, d0b, d0e, detect, counts);
+    int cnt = vote_region<CW, MODE>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, sig_ld, frame, i0, d0b, d0e, detect,
+                                    counts);
     if (COUNT) {                                     // this region's detection count
 #pragma unroll
       for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
