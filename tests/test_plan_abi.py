@@ -137,3 +137,26 @@ def test_mode_resolution():
     assert B.Plan((4096,), (64,), 8, support=(512,)).mode == 1
     assert B.Plan((256, 256), (16, 16), 6, max_batch=1).mode == 2
     assert B.Plan((512, 128, 32), (32, 16, 8), 8).mode == 2
+
+
+def test_new_entry_points_validate_before_any_launch():
+    """rsft_run / rsft_bucketize_partial / rsft_finalize / rsft_design_thresholds: argument and
+    state errors are returned before any CUDA call (no GPU needed)."""
+    import ctypes
+    L = B.lib()
+    p = B.Plan((64, 32, 64), (8, 4, 8), 4)
+    h = p.handle
+    dummy = ctypes.c_void_p(256)
+    assert L.rsft_bucketize_partial(h, None, 0, 8, dummy, None) == 1            # E_ARG
+    assert L.rsft_bucketize_partial(h, dummy, 0, 8, dummy, None) == 7           # E_STATE (unbound)
+    assert L.rsft_finalize(h, None, 0, 4, dummy, None, None) == 1
+    assert L.rsft_finalize(h, dummy, 0, 4, dummy, None, None) == 7
+    assert L.rsft_run(h, None, 1, dummy, dummy, dummy, 10, dummy, None) == 1
+    assert L.rsft_run(h, dummy, 1, dummy, dummy, dummy, 10, dummy, None) == 7
+    with pytest.raises(B.RsftError) as e:
+        p.design_thresholds(K=100, loops=20)                                    # K eta_m >= B (Remark 2)
+    assert e.value.status == 1
+    with pytest.raises(B.RsftError):
+        p.design_thresholds(K=2, p_d=1.5)
+    r = p.design_thresholds(K=2, loops=20, omega=(3.5, 1.0, 7.25))
+    assert 1 <= r["mu"] <= 20 and r["pfa_bar"] < r["pd_bar"] and r["gamma"] > 0
