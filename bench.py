@@ -345,6 +345,8 @@ def bench_c5(a, wl, rank, world, dev):
     n0 = wl.n[0]
     d0b, d0e = shard.slab_range(rank, world, n0, plan.ntot // n0)
     hx = synth.gen_batch(wl, [0])
+    if a.c5_variant == "B" and world == 1:
+        a.c5_variant = "A"          # one GPU: the slab is the whole cube; rsft_execute is the same computation
     if a.c5_variant == "B":
         x = torch.from_numpy(np.ascontiguousarray(hx[0, d0b:d0e])).to(dev)     # this rank's slab only
         partial = torch.empty((L, plan.btot), dtype=torch.complex64, device=dev)

@@ -1291,7 +1291,8 @@ __global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __rest
   const int64_t per = (n + 1023) / 1024;
   const int64_t b = t * per, e = b + per < n ? b + per : n;
   long long s = 0;
-  for (int64_t i = b; i < e; ++i) s += (long long)counts[i];
+#pragma unroll 16
+  for (int64_t i = b; i < e; ++i) s += (long long)__ldcg(counts + i);   // independent loads in flight
   // block exclusive scan of part[] (Hillis-Steele in shared memory)
   part[t] = s;
   __syncthreads();
@@ -1303,7 +1304,8 @@ __global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __rest
   }
   long long run = part[t] - s;
   if (t == 1023) *d_count = part[t];
-  for (int64_t i = b; i < e; ++i) { long long v = (long long)counts[i]; counts[i] = (unsigned long long)run; run += v; }
+#pragma unroll 16
+  for (int64_t i = b; i < e; ++i) { long long v = (long long)__ldcg(counts + i); counts[i] = (unsigned long long)run; run += v; }
 }
 
 // One CTA per region: each thread owns 32 consecutive detection words of a pass of
