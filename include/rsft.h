@@ -135,6 +135,16 @@ rsft_status rsft_bind(rsft_plan_t plan, void* d_workspace, size_t bytes, void* s
 rsft_status rsft_execute(rsft_plan_t plan, const void* d_x, int64_t batch, int32_t loop_begin,
                          int32_t loop_end, uint32_t* d_bitmaps, void* d_spectra, void* stream);
 
+/* Segment mode ("iterations ... on different segments"; Eq. sig_model):
+ * loop l runs the first stage on segment l of each frame.
+ *   d_x        device complex64 [batch][L][N_0]...[N_{D-1}] (segment l of frame f at (f L + l) N_tot).
+ *   d_bitmaps  device uint32 [batch][L][bitmap_words]: the input of rsft_detect, unchanged.
+ *   d_spectra  NULL or device complex64 [batch][L][B_tot].
+ * Fused mode: one strided launch per loop; split mode: one launch per (frame, segment).
+ * Errors: as rsft_execute. */
+rsft_status rsft_execute_segments(rsft_plan_t plan, const void* d_x, int64_t batch, uint32_t* d_bitmaps,
+                                  void* d_spectra, void* stream);
+
 /* Slab sharding of ONE frame (SURVEY §8(e) variant B).  Pre-window, permutation, flat
  * window and aliasing (Alg. 1 l.5-8) are linear in x (Eqs. z, l: P:272-279), so
  * dim-0 slabs produce partial folded spectra that add up (in any order, up to fp32 rounding)

@@ -407,6 +407,20 @@ def rsft_run(x: np.ndarray, p: Params, tb: Tables | None = None, loops=None) -> 
     return RsftResult(st, abar, amin, amax, det, idx)
 
 
+def rsft_run_segments(xs: np.ndarray, p: Params, tb: Tables | None = None) -> RsftResult:
+    """Algorithm 1 with "iterations on different segments": loop l runs the first stage
+    on segment r_l (Eq. sig_model: fresh amplitudes and noise per segment), the
+    reverse-mapped votes accumulate over the loops as in Eq. a_i and the second stage
+    is unchanged.  xs: [L][N_0]...[N_{D-1}]."""
+    tb = make_tables(p) if tb is None else tb
+    st = [first_stage(xs[l], p, tb, l) for l in range(p.loops)]
+    abar = accumulate([s.c for s in st], p, tb)
+    amin = accumulate([s.c & ~s.ambiguous for s in st], p, tb)
+    amax = accumulate([s.c | s.ambiguous for s in st], p, tb)
+    det, idx = second_stage(abar, p.mu)
+    return RsftResult(st, abar, amin, amax, det, idx)
+
+
 # ----------------------------------------------------------------------------------
 # Brute-force references (pins only; tiny sizes)
 # ----------------------------------------------------------------------------------

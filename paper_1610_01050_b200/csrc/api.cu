@@ -9,6 +9,8 @@
 namespace rsft {
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                            void* spectra, cudaStream_t st);
+rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, void* spectra,
+                            cudaStream_t st);
 rsft_status launch_partial(rsft_plan_s* p, const void* d_x, int64_t off, int64_t len, void* d_partial,
                            cudaStream_t st);
 rsft_status launch_finalize(rsft_plan_s* p, const void* d_folded, int l0, int nl, uint32_t* bm, void* spectra,
@@ -127,6 +129,17 @@ rsft_status rsft_execute(rsft_plan_t p, const void* d_x, int64_t batch, int32_t 
   if (batch == 0) return RSFT_OK;
   return launch_execute(p, d_x, batch, loop_begin, loop_end - loop_begin, d_bitmaps, d_spectra,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+rsft_status rsft_execute_segments(rsft_plan_t p, const void* d_x, int64_t batch, uint32_t* d_bitmaps,
+                                  void* d_spectra, void* stream) {
+  if (!p || !d_x || !d_bitmaps) return RSFT_E_ARG;
+  if (!p->bound) return RSFT_E_STATE;
+  if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
+  if (reinterpret_cast<uintptr_t>(d_x) & 15) return RSFT_E_ARG;
+  p->last_launches = 0;
+  if (batch == 0) return RSFT_OK;
+  return launch_segments(p, d_x, batch, d_bitmaps, d_spectra, reinterpret_cast<cudaStream_t>(stream));
 }
 
 rsft_status rsft_bucketize_partial(rsft_plan_t p, const void* d_x_slab, int64_t off, int64_t len, void* d_partial,

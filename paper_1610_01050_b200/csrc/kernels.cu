@@ -605,7 +605,8 @@ template <int LP, int U>
 __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
                                                     int64_t batch, int l0, int nl,
                                                     uint32_t* __restrict__ bitmaps,
-                                                    float2* __restrict__ spectra) {
+                                                    float2* __restrict__ spectra, int64_t bm_stride,
+                                                    int64_t sp_stride) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int S = kStages;
   const int D = pd.D;
@@ -823,10 +824,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
         int ko = k / blast, kl = k - ko * blast;
         float2 v = F[((size_t)l * bouter + ko) * fstride + kl];
         bit = v.x * v.x + v.y * v.y > pd.loops[l0 + l].gamma;
-        if (spectra) spectra[((size_t)frame * nl + l) * pd.btot + k] = v;
+        if (spectra) spectra[(size_t)frame * sp_stride + (size_t)l * pd.btot + k] = v;
       }
       unsigned word = __ballot_sync(0xffffffffu, bit);
-      if (lane == 0) bitmaps[((size_t)frame * nl + l) * wpl + (k >> 5)] = word;
+      if (lane == 0) bitmaps[(size_t)frame * bm_stride + (size_t)l * wpl + (k >> 5)] = word;
     }
     __syncthreads();
   }
@@ -1532,12 +1533,14 @@ static rsft_status make_map(CUtensorMap* m, const void* base, int rank, const cu
 // Map for the fold kernels: D >= 2 -> [N_last][B_o][A_o][planes] (B_o, A_o of the innermost
 // outer dim, planes = batch (D == 2) or batch * n0 (D == 3)); D == 1 -> [64][N/64][batch].
 // n0 = dim-0 extent of one frame in this launch (N_0, or a slab's length for variant B).
-static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, int64_t n0, CUtensorMap* m, int u) {
+static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, int64_t n0, CUtensorMap* m, int u,
+                            int64_t frame_stride = 0) {
   const int D = p->D;
   const uint64_t e = 8;
+  if (frame_stride == 0) frame_stride = p->ntot;
   if (D == 1) {
     cuuint64_t dims[3] = {64, (cuuint64_t)(p->n[0] / 64), (cuuint64_t)batch};
-    cuuint64_t str[2] = {64 * e, (cuuint64_t)p->n[0] * e};
+    cuuint64_t str[2] = {64 * e, (cuuint64_t)frame_stride * e};
     cuuint32_t box[3] = {64, (cuuint32_t)u, 1};
     return make_map(m, d_x, 3, dims, str, box);
   }
@@ -1545,18 +1548,24 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
   const int64_t planes = D == 3 ? batch * n0 : batch;
   const int64_t rpw = nl >= 64 ? 1 : 64 / nl;
   cuuint64_t dims[4] = {(cuuint64_t)nl, (cuuint64_t)bo, (cuuint64_t)ao, (cuuint64_t)planes};
-  cuuint64_t str[3] = {(cuuint64_t)(nl * e), (cuuint64_t)(bo * nl * e), (cuuint64_t)(no * nl * e)};
+  cuuint64_t str[3] = {(cuuint64_t)(nl * e), (cuuint64_t)(bo * nl * e),
+                       (cuuint64_t)(D == 2 ? frame_stride * e : no * nl * e)};
   cuuint32_t box[4] = {(cuuint32_t)(nl >= 64 ? 64 : nl), 1, (cuuint32_t)(u * rpw), 1};
   return make_map(m, d_x, 4, dims, str, box);
 }
 
+// frame_stride (complex elements between frames), bm_stride (words) and sp_stride (complex)
+// default to the dense layouts; segment mode (rsft_execute_segments) strides over segments.
 template <int LP>
 static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
-                                  uint32_t* bm, void* spectra, cudaStream_t st) {
+                                  uint32_t* bm, void* spectra, cudaStream_t st, int64_t frame_stride = 0,
+                                  int64_t bm_stride = 0, int64_t sp_stride = 0) {
   auto kern = k_fused<LP, kU>;
   const size_t smem = fused_smem_bytes(p, nl, LP);
+  if (bm_stride == 0) bm_stride = (int64_t)nl * p->dev.wpl;
+  if (sp_stride == 0) sp_stride = (int64_t)nl * p->btot;
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, kU);
+  rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, kU, frame_stride);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
@@ -1566,7 +1575,8 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
   if (nb < 1) { set_error("k_fused: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > batch) grid = batch;
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra));
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra),
+                                               bm_stride, sp_stride);
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_fused launch");
 }
@@ -1673,6 +1683,42 @@ rsft_status launch_finalize(rsft_plan_s* p, const void* d_folded, int l0, int nl
   rsft_status s = check(cudaMemsetAsync(bm, 0, (size_t)nl * p->dev.wpl * 4, st), "bitmap reset");
   if (s) return s;
   return launch_split_fft(p, reinterpret_cast<const float2*>(d_folded), l0, nl, 1, 1, l0, nl, bm, spectra, st);
+}
+
+// Segment mode (second mode; Eq. sig_model): x [batch][L][N...], loop l runs on
+// segment l of every frame; bitmaps [batch][L][wpl], spectra [batch][L][B_tot].
+template <int LP>
+static rsft_status launch_segments_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm,
+                                           void* spectra, cudaStream_t st) {
+  const int64_t L = p->L, wpl = p->dev.wpl;
+  for (int64_t l = 0; l < L; ++l) {
+    const char* x = reinterpret_cast<const char*>(d_x) + (size_t)l * p->ntot * 8;
+    void* sp = spectra ? reinterpret_cast<char*>(spectra) + (size_t)l * p->btot * 8 : nullptr;
+    rsft_status s = launch_fused_t<LP>(p, x, batch, (int)l, 1, bm + l * wpl, sp, st, L * p->ntot, L * wpl,
+                                       L * p->btot);
+    if (s) return s;
+  }
+  return RSFT_OK;
+}
+
+rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                           void* spectra, cudaStream_t st);
+
+rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, void* spectra,
+                            cudaStream_t st) {
+  if (resolve_mode(p, batch) == RSFT_MODE_FUSED && loop_pad(1) == 2) {
+    return launch_segments_fused_t<2>(p, d_x, batch, bm, spectra, st);
+  }
+  // split mode: one launch per (frame, segment) on the contiguous segment
+  const int64_t L = p->L, wpl = p->dev.wpl;
+  for (int64_t f = 0; f < batch; ++f)
+    for (int64_t l = 0; l < L; ++l) {
+      const char* x = reinterpret_cast<const char*>(d_x) + (size_t)(f * L + l) * p->ntot * 8;
+      void* sp = spectra ? reinterpret_cast<char*>(spectra) + (size_t)(f * L + l) * p->btot * 8 : nullptr;
+      rsft_status s = launch_execute(p, x, 1, (int)l, 1, bm + (f * L + l) * wpl, sp, st);
+      if (s) return s;
+    }
+  return RSFT_OK;
 }
 
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,

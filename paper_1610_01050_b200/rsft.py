@@ -77,6 +77,7 @@ def lib():
         "rsft_workspace_bytes": (c_size_t, [c_void_p]),
         "rsft_bind": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
         "rsft_execute": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+        "rsft_execute_segments": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
         "rsft_bucketize_partial": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
         "rsft_finalize": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
         "rsft_detect": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -104,7 +105,8 @@ def lib():
 
 EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsft_set_schedule",
             "rsft_get_schedule", "rsft_get_thresholds", "rsft_get_window", "rsft_get_info",
-            "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_bucketize_partial", "rsft_finalize",
+            "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_execute_segments", "rsft_bucketize_partial",
+            "rsft_finalize",
             "rsft_detect", "rsft_compact",
             "rsft_detect_compact", "rsft_run",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
@@ -245,6 +247,21 @@ class Plan:
         sp = c_void_p(spectra.data_ptr()) if spectra is not None else None
         _check(lib().rsft_execute(self._h, c_void_p(x.data_ptr()), batch, loop_begin, loop_end,
                                   c_void_p(bitmaps.data_ptr()), sp, _stream_handle(stream)))
+        return bitmaps
+
+    def execute_segments(self, x, bitmaps=None, spectra=None, stream=None):
+        """Segment mode: x [batch, L, *n] complex64; loop l folds segment l.  Returns
+        bitmaps [batch, L, words] (the input of detect / detect_compact)."""
+        import torch
+        self._need_bind()
+        batch = x.shape[0]
+        assert x.dtype == torch.complex64 and x.is_cuda and x.is_contiguous()
+        assert x.shape[1] == self.loops and tuple(x.shape[2:]) == self.n
+        if bitmaps is None:
+            bitmaps = self.new_bitmaps(batch)
+        sp = c_void_p(spectra.data_ptr()) if spectra is not None else None
+        _check(lib().rsft_execute_segments(self._h, c_void_p(x.data_ptr()), batch, c_void_p(bitmaps.data_ptr()), sp,
+                                           _stream_handle(stream)))
         return bitmaps
 
     def bucketize_partial(self, x_slab, dim0_offset, partial=None, stream=None):

@@ -262,3 +262,37 @@ def test_variant_b_c5_full_cube():
         b2 = B.bitmap_to_bool(bm_full.cpu().numpy()[0, l], plan.btot)
         band = np.abs(np.abs(f[l]) ** 2 - gamma[l]) <= 1e-3 * gamma[l]
         assert np.all((b1 == b2) | band)
+
+
+# ----------------------------------------------------------------------------- segment mode
+@pytest.mark.parametrize("n,b,L,mode", [
+    ((128, 64), (16, 8), 5, "fused"),
+    ((1024,), (32,), 4, "fused"),
+    ((32, 16, 64), (4, 4, 8), 3, "split"),
+])
+def test_segment_mode_parity(n, b, L, mode):
+    """Segment mode (P:204): loop l folds segment l of each frame (rsft_execute_segments);
+    buckets, bits and the detection set against the oracle's rsft_run_segments."""
+    import torch
+    from paper_1610_01050_b200 import rsft as B
+    batch = 3
+    op = oracle_params(n, b, L, p_fa=1e-3, seed=41, random_tau=True, mu=max(1, L - 1))
+    wl = synth.Workload("seg", n, b, L, 1e-3, 1.0, (3, 6), (0.0, 20.0), batch * L, data_seed=19)
+    xs = frames(wl, batch * L).reshape((batch, L) + tuple(n))
+    plan = make_plan(op, max_batch=batch, mode=mode).bind()
+    xt = torch.from_numpy(np.ascontiguousarray(xs)).cuda()
+    sp = torch.empty((batch, L, plan.btot), dtype=torch.complex64, device="cuda")
+    bm = plan.execute_segments(xt, spectra=sp)
+    det = plan.detect(bm)
+    torch.cuda.synchronize()
+    tb = R.make_tables(op)
+    spn, bmn, detn = sp.cpu().numpy(), bm.cpu().numpy(), det.cpu().numpy()
+    for f in range(batch):
+        ref = R.rsft_run_segments(xs[f], op, tb)
+        for l, st in enumerate(ref.stages):
+            px = float(np.mean(np.abs(xs[f, l].astype(np.complex128)) ** 2))
+            cb = R.compare_buckets(spn[f, l].reshape(b), st, px)
+            assert cb["ok"], (f, l, cb)
+            assert R.compare_bits(B.bitmap_to_bool(bmn[f, l], plan.btot).reshape(b), st)["ok"], (f, l)
+        dset = B.bitmap_to_bool(detn[f], plan.ntot).reshape(n)
+        assert R.compare_sets(dset, ref, op.mu)["ok"], f
