@@ -247,6 +247,17 @@ void rsft_default_design_params(rsft_design_params* d);
 /* Errors: E_ARG (ranges; infeasible design, e.g. K eta_m >= B per Remark 2 P:517). Host only. */
 rsft_status rsft_design_thresholds(rsft_plan_t plan, const rsft_design_params* d, rsft_design_result* out);
 
+/* Scene generator for Monte Carlo runs (harness utility, not part of the method): writes
+ * complex64 d_x [batch][segments][N...] following Eq. sig_model / sinusoid,
+ * separable over dims: x = sum_k b_{f,k,s} prod_d e^{j 2 pi omega_{f,k,d} n_d / N_d} + nu, with
+ * b_{f,k,s} ~ CN(0, sigma_b[f][k]^2) redrawn per segment and nu ~ CN(0, sigma_n^2);
+ * counter-based random numbers (SplitMix64 + Box-Muller; synth.counter_normals mirrors them).
+ *   n[ndim]: N_d;  d_omega: device fp64 [batch][K][ndim] in DFT bins;  d_sigma_b: device fp64
+ *   [batch][K].  Errors: E_ARG, E_CUDA. */
+rsft_status rsft_synthesize(const int64_t* n, int32_t ndim, int64_t batch, int32_t segments, int32_t K,
+                            const double* d_omega, const double* d_sigma_b, double sigma_n, uint64_t seed,
+                            void* d_x, void* stream);
+
 /* Number of kernels the last execute/detect/compact/run_host call launched. */
 int32_t rsft_last_launch_count(rsft_plan_t plan);
 

@@ -91,6 +91,8 @@ def lib():
                                     c_size_t, c_void_p]),
         "rsft_last_launch_count": (c_int32, [c_void_p]),
         "rsft_default_design_params": (None, [P(RsftDesignParams)]),
+        "rsft_synthesize": (c_int32, [P(c_int64), c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_double,
+                                      c_uint64, c_void_p, c_void_p]),
         "rsft_design_thresholds": (c_int32, [c_void_p, P(RsftDesignParams), P(RsftDesignResult)]),
         "rsft_status_string": (ctypes.c_char_p, [c_int32]),
         "rsft_last_error": (ctypes.c_char_p, []),
@@ -110,7 +112,7 @@ EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsf
             "rsft_detect", "rsft_compact",
             "rsft_detect_compact", "rsft_run",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
-            "rsft_default_design_params", "rsft_design_thresholds",
+            "rsft_default_design_params", "rsft_design_thresholds", "rsft_synthesize",
             "rsft_last_error"]
 
 
@@ -386,6 +388,23 @@ class Plan:
 
     def last_launch_count(self):
         return int(lib().rsft_last_launch_count(self._h))
+
+
+def synthesize(n, batch, segments, omega, sigma_b, sigma_n, seed, out=None, stream=None):
+    """GPU scene generator (rsft_synthesize): complex64 [batch, segments, *n] per Eq. sig_model
+    with per-segment Swerling amplitudes.  omega: [batch, K, D] bins, sigma_b: [batch, K]
+    (torch fp64 CUDA tensors or None when K = 0)."""
+    import torch
+    n = tuple(int(v) for v in n)
+    K = 0 if omega is None else int(omega.shape[1])
+    if out is None:
+        out = torch.empty((batch, segments) + n, dtype=torch.complex64, device="cuda")
+    nn = (c_int64 * len(n))(*n)
+    op = c_void_p(omega.data_ptr()) if K else None
+    sp = c_void_p(sigma_b.data_ptr()) if K else None
+    _check(lib().rsft_synthesize(nn, len(n), batch, segments, K, op, sp, float(sigma_n), int(seed),
+                                 c_void_p(out.data_ptr()), _stream_handle(stream)))
+    return out
 
 
 def bitmap_to_bool(words, nbits):

@@ -120,3 +120,54 @@ def gen_ongrid(shape, bins, amps) -> np.ndarray:
     bins = np.asarray(bins, dtype=np.float64).reshape(len(amps), len(shape))
     tr = Truth(bins / np.asarray(shape, dtype=np.float64)[None, :], np.asarray(amps, dtype=np.complex128))
     return tones(tuple(shape), tr)
+
+
+# ----------------------------------------------------------------------------- counter RNG
+# NumPy mirror of the library's Monte Carlo scene generator (rsft_synthesize): SplitMix64 of
+# (seed, stream, counter) -> two 32-bit uniforms -> Box-Muller, E|z|^2 = 1.  Pure input
+# generation (no arithmetic of the method).
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _splitmix64_np(z):
+    with np.errstate(over="ignore"):
+        z = (z + np.uint64(0x9E3779B97F4A7C15)) & _M64
+        z = ((z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & _M64
+        z = ((z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & _M64
+        return z ^ (z >> np.uint64(31))
+
+
+def counter_normals(seed: int, stream: int, ctr) -> np.ndarray:
+    """CN(0, 1) samples (complex128) for counters ctr (array of non-negative ints)."""
+    ctr = np.asarray(ctr, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        key = np.uint64(seed) ^ ((np.uint64(stream) * np.uint64(0xD1B54A32D192ED03)) & _M64)
+    r = _splitmix64_np(key ^ _splitmix64_np(ctr))
+    u1 = ((r >> np.uint64(32)).astype(np.float64) + 1.0) / 4294967296.0
+    u2 = (r & np.uint64(0xFFFFFFFF)).astype(np.float64) / 4294967296.0
+    rad = np.sqrt(-np.log(u1))
+    return rad * np.exp(2j * np.pi * u2)
+
+
+def synth_segments(n, batch: int, segments: int, omega: np.ndarray, sigma_b: np.ndarray, sigma_n: float,
+                   seed: int) -> np.ndarray:
+    """NumPy reference of rsft_synthesize: [batch][segments][*n] complex128."""
+    n = tuple(int(v) for v in n)
+    D = len(n)
+    K = omega.shape[1] if omega.size else 0
+    ntot = int(np.prod(n))
+    grids = np.meshgrid(*[np.arange(v) for v in n], indexing="ij")
+    out = np.zeros((batch, segments) + n, dtype=np.complex128)
+    for f in range(batch):
+        for s in range(segments):
+            x = np.zeros(n, dtype=np.complex128)
+            for k in range(K):
+                b = counter_normals(seed, 1, [(f * K + k) * segments + s])[0] * sigma_b[f, k]
+                ph = np.zeros(n)
+                for d in range(D):
+                    ph = ph + 2.0 * np.fmod(omega[f, k, d] * grids[d], n[d]) / n[d]
+                x = x + b * np.exp(1j * np.pi * ph)
+            ctr = (f * segments + s) * ntot + np.arange(ntot)
+            x = x + sigma_n * counter_normals(seed, 2, ctr).reshape(n)
+            out[f, s] = x
+    return out
