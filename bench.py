@@ -203,6 +203,10 @@ def main_gpu(a):
     wl = synth.WORKLOADS[a.workload]
     stream = torch.cuda.current_stream()
 
+    if a.bartlett:
+        return bench_bartlett(a, wl, rank, world, dev)
+    if a.segments:
+        return bench_segments(a, wl, rank, world, dev)
     if wl.name == "c5_cube":
         return bench_c5(a, wl, rank, world, dev)
 
@@ -427,6 +431,96 @@ def bench_c5(a, wl, rank, world, dev):
     return 0
 
 
+def bench_bartlett(a, wl, rank, world, dev):
+    """Bartlett baseline (Alg. 2, App. A) on the workload's frame shape, batched: each frame is
+    T = L segments (the paper's comparison of Tables I-II: T segments vs T RSFT iterations);
+    one rsft_bartlett call per step over `frames` frames, CUDA events; reported beside the
+    RSFT line, not as the headline."""
+    import torch
+    from paper_1610_01050_b200 import rsft as B
+    stream = torch.cuda.current_stream()
+    T = wl.loops
+    per_frame = T * int(np.prod(wl.n)) * 8
+    frames = a.frames or max(1, min(512, (4 << 30) // per_frame))
+    plan = B.Plan(wl.n, wl.b, wl.loops, p_fa=wl.p_fa, noise_var=wl.noise_var, seed=wl.sched_seed).bind()
+    pool = min(frames, 16)
+    base = torch.from_numpy(synth.gen_batch(wl, range(pool * T)).reshape((pool, T) + tuple(wl.n))).to(dev)
+    reps = (frames + pool - 1) // pool
+    xs = base.repeat((reps,) + (1,) * (base.dim() - 1))[:frames].contiguous()
+    g = plan.bartlett_threshold(T, wl.p_fa)
+    power = torch.empty((frames,) + tuple(wl.n), dtype=torch.float32, device=dev)
+    det = torch.empty((frames, plan.detect_words), dtype=torch.int32, device=dev)
+    scratch = torch.empty((frames,) + tuple(wl.n), dtype=torch.complex64, device=dev)
+    for _ in range(a.warmup):
+        plan.bartlett(xs, gamma=g, power=power, detect=det, scratch=scratch)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t0.record(stream)
+    for _ in range(a.steps):
+        plan.bartlett(xs, gamma=g, power=power, detect=det, scratch=scratch)
+        launches += plan.last_launch_count()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    out = {"metric": "Bartlett baseline (Alg. 2) frames/s, T = L segments per frame", "value": frames * 1000.0 / ms,
+           "unit": "frames/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded Eq. sig_model segments)",
+           "config": {"workload": wl.name, "n": list(wl.n), "segments": T, "frames": frames, "impl": "bartlett"},
+           "gpu_launches": launches}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def bench_segments(a, wl, rank, world, dev):
+    """RSFT in segment mode: frames of T = L segments, loop l folds segment l
+    (rsft_execute_segments + rsft_detect_compact); the like-for-like partner of the Bartlett
+    baseline line (both read T x N samples per frame)."""
+    import torch
+    from paper_1610_01050_b200 import rsft as B
+    stream = torch.cuda.current_stream()
+    T = wl.loops
+    per_frame = T * int(np.prod(wl.n)) * 8
+    frames = a.frames or max(1, min(4096, (4 << 30) // per_frame))
+    plan = B.Plan(wl.n, wl.b, wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
+                  seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu, max_batch=frames).bind()
+    pool = min(frames, 16)
+    base = torch.from_numpy(synth.gen_batch(wl, range(pool * T)).reshape((pool, T) + tuple(wl.n))).to(dev)
+    reps = (frames + pool - 1) // pool
+    xs = base.repeat((reps,) + (1,) * (base.dim() - 1))[:frames].contiguous()
+    bm = plan.new_bitmaps(frames)
+    cap = frames * 4096
+    det = torch.empty((frames, plan.detect_words), dtype=torch.int32, device=dev)
+    idx = torch.empty(cap, dtype=torch.int64, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def step():
+        plan.execute_segments(xs, bitmaps=bm)
+        n = plan.last_launch_count()
+        plan.detect_compact(bm, cap, detect=det, idx=idx, count=cnt)
+        return n + plan.last_launch_count()
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t0.record(stream)
+    for _ in range(a.steps):
+        launches += step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    out = {"metric": "RSFT segment mode frames/s, T = L segments per frame", "value": frames * 1000.0 / ms,
+           "unit": "frames/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded Eq. sig_model segments)",
+           "config": {"workload": wl.name, "n": list(wl.n), "segments": T, "frames": frames, "impl": "rsft-segments",
+                      "hbm_read_gbs": frames * per_frame / (ms / 1000.0) / 1e9},
+           "gpu_launches": launches}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -439,6 +533,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--bartlett", action="store_true", help="time the Bartlett baseline (Alg. 2) instead")
+    ap.add_argument("--segments", action="store_true", help="time the RSFT in segment mode (P:204)")
     ap.add_argument("--c5-variant", default="B", choices=["A", "B"], help="c5 multi-GPU scheme (DESIGN.md §8)")
     a = ap.parse_args()
     if a.warmup < 3:

@@ -258,6 +258,19 @@ rsft_status rsft_synthesize(const int64_t* n, int32_t ndim, int64_t batch, int32
                             const double* d_omega, const double* d_sigma_b, double sigma_n, uint64_t seed,
                             void* d_x, void* stream);
 
+/* Bartlett baseline (Algorithm 2, App. A): for each frame
+ * and each of its `segments` segments u = W r_s (the plan's separable pre-window), N-D FFT
+ * (hand-written, N_d <= 4096), x += |u_hat|^2; then bit i of d_detect = (x_i / segments > gamma).
+ *   d_x      device complex64 [batch][segments][N...];  d_scratch device complex64 [batch][N_tot];
+ *   d_power  device fp32 [batch][N_tot] (x, overwritten);  d_detect NULL or uint32
+ *            [batch][detect_words].  Errors: E_ARG, E_STATE, E_UNSUPPORTED (N_d > 4096), E_CUDA. */
+rsft_status rsft_bartlett(rsft_plan_t plan, const void* d_x, int64_t batch, int32_t segments, void* d_scratch,
+                          float* d_power, double gamma, uint32_t* d_detect, void* stream);
+/* gamma of Eq. bartlettROC for a per-bin false-alarm target: the H'0 statistic is
+ * N(sigma_n^2 beta', sigma_n^4 beta'^2 / T), beta' = ||w||^2; gamma = sigma_n^2 beta'
+ * (1 + Phi^{-1}(1 - p_fa) / sqrt(T)).  Host only. */
+rsft_status rsft_bartlett_threshold(rsft_plan_t plan, int32_t segments, double p_fa, double* gamma);
+
 /* Number of kernels the last execute/detect/compact/run_host call launched. */
 int32_t rsft_last_launch_count(rsft_plan_t plan);
 

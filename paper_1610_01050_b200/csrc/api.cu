@@ -74,6 +74,25 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.ht_off[d], ht.data(), sizeof(float) * ht.size(),
                                         cudaMemcpyHostToDevice, st), "upload class-major weights"))) return s;
   }
+  {                                                // Bartlett baseline: fp32 windows, twiddles
+    static thread_local std::vector<float> bw;
+    for (int d = 0; d < p->D; ++d) {
+      bw.assign(p->prewin[d].begin(), p->prewin[d].end());
+      if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.bwin_off[d], bw.data(), 4 * bw.size(), cudaMemcpyHostToDevice, st),
+                          "upload bartlett windows"))) return s;
+    }
+    static thread_local std::vector<float> tw;
+    tw.assign(4096 + 1, 0.f);
+    tw[4096] = 1.0f;
+    for (int k = 0; k < 2048; ++k) {
+      tw[2 * k] = (float)std::cos(-2.0 * M_PI * k / 4096.0);
+      tw[2 * k + 1] = (float)std::sin(-2.0 * M_PI * k / 4096.0);
+    }
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.btw_off, tw.data(), 8 * 2048, cudaMemcpyHostToDevice, st),
+                        "upload bartlett twiddles"))) return s;
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.bone_off, &tw[4096], 4, cudaMemcpyHostToDevice, st),
+                        "upload one"))) return s;
+  }
   if (!p->xmask.empty() && p->ws.xmask_bytes == p->xmask.size() * 4)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
                                         cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
@@ -113,6 +132,9 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.region_state = reinterpret_cast<unsigned long long*>(base + p->ws.region_off);
   pd.region_capacity = p->ws.region_capacity;
   pd.region_slots = p->ws.slots_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.slots_off) : nullptr;
+  for (int d = 0; d < 3; ++d) pd.bwin[d] = d < p->D ? reinterpret_cast<const float*>(base + p->ws.bwin_off[d]) : nullptr;
+  pd.bone = reinterpret_cast<const float*>(base + p->ws.bone_off);
+  pd.btw = reinterpret_cast<const float2*>(base + p->ws.btw_off);
   p->d_ws = d_ws;
   p->bound = true;
   return RSFT_OK;

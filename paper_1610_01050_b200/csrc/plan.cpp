@@ -201,6 +201,12 @@ void layout_workspace(rsft_plan_s* p) {
   w.slots_off = off;                               // vote index lists (kListCap per region)
   w.slots_bytes = (size_t)w.region_capacity * kListCap * 4;
   off = align256(off + w.slots_bytes);
+  for (int d = 0; d < 3; ++d) {                    // Bartlett baseline tables
+    w.bwin_off[d] = off;
+    if (d < p->D) off = align256(off + 4 * (size_t)p->n[d]);
+  }
+  w.bone_off = off; off = align256(off + 4);
+  w.btw_off = off; off = align256(off + 8 * 2048);
   w.total = off;
 }
 

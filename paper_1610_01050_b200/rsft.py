@@ -91,6 +91,9 @@ def lib():
                                     c_size_t, c_void_p]),
         "rsft_last_launch_count": (c_int32, [c_void_p]),
         "rsft_default_design_params": (None, [P(RsftDesignParams)]),
+        "rsft_bartlett": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_double, c_void_p,
+                                    c_void_p]),
+        "rsft_bartlett_threshold": (c_int32, [c_void_p, c_int32, c_double, P(c_double)]),
         "rsft_synthesize": (c_int32, [P(c_int64), c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_double,
                                       c_uint64, c_void_p, c_void_p]),
         "rsft_design_thresholds": (c_int32, [c_void_p, P(RsftDesignParams), P(RsftDesignResult)]),
@@ -113,6 +116,7 @@ EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsf
             "rsft_detect_compact", "rsft_run",
             "rsft_host_scratch_bytes", "rsft_run_host", "rsft_last_launch_count", "rsft_status_string",
             "rsft_default_design_params", "rsft_design_thresholds", "rsft_synthesize",
+            "rsft_bartlett", "rsft_bartlett_threshold",
             "rsft_last_error"]
 
 
@@ -385,6 +389,35 @@ class Plan:
         r = RsftDesignResult()
         _check(lib().rsft_design_thresholds(self._h, ctypes.byref(d), ctypes.byref(r)))
         return {f: getattr(r, f) for f, _ in RsftDesignResult._fields_}
+
+    def bartlett(self, x, gamma=None, p_fa=None, power=None, detect=None, scratch=None, stream=None):
+        """Bartlett baseline (Alg. 2): x [batch, segments, *n] (or [segments, *n]) complex64 ->
+        (power x [batch, *n], detect bitmap [batch, words])."""
+        import torch
+        self._need_bind()
+        single = x.dim() == len(self.n) + 1
+        xb = x.unsqueeze(0) if single else x
+        batch, T = xb.shape[0], xb.shape[1]
+        assert xb.dtype == torch.complex64 and xb.is_cuda and xb.is_contiguous() and tuple(xb.shape[2:]) == self.n
+        if gamma is None:
+            gamma = self.bartlett_threshold(T, p_fa if p_fa is not None else 1e-6)
+        if power is None:
+            power = torch.empty((batch,) + self.n, dtype=torch.float32, device=self.device)
+        if detect is None:
+            detect = torch.empty((batch, self.detect_words), dtype=torch.int32, device=self.device)
+        if scratch is None:
+            scratch = torch.empty((batch,) + self.n, dtype=torch.complex64, device=self.device)
+        _check(lib().rsft_bartlett(self._h, c_void_p(xb.data_ptr()), batch, T, c_void_p(scratch.data_ptr()),
+                                   c_void_p(power.data_ptr()), float(gamma), c_void_p(detect.data_ptr()),
+                                   _stream_handle(stream)))
+        if single:
+            return power[0], detect[0]
+        return power, detect
+
+    def bartlett_threshold(self, segments, p_fa):
+        g = c_double(0.0)
+        _check(lib().rsft_bartlett_threshold(self._h, segments, p_fa, ctypes.byref(g)))
+        return g.value
 
     def last_launch_count(self):
         return int(lib().rsft_last_launch_count(self._h))
