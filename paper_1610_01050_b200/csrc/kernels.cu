@@ -173,6 +173,43 @@ __device__ __forceinline__ void lane_fold(float2 (&acc)[LP][2], int blast) {
   }
 }
 
+// Residue fold through shared memory (reduce over the lanes that share residues, written
+// to slot[l][r]; segments add).  Same sums as lane_fold, a quarter of its instructions at
+// B_last = 8: every lane stores its LP float4 (acc[l][0], acc[l][1]) to scr[l][lane] (odd l
+// xor-swizzled by 4 slots, so the reads below are bank-conflict free), then each lane sums
+// the 32 / (B_last / 2) entries of an item (l, q) and writes residues 2q, 2q + 1.
+// 2 <= B_last <= 32; scr holds LP x 32 float4 and is free (a consumed TMA stage).
+template <int LP>
+__device__ __forceinline__ void fold_smem(const float2 (&acc)[LP][2], float4* scr, float2* slot, int lane, int blast,
+                                          int lghq, int nl, bool first) {
+#pragma unroll
+  for (int l = 0; l < LP; ++l)
+    scr[l * 32 + (lane ^ ((l & 1) << 2))] = make_float4(acc[l][0].x, acc[l][0].y, acc[l][1].x, acc[l][1].y);
+  __syncwarp();
+  const int hq = 1 << lghq, G = 32 >> lghq;
+  for (int it = lane; it < LP * hq; it += 32) {
+    const int l = it >> lghq, q = it & (hq - 1);
+    const float4* src = scr + l * 32;
+    const int sw = (l & 1) << 2;
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+    for (int g = 0; g < G; ++g) {
+      const float4 v = src[(g * hq + q) ^ sw];
+      s0 = __fadd2_rn(s0, make_float2(v.x, v.y));
+      s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
+    }
+    if (l < nl) {
+      float4* d = reinterpret_cast<float4*>(slot + l * blast + 2 * q);
+      if (first) *d = make_float4(s0.x, s0.y, s1.x, s1.y);
+      else {
+        const float4 o = *d;
+        *d = make_float4(o.x + s0.x, o.y + s0.y, o.z + s1.x, o.w + s1.y);
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // scr is a TMA stage again
+  __syncwarp();
+}
+
 template <int LP>
 __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float* __restrict__ hlast,
                                                int l0, int nl, int nlast, int col, int blast) {
@@ -850,6 +887,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int LP, int U, int RPW>
@@ -911,6 +951,29 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
                                          ((size_t)LP * nlast * 4 <= kSplitHlastBytes ? (size_t)LP * nlast * 4 : 0));
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = c_tw128[i];
   __syncthreads();
+  // last-dim DFT factors e^{-j pi b_l(r) (2k + 1) / B} [or e^{-j 2 pi b_l(r) k / B}],
+  // b_l(r) = sigma^{-1}(r - tau) mod B_last, as (T, jT) float4 [r][l][k] (I3, L1)
+  const int dl = D - 1, lgbl = pd.lgb[dl], shl = pd.shift[dl];
+  const float4* dtab = nullptr;
+  if ((size_t)LP * blast * blast * 16 <= kSplitDftBytes) {
+    float4* t = reinterpret_cast<float4*>(tws + 128);
+    const int m2 = shl ? 2 * blast - 1 : blast - 1;
+    const int tsh = shl ? 6 - lgbl : 7 - lgbl;
+    for (int i = threadIdx.x; i < LP * blast * blast; i += blockDim.x) {
+      const int r = i / (LP * blast), rem = i - r * (LP * blast);
+      const int l = rem >> lgbl, k = rem & (blast - 1);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (l < nl) {
+        const LoopDev& lp = pd.loops[l0 + l];
+        const int b = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
+        const float2 w = tws[((b * (shl ? 2 * k + 1 : k)) & m2) << tsh];
+        v = make_float4(w.x, w.y, -w.y, w.x);
+      }
+      t[i] = v;
+    }
+    __syncthreads();
+    dtab = t;
+  }
   // zero the parts of the weight tables cp.async never writes: padded loops and pad rows
   for (int i = lane; i < 2 * hs_f; i += 32) hsb[i] = 0.f;
 
@@ -934,8 +997,25 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   };
   // stage h0[l0 + l][(a0_base + chunk A0c + a) B0 + r0] (a < A0c) [and h1[l0 + l][r1 + B1 a1]]
   // from the class-major tables into hs with an LP row stride (cp.async, waited per unit)
+  const bool stage16 = ((nl | l0 | pd.L) & 3) == 0;
   auto stage = [&](const Unit& t, float* h) {
     const float* s0 = pd.ht[0] + ((size_t)t.r0 * A0 + a0_base + t.chunk * A0c) * pd.L + l0;
+    if (stage16) {                                   // 16-B copies: rows of nl loops, 16-B aligned
+      const int nl4 = nl >> 2;
+      for (int i = lane; i < A0c * nl4; i += 32) {
+        const int a = i / nl4, l = (i - a * nl4) << 2;
+        cp_async16(h + a * LP + l, s0 + (size_t)a * pd.L + l);
+      }
+      if (D == 3) {
+        const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + l0;
+        float* h1 = h + A0c * LP;
+        for (int i = lane; i < A1 * nl4; i += 32) {
+          const int a = i / nl4, l = (i - a * nl4) << 2;
+          cp_async16(h1 + a * LP + l, s1 + (size_t)a * pd.L + l);
+        }
+      }
+      return;
+    }
     for (int i = lane; i < A0c * nl; i += 32) {
       const int a = i / nl, l = i - a * nl;
       cp_async4(h + a * LP + l, s0 + (size_t)a * pd.L + l);
@@ -1070,12 +1150,13 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
         }
       }
       // column weights of this segment + cross-lane residue fold -> slot[l][r] (segments add)
-      if (hl_smem) {
-        colweight_plain<LP>(acc, hl_smem, nlast, seg * 64 + 2 * lane_c4);
-        lane_fold<LP>(acc, blast);
-      } else {
-        colweight_fold<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane_c4, blast);
+      if (hl_smem) colweight_plain<LP>(acc, hl_smem, nlast, seg * 64 + 2 * lane_c4);
+      else colweight<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane_c4);
+      if (LP <= kUSplit && blast >= 2 && blast <= 32) {
+        fold_smem<LP>(acc, ring + (size_t)((c_st + S - 1) % S) * U * 32, slot, lane, blast, lgbl - 1, nl, seg == 0);
+        continue;
       }
+      lane_fold<LP>(acc, blast);
       if (lane < fold_lanes) {
 #pragma unroll
         for (int l = 0; l < LP; ++l)
@@ -1092,8 +1173,23 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
     //   F[l][k][kappa] = sum_r slot[l][r] e^{-j pi b_l(r) (2k + 1) / B},  b_l(r) = sigma^{-1}(r - tau)
     // (no shift when B_last = N_last: e^{-j 2 pi b k / B}).  Written per dim-0 chunk;
     // k_split_fft adds the chunks in order (deterministic, no atomics).
-    {
-      const int dl = D - 1, lgbl = pd.lgb[dl], shl = pd.shift[dl];
+    if (dtab) {
+      float2* dst = R + (size_t)t.frame * nl * blast * nchunk * bouter + (size_t)t.chunk * bouter + t.kappa;
+      for (int i = lane; i < nl * blast; i += 32) {
+        const int l = i >> lgbl, k = i & (blast - 1);
+        const float2* row = slot + l * blast;
+        const float4* tk = dtab + l * blast + k;
+        float2 v = make_float2(0.f, 0.f);
+#pragma unroll 8
+        for (int r = 0; r < blast; ++r) {
+          const float2 x = row[r];
+          const float4 w = tk[r * LP * blast];
+          v = __ffma2_rn(make_float2(x.x, x.x), make_float2(w.x, w.y), v);
+          v = __ffma2_rn(make_float2(x.y, x.y), make_float2(w.z, w.w), v);
+        }
+        dst[(size_t)i * nchunk * bouter] = v;
+      }
+    } else {
       float2* dst = R + (size_t)t.frame * nl * blast * nchunk * bouter + (size_t)t.chunk * bouter + t.kappa;
       const int m2 = shl ? 2 * blast - 1 : blast - 1;     // twiddle index mod 2B (shift) or B
       const int tsh = shl ? 6 - lgbl : 7 - lgbl;

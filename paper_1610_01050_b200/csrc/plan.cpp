@@ -230,7 +230,9 @@ size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c) {
   SplitWarpLayout w = split_warp_layout(D, lpad, nl, (int)a0c, D == 3 ? (int)p->a[1] : 1, (int)p->b[D - 1], nseg,
                                         nlast >= 64 ? 1 : (int)(64 / nlast));
   const size_t hl = (size_t)lpad * nlast * 4;
-  return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0) + 128 * 8;
+  const size_t dft = (size_t)lpad * p->b[D - 1] * p->b[D - 1] * 16;
+  return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0) + 128 * 8 +
+         (dft <= (size_t)kSplitDftBytes ? dft : 0);
 }
 
 // Split-mode work units are (frame, outer residue class, dim-0 chunk) per WARP.  Chunk the

@@ -47,6 +47,7 @@ constexpr int kThreadsSplit = RSFT_SPLIT_THREADS; // threads per CTA ...
 constexpr int kCtasSplit = RSFT_SPLIT_CTAS;       // ... and CTAs per SM the kernel is built for
 constexpr int kSplitUnitsPerWarp = 4;
 constexpr int kListCap = 2048;                   // vote: region-local index slots per region
+constexpr int kSplitDftBytes = 16384;            // split-mode last-dim DFT factor table [r][l][k] (float4) up to this size
 constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in smem up to this size             // chunking target: >= this many units per warp
 
 #ifdef __CUDACC__
