@@ -1210,6 +1210,359 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Split-mode fold on the tensor cores (D == 3, N_last == 64, L <= 16, A_1 % 16 == 0).
+// Per residue class the fold is the dense contraction C[m][l] = sum_rows X[row][m] W[row][l]
+// (m = 128 real columns of the 64 complex samples of a row, l = loop, W[row][l] =
+// h0_l[a0] h1_l[a1], identity I3), run as 3xTF32 tcgen05.mma (kind::tf32, fp32 accumulators
+// in TMEM): X = Xh + Xl, W = Wh + Wl with Xh, Wh the tf32 truncations (the tensor core
+// truncates fp32 operands, scripts/micro/umma_tf32.cu) and Xl, Wl the exact fp32 remainders;
+// C = Xh (Wh | Wl) + Xl Wh, relative error ~2^-20 (the dropped Xl Wl term).  A = X^T comes
+// from TMEM (lane m = real column m, one TMEM column per row): shared-memory operand tiles
+// would have to be K-major (tcgen05 takes tf32 from shared memory K-major only; MN-major
+// returned zeros in scripts/micro/umma_tf32.cu) and their extra traffic made the kernel
+// shared-memory bound; B = the weights, K-major in shared memory.
+// Persistent, one CTA per SM, 14 warps:
+//   warps 0-7   workers, two groups of 4 taking alternate stage PAIRS: thread m of the
+//               group reads column m of the X stage (TMA box, row-major), splits it into
+//               Xh / Xl and stores both to its TMEM lane (tcgen05.st); the group writes the
+//               K-major weight tiles (Wh | Wl); after a group barrier the group's first warp
+//               issues the pair's 8 MMAs into the GROUP's accumulator (one per group: the two
+//               groups' partial sums are added in a fixed order, so results are deterministic)
+//   warp 8      TMA producer (lane 0), 16-row boxes into a kMmaSX-deep ring
+//   warp 9      TMEM owner: accumulators (2 classes in flight x 2 groups x 32 columns) and
+//               the A stages (kMmaSP pairs x 2 stages x 32 columns)
+//   warps 10-13 epilogue: TMEM -> (Wh | Wl) halves and groups summed, column weights h_last,
+//               residue fold (shared memory), last-dim DFT (factor table) -> R
+// One class = a0_count x A_1 rows of one (frame, r0, r1); one stage = 16 rows (one a0).
+// ------------------------------------------------------------------------------------
+// X ring: kMmaSX stage slots; operand ring (TMEM A + shared-memory W): kMmaSP pair slots
+#ifndef RSFT_MMA_SX
+#define RSFT_MMA_SX 16
+#endif
+#ifndef RSFT_MMA_SP
+#define RSFT_MMA_SP 4
+#endif
+constexpr int kMmaSX = RSFT_MMA_SX, kMmaSP = RSFT_MMA_SP, kMmaThreads = 448, kMmaLP = 16, kMmaEStride = 144;
+constexpr int kMmaWorkers = 8, kMmaProd = 8, kMmaTmem = 9, kMmaEpi0 = 10;   // warp roles
+constexpr int kMmaWStage = 2048;                                           // (Wh | Wl) per stage
+static_assert(128 + kMmaSP * 2 * 32 <= 512, "TMEM columns");
+
+struct MmaLayout {
+  int x, op, tab, tab_stride, hl, tws, dtab, e, slot, bar, taddr, total;
+};
+RSFT_HD inline MmaLayout mma_layout(int a0c, int a1, int nlast, int blast) {
+  MmaLayout L;
+  int off = 0;
+  L.x = off; off += kMmaSX * 8192;
+  L.op = off; off += kMmaSP * 2 * kMmaWStage;
+  L.tab = off; L.tab_stride = (a0c + a1) * kMmaLP * 4; off += 2 * L.tab_stride;
+  L.hl = off; off += kMmaLP * nlast * 4;
+  L.tws = off; off += 128 * 8;
+  L.dtab = off; off += kMmaLP * blast * blast * 16;
+  L.e = off; off += kMmaLP * kMmaEStride * 4;
+  L.slot = off; off += kMmaLP * blast * 8;
+  off = (off + 15) / 16 * 16;
+  L.bar = off; off += (2 * kMmaSX + kMmaSP + 4) * 8;
+  L.taddr = off; off += 16;
+  L.total = off;
+  return L;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  // no swizzle, K-major canonical layout; version 1 (sm_100)
+  return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// warp-wide call sites (uniform descriptors stay in uniform registers); one elected lane issues
+__device__ __forceinline__ void umma_tf32_elect(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+               "setp.ne.b32 p, %4, 0;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+               :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+               "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+               :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                  "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+                  "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+                  "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+               : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(kMmaThreads, 1)
+k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch, int a0_base,
+            int a0_count, float2* __restrict__ R, uint32_t* __restrict__ zero_bm, int64_t zero_words) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int LP = kMmaLP;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int D = pd.D;                                  // == 3
+  const int nlast = pd.nlast, blast = pd.blast, bouter = pd.bouter;
+  const int B0 = pd.b[0], B1 = pd.b[1], A0 = pd.a[0], A1 = pd.a[1], lgb1 = pd.lgb[1];
+  const int nst = a0_count * (A1 >> 4);               // 16-row stages per class (one a0, 16 a1 each)
+  const int npairs = nst >> 1;                         // even, >= 2 (launcher)
+  const MmaLayout ly = mma_layout(a0_count, A1, nlast, blast);
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + ly.bar);
+  uint64_t* xempty = xfull + kMmaSX;
+  uint64_t* opempty = xempty + kMmaSX;
+  uint64_t* accfull = opempty + kMmaSP;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(smem + ly.taddr);
+  float* hl = reinterpret_cast<float*>(smem + ly.hl);
+  float2* tws = reinterpret_cast<float2*>(smem + ly.tws);
+  float4* dtab = reinterpret_cast<float4*>(smem + ly.dtab);
+  const int64_t nunits = batch * bouter;
+
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + t; w < zero_words; w += (int64_t)gridDim.x * blockDim.x)
+    zero_bm[w] = 0u;
+  // column weights h_last[l0 + l][c] (zero rows for padded loops), twiddles
+  for (int i = t; i < LP * nlast; i += blockDim.x) {
+    const int l = i / nlast, c = i - l * nlast;
+    hl[i] = l < nl ? pd.h[D - 1][(size_t)(l0 + l) * nlast + c] : 0.f;
+  }
+  for (int i = t; i < 128; i += blockDim.x) tws[i] = c_tw128[i];
+  // zero both class-table buffers (padded loops stay zero; cp.async writes l < nl)
+  for (int i = t; i < 2 * ly.tab_stride / 4; i += blockDim.x) reinterpret_cast<float*>(smem + ly.tab)[i] = 0.f;
+  if (t == 0) {
+    for (int i = 0; i < kMmaSX; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4); }   // 4 warps of a group
+    for (int i = 0; i < kMmaSP; ++i) mbar_init(&opempty[i], 1);                              // MMA commit
+    for (int i = 0; i < 2; ++i) { mbar_init(&accfull[i], 2); mbar_init(&accempty[i], 4); }  // 2 groups / 4 epi warps
+    fence_mbar_init();
+  }
+  if (warp == kMmaTmem) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(taddr_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = *taddr_s;
+  {  // last-dim DFT factors e^{-j pi b_l(r) (2k + 1) / B} [or e^{-j 2 pi b_l(r) k / B}] as (T, jT) [r][l][k]
+    const int dl = D - 1, lgbl = pd.lgb[dl], shl = pd.shift[dl];
+    const int m2 = shl ? 2 * blast - 1 : blast - 1;
+    const int tsh = shl ? 6 - lgbl : 7 - lgbl;
+    for (int i = t; i < LP * blast * blast; i += blockDim.x) {
+      const int r = i / (LP * blast), rem = i - r * (LP * blast);
+      const int l = rem >> lgbl, k = rem & (blast - 1);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (l < nl) {
+        const LoopDev& lp = pd.loops[l0 + l];
+        const int b = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
+        const float2 w = tws[((b * (shl ? 2 * k + 1 : k)) & m2) << tsh];
+        v = make_float4(w.x, w.y, -w.y, w.x);
+      }
+      dtab[i] = v;
+    }
+  }
+  __syncthreads();
+
+  if (warp < kMmaWorkers) {
+    // ---------------- workers (+ MMA issue by each group's first warp) ----------------
+    float* tab = reinterpret_cast<float*>(smem + ly.tab);
+    const int tabf = ly.tab_stride / 4;
+    const int nl4 = nl >> 2;
+    auto stage_tables = [&](int64_t u, float* dst) {
+      const int kappa = (int)(u % bouter);
+      const int r0 = kappa >> lgb1, r1 = kappa & (B1 - 1);
+      const float* s0 = pd.ht[0] + ((size_t)r0 * A0 + a0_base) * pd.L + l0;
+      for (int i = t; i < a0_count * nl4; i += 32 * kMmaWorkers) {
+        const int a = i / nl4, l = (i - a * nl4) << 2;
+        cp_async16(dst + a * LP + l, s0 + (size_t)a * pd.L + l);
+      }
+      const float* s1 = pd.ht[1] + (size_t)r1 * A1 * pd.L + l0;
+      float* d1 = dst + a0_count * LP;
+      for (int i = t; i < A1 * nl4; i += 32 * kMmaWorkers) {
+        const int a = i / nl4, l = (i - a * nl4) << 2;
+        cp_async16(d1 + a * LP + l, s1 + (size_t)a * pd.L + l);
+      }
+    };
+    constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+    constexpr uint32_t id16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint64_t dw0 = umma_desc(smem_u32(smem + ly.op), 512, 128);
+    const int kq = warp & 3, grp = warp >> 2;
+    const int m = kq * 32 + lane;                      // this thread's real column = TMEM lane
+    const uint32_t lane_off = (uint32_t)(kq * 32) << 16;
+    int lgJ = 0;
+    while ((16 << lgJ) < A1) ++lgJ;
+    // pair P = (ci nst + gl) / 2 goes to group P & 1 and uses x slots 2 (P mod SX/2) + {0, 1}
+    // and operand pair slot P mod SP (TMEM A columns, shared-memory W tiles)
+    int64_t ci = 0;
+    if ((int64_t)blockIdx.x < nunits) stage_tables(blockIdx.x, tab);
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++ci) {
+      cp_async_wait_all();
+      named_bar(1, 32 * kMmaWorkers);
+      if (u + gridDim.x < nunits) stage_tables(u + gridDim.x, tab + ((ci + 1) & 1) * tabf);
+      const float* h0s = tab + (ci & 1) * tabf;
+      const float* h1s = h0s + a0_count * LP;
+      const int buf = (int)(ci & 1);
+      const uint32_t dacc = taddr + (uint32_t)(buf * 2 + grp) * 32;
+      const int pl0 = (int)((grp + ci * npairs) & 1);
+      for (int pl = pl0; pl < npairs; pl += 2) {
+        const uint32_t P = (uint32_t)(ci * npairs + pl);
+        const int x = 2 * (int)(P % (kMmaSX / 2)), op = (int)(P % kMmaSP);
+        const uint32_t xph = (P / (kMmaSX / 2)) & 1, oph = (P / kMmaSP) & 1;
+        float* wsl = reinterpret_cast<float*>(smem + ly.op + op * 2 * kMmaWStage);
+        const uint32_t acol = taddr + 128 + (uint32_t)(op * 2) * 32;
+        mbar_wait(&opempty[op], oph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {                  // weight tiles: rows 4 kq + j, column n = lane
+          const int gl = 2 * pl + h;
+          const int a0l = gl >> lgJ, a1b = (gl & ((1 << lgJ) - 1)) << 4;
+          const int n = lane, l = n & 15;
+          const float h0v = h0s[a0l * LP + l];
+          float wv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float w = h0v * h1s[(a1b + 4 * kq + j) * LP + l];
+            wv[j] = n < 16 ? w : w - tf32_trunc(w);
+          }
+          *reinterpret_cast<float4*>(wsl + h * (kMmaWStage / 4) + (((kq * 4 + (n >> 3)) * 8 + (n & 7)) << 2)) =
+              make_float4(wv[0], wv[1], wv[2], wv[3]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {                  // A = X^T: column m of the stage -> TMEM lane m
+          mbar_wait(&xfull[x + h], xph);
+          const float* xs = reinterpret_cast<const float*>(smem + ly.x + (x + h) * 8192) + m;
+          uint32_t v[32];
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const float xv = xs[r * 128];
+            v[r] = __float_as_uint(xv);                                  // Xh: the tensor core truncates
+            v[16 + r] = __float_as_uint(xv - tf32_trunc(xv));            // Xl, exact
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xempty[x + h]);
+          tmem_st32(acol + h * 32 + lane_off, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");    // W tiles -> tensor core
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        named_bar(2 + grp, 128);                       // the group's operands are complete
+        if (kq == 0) {
+          if (pl == pl0) mbar_wait(&accempty[buf], (((uint32_t)(ci >> 1)) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#if RSFT_MMA_DEBUG != 3
+          const uint64_t so = (uint64_t)((op * 2 * kMmaWStage) >> 4);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const uint64_t sw = so + (uint64_t)((h * kMmaWStage + c * 1024) >> 4);
+              const uint32_t ah = acol + h * 32 + c * 8;
+              umma_tf32_elect(dacc, ah, dw0 + sw, id32, (pl > pl0 || h > 0 || c > 0) ? 1u : 0u);
+              umma_tf32_elect(dacc, ah + 16, dw0 + sw, id16, 1u);
+            }
+#endif
+          umma_commit_elect(&opempty[op]);
+          if (pl + 2 >= npairs) umma_commit_elect(&accfull[buf]);
+        }
+      }
+    }
+  } else if (warp == kMmaProd) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int x = 0;
+      uint32_t ph = 0;
+      const uint64_t tm = reinterpret_cast<uint64_t>(&tmap);
+      const int plane_stride = a0_count * B0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int frame = (int)(u / bouter), kappa = (int)(u % bouter);
+        const int r0 = kappa >> lgb1, r1 = kappa & (B1 - 1);
+        int a0l = 0, a1b = 0;
+        for (int gl = 0; gl < nst; ++gl) {
+          mbar_wait(&xempty[x], ph ^ 1);
+#if RSFT_MMA_DEBUG == 2                               // compute ceiling: no HBM traffic
+          mbar_arrive(&xfull[x]);
+#else
+          mbar_expect_tx(&xfull[x], 8192u);
+          tma_load_4d(smem + ly.x + x * 8192, tm, 0, r1, a1b, frame * plane_stride + a0l * B0 + r0, &xfull[x]);
+#endif
+          if (++x == kMmaSX) { x = 0; ph ^= 1; }
+          if ((a1b += 16) == A1) { a1b = 0; ++a0l; }
+        }
+      }
+    }
+  } else if (warp >= kMmaEpi0) {
+    // ---------------- epilogue ----------------
+    const int e = t - kMmaEpi0 * 32, quarter = warp & 3, m = quarter * 32 + lane, c = m >> 1;
+    float* E = reinterpret_cast<float*>(smem + ly.e);
+    float* slotf = reinterpret_cast<float*>(smem + ly.slot);
+    const float2* slot = reinterpret_cast<const float2*>(slotf);
+    const int lgbl = pd.lgb[D - 1];
+    const int per = 64 / blast;                        // columns per residue (N_last = 64)
+    int64_t ci = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++ci) {
+      const int frame = (int)(u / bouter), kappa = (int)(u % bouter);
+      const int buf = (int)(ci & 1);
+      mbar_wait(&accfull[buf], ((uint32_t)(ci >> 1)) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r0v[32], r1v[32];
+      const uint32_t ta = taddr + (uint32_t)(buf * 64) + ((uint32_t)(quarter * 32) << 16);
+      tmem_ld32(ta, r0v);
+      tmem_ld32(ta + 32, r1v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[buf]);
+      // group 0 + group 1, each (Xh Wh + Xl Wh) + Xh Wl, then the column weight
+#pragma unroll
+      for (int l = 0; l < LP; ++l)
+        E[l * kMmaEStride + m] = ((__uint_as_float(r0v[l]) + __uint_as_float(r0v[16 + l])) +
+                                  (__uint_as_float(r1v[l]) + __uint_as_float(r1v[16 + l]))) * hl[l * nlast + c];
+      named_bar(4, 128);
+      for (int it = e; it < LP * 2 * blast; it += 128) {         // (l, r, part): residue sums
+        const int l = it / (2 * blast), rp = it - l * 2 * blast;
+        const float* src = E + l * kMmaEStride + rp;
+        float acc = 0.f;
+        for (int j = 0; j < per; ++j) acc += src[2 * blast * j];
+        slotf[it] = acc;
+      }
+      named_bar(4, 128);
+      float2* dst = R + (size_t)frame * nl * blast * bouter + kappa;
+      for (int i = e; i < nl * blast; i += 128) {                // last-dim DFT (I3, L1)
+        const int l = i >> lgbl, k = i & (blast - 1);
+        const float2* row = slot + l * blast;
+        const float4* tk = dtab + l * blast + k;
+        float2 v = make_float2(0.f, 0.f);
+        for (int rr = 0; rr < blast; ++rr) {
+          const float2 xv = row[rr];
+          const float4 w = tk[rr * LP * blast];
+          v = __ffma2_rn(make_float2(xv.x, xv.x), make_float2(w.x, w.y), v);
+          v = __ffma2_rn(make_float2(xv.y, xv.y), make_float2(w.z, w.w), v);
+        }
+        dst[(size_t)i * bouter] = v;
+      }
+      named_bar(4, 128);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == kMmaTmem) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(taddr));
+}
+
 // Split mode, kernel 2: one CTA per (loop, k_last, frame).  From the folded spectra F (k_last
 // domain, one slice per dim-0 chunk): sum the chunks in order, outer relabelling
 // b_d = sigma^{-1}(r_d - tau_d) mod B_d + half twiddles e^{-j pi b_d / B_d} (I3, L1), outer-dims
@@ -1679,10 +2032,42 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
 
 // Split-mode fold of dim-0 rows [a0_base*B0, (a0_base + a0_count)*B0) of `batch` frames
 // into residue sums R [batch][nl][B_outer][B_last]; zeroes zero_words bitmap words.
+// Tensor-core split fold (k_split_mma): c5-like shapes, one class per CTA iteration (no chunks).
+static bool mma_fold_ok(const rsft_plan_s* p, int64_t batch, int l0, int nl, int64_t a0_count) {
+  static const bool off = getenv("RSFT_NO_MMA") != nullptr;
+  if (off || p->D != 3 || p->n[2] != 64 || p->a[1] % 16 != 0 || nl > kMmaLP || (nl | l0 | p->L) % 4 != 0) return false;
+  const int64_t nst = a0_count * (p->a[1] / 16);                   // 16-row stages per class
+  if (nst % 2 != 0 || nst < 4) return false;                        // stage pairs, both worker groups busy
+  const int64_t blast = p->b[2];
+  if ((int64_t)kMmaLP * blast * blast * 16 > kSplitDftBytes) return false;
+  if (batch * nl * p->btot > p->dev.fbuf_capacity) return false;
+  return mma_layout((int)a0_count, (int)p->a[1], 64, (int)blast).total <= 227 * 1024;
+}
+
+static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, int64_t a0_base,
+                                    int64_t a0_count, uint32_t* zero_bm, int64_t zero_words, cudaStream_t st) {
+  const size_t smem = (size_t)mma_layout((int)a0_count, (int)p->a[1], 64, (int)p->b[2]).total;
+  CUtensorMap tmap;
+  rsft_status s = fold_map(p, d_x, batch, a0_count * p->b[0], &tmap, kUSplit);
+  if (s) return s;
+  s = check(cudaFuncSetAttribute(k_split_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  const int64_t units = batch * p->dev.bouter;
+  const int64_t grid = units < p->num_sms ? units : p->num_sms;
+  k_split_mma<<<(unsigned)grid, kMmaThreads, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count,
+                                                         p->dev.fbuf, zero_bm, zero_words);
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_split_mma launch");
+}
+
 template <int LP>
 static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                        int64_t a0_base, int64_t a0_count, int* lg_out, uint32_t* zero_bm,
                                        int64_t zero_words, cudaStream_t st) {
+  if (LP <= kMmaLP && mma_fold_ok(p, batch, l0, nl, a0_count)) {
+    *lg_out = 0;
+    return launch_split_mma(p, d_x, batch, l0, nl, a0_base, a0_count, zero_bm, zero_words, st);
+  }
   auto kern = p->n[p->D - 1] >= 64 ? k_split_fold<LP, kUSplit, 1> : k_split_fold<LP, kUSplit, 2>;
   const int64_t per = (int64_t)nl * p->btot;          // folded spectrum elements per frame and chunk
   int lg = split_lg_chunks(p, batch, nl, a0_count, (int64_t)p->num_sms * (kThreadsSplit / 32) * (LP >= 24 ? 1 : kCtasSplit));

@@ -51,6 +51,9 @@ constexpr int kSplitDftBytes = 16384;            // split-mode last-dim DFT fact
 constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in smem up to this size             // chunking target: >= this many units per warp
 
 #ifdef __CUDACC__
+#ifndef RSFT_MMA_DEBUG
+#define RSFT_MMA_DEBUG 0   // k_split_mma measurement variants: 1 = no operand work, 2 = no TMA, 3 = no MMA
+#endif
 #define RSFT_HD __host__ __device__
 #else
 #define RSFT_HD

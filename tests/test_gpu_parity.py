@@ -55,6 +55,10 @@ CASES = [
     ("2d_Blast1_split", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "split"),
     ("2d_rect_cheb40", (128, 128), (16, 16), 4, dict(prewin="cheb", prewin_param=40.0, p_fa=1e-4), 2, "fused"),
     ("3d_B_eq_N_last", (16, 32, 32), (4, 8, 32), 3, dict(p_fa=1e-3), 1, "split"),
+    # tensor-core split fold (k_split_mma: N_last = 64, A_1 % 16 == 0, L <= 16, L % 4 == 0)
+    ("3d_mma_A16", (16, 128, 64), (4, 8, 8), 8, dict(p_fa=1e-3, random_tau=True), 2, "split"),
+    ("3d_mma_A32_L4", (8, 256, 64), (4, 8, 4), 4, dict(p_fa=1e-3), 1, "split"),
+    ("3d_mma_L16_mu", (8, 128, 64), (2, 8, 8), 16, dict(p_fa=1e-4, mu=12), 1, "split"),
 ]
 
 
@@ -211,6 +215,7 @@ def _slab_run(plan, x, slabs):
     ((64, 32, 32), (8, 4, 8), 6, [(0, 16), (16, 40), (40, 64)]),
     ((128, 64), (16, 16), 4, [(0, 64), (64, 128)]),
     ((32, 16, 64), (4, 4, 8), 12, [(0, 8), (8, 12), (12, 32)]),
+    ((16, 128, 64), (4, 8, 8), 8, [(0, 4), (4, 12), (12, 16)]),     # tensor-core fold
 ])
 def test_variant_b_slab_partials(n, b, L, slabs):
     """Slab partial folds (linear in x) summed + rsft_finalize == the whole-frame first stage:
