@@ -249,6 +249,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, uint64_t tmap, int c0, in
                :: "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, uint64_t tmap, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+               :: "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, uint64_t tmap, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
                " [%0], [%1, {%2, %3, %4}], [%5];"
@@ -1229,7 +1236,8 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
 //               K-major weight tiles (Wh | Wl); after a group barrier the group's first warp
 //               issues the pair's 8 MMAs into the GROUP's accumulator (one per group: the two
 //               groups' partial sums are added in a fixed order, so results are deterministic)
-//   warp 8      TMA producer (lane 0), 16-row boxes into a kMmaSX-deep ring
+//   warp 8      TMA producer (lane 0): one 5-D tensor-map box (32 rows = 2 stages, 16 KiB)
+//               per stage pair into a kMmaSX/2-deep ring
 //   warp 9      TMEM owner: accumulators (2 classes in flight x 2 groups x 32 columns) and
 //               the A stages (kMmaSP pairs x 2 stages x 32 columns)
 //   warps 10-13 epilogue: TMEM -> (Wh | Wl) halves and groups summed, column weights h_last,
@@ -1319,7 +1327,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int D = pd.D;                                  // == 3
   const int nlast = pd.nlast, blast = pd.blast, bouter = pd.bouter;
-  const int B0 = pd.b[0], B1 = pd.b[1], A0 = pd.a[0], A1 = pd.a[1], lgb1 = pd.lgb[1];
+  const int B1 = pd.b[1], A0 = pd.a[0], A1 = pd.a[1], lgb1 = pd.lgb[1];
   const int nst = a0_count * (A1 >> 4);               // 16-row stages per class (one a0, 16 a1 each)
   const int npairs = nst >> 1;                         // even, >= 2 (launcher)
   const MmaLayout ly = mma_layout(a0_count, A1, nlast, blast);
@@ -1345,7 +1353,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
   // zero both class-table buffers (padded loops stay zero; cp.async writes l < nl)
   for (int i = t; i < 2 * ly.tab_stride / 4; i += blockDim.x) reinterpret_cast<float*>(smem + ly.tab)[i] = 0.f;
   if (t == 0) {
-    for (int i = 0; i < kMmaSX; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4); }   // 4 warps of a group
+    for (int i = 0; i < kMmaSX / 2; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4); }   // 4 warps of a group
     for (int i = 0; i < kMmaSP; ++i) mbar_init(&opempty[i], 1);                              // MMA commit
     for (int i = 0; i < 2; ++i) { mbar_init(&accfull[i], 2); mbar_init(&accempty[i], 4); }  // 2 groups / 4 epi warps
     fence_mbar_init();
@@ -1420,7 +1428,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
       const int pl0 = (int)((grp + ci * npairs) & 1);
       for (int pl = pl0; pl < npairs; pl += 2) {
         const uint32_t P = (uint32_t)(ci * npairs + pl);
-        const int x = 2 * (int)(P % (kMmaSX / 2)), op = (int)(P % kMmaSP);
+        const int px = (int)(P % (kMmaSX / 2)), x = 2 * px, op = (int)(P % kMmaSP);
         const uint32_t xph = (P / (kMmaSX / 2)) & 1, oph = (P / kMmaSP) & 1;
         float* wsl = reinterpret_cast<float*>(smem + ly.op + op * 2 * kMmaWStage);
         const uint32_t acol = taddr + 128 + (uint32_t)(op * 2) * 32;
@@ -1441,26 +1449,32 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
           *reinterpret_cast<float4*>(wsl + h * (kMmaWStage / 4) + (((kq * 4 + (n >> 3)) * 8 + (n & 7)) << 2)) =
               make_float4(wv[0], wv[1], wv[2], wv[3]);
         }
+        // A = X^T: column m of both stages -> TMEM lane m (Xh: the tensor core truncates; Xl exact)
+        mbar_wait(&xfull[px], xph);
+        float xv[2][16];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {                  // A = X^T: column m of the stage -> TMEM lane m
-          mbar_wait(&xfull[x + h], xph);
+        for (int h = 0; h < 2; ++h) {
           const float* xs = reinterpret_cast<const float*>(smem + ly.x + (x + h) * 8192) + m;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) xv[h][r] = xs[r * 128];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[px]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
           uint32_t v[32];
 #pragma unroll
           for (int r = 0; r < 16; ++r) {
-            const float xv = xs[r * 128];
-            v[r] = __float_as_uint(xv);                                  // Xh: the tensor core truncates
-            v[16 + r] = __float_as_uint(xv - tf32_trunc(xv));            // Xl, exact
+            v[r] = __float_as_uint(xv[h][r]);
+            v[16 + r] = __float_as_uint(xv[h][r] - tf32_trunc(xv[h][r]));
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&xempty[x + h]);
           tmem_st32(acol + h * 32 + lane_off, v);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");    // W tiles -> tensor core
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         named_bar(2 + grp, 128);                       // the group's operands are complete
-        if (kq == 0) {
+        if (kq == grp) {                               // issuing warp: SMSP 0 (group 0) / 1 (group 1)
           if (pl == pl0) mbar_wait(&accempty[buf], (((uint32_t)(ci >> 1)) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #if RSFT_MMA_DEBUG != 3
@@ -1482,25 +1496,26 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
     }
   } else if (warp == kMmaProd) {
     // ---------------- TMA producer ----------------
+    // map dims {N_last, r1, a1, r0, frame * a0_count + a0}; a pair = 2 a0 x 16 a1 (A_1 == 16)
+    // or 1 a0 x 32 a1 (A_1 >= 32)
     if (lane == 0) {
-      int x = 0;
+      int px = 0;
       uint32_t ph = 0;
       const uint64_t tm = reinterpret_cast<uint64_t>(&tmap);
-      const int plane_stride = a0_count * B0;
+      const int lgJ = A1 == 16 ? 0 : __ffs(A1 >> 4) - 1;
       for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int frame = (int)(u / bouter), kappa = (int)(u % bouter);
         const int r0 = kappa >> lgb1, r1 = kappa & (B1 - 1);
-        int a0l = 0, a1b = 0;
-        for (int gl = 0; gl < nst; ++gl) {
-          mbar_wait(&xempty[x], ph ^ 1);
+        for (int pl = 0; pl < npairs; ++pl) {
+          const int gl = 2 * pl, a0l = gl >> lgJ, a1b = (gl & ((1 << lgJ) - 1)) << 4;
+          mbar_wait(&xempty[px], ph ^ 1);
 #if RSFT_MMA_DEBUG == 2                               // compute ceiling: no HBM traffic
-          mbar_arrive(&xfull[x]);
+          mbar_arrive(&xfull[px]);
 #else
-          mbar_expect_tx(&xfull[x], 8192u);
-          tma_load_4d(smem + ly.x + x * 8192, tm, 0, r1, a1b, frame * plane_stride + a0l * B0 + r0, &xfull[x]);
+          mbar_expect_tx(&xfull[px], 16384u);
+          tma_load_5d(smem + ly.x + px * 16384, tm, 0, r1, a1b, r0, frame * a0_count + a0l, &xfull[px]);
 #endif
-          if (++x == kMmaSX) { x = 0; ph ^= 1; }
-          if ((a1b += 16) == A1) { a1b = 0; ++a0l; }
+          if (++px == kMmaSX / 2) { px = 0; ph ^= 1; }
         }
       }
     }
@@ -2047,8 +2062,14 @@ static bool mma_fold_ok(const rsft_plan_s* p, int64_t batch, int l0, int nl, int
 static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, int64_t a0_base,
                                     int64_t a0_count, uint32_t* zero_bm, int64_t zero_words, cudaStream_t st) {
   const size_t smem = (size_t)mma_layout((int)a0_count, (int)p->a[1], 64, (int)p->b[2]).total;
+  // x [batch][a0_count B0][N1][64] as {64, r1 (B1), a1 (A1), r0 (B0), frame a0_count + a0}
+  const uint64_t e = 8, row = 64 * e;
+  const int64_t N1 = p->n[1], B1 = p->b[1], A1 = p->a[1], B0 = p->b[0];
+  cuuint64_t dims[5] = {64, (cuuint64_t)B1, (cuuint64_t)A1, (cuuint64_t)B0, (cuuint64_t)(batch * a0_count)};
+  cuuint64_t str[4] = {row, (cuuint64_t)(B1 * row), (cuuint64_t)(N1 * row), (cuuint64_t)(B0 * N1 * row)};
+  cuuint32_t box[5] = {64, 1, (cuuint32_t)(A1 == 16 ? 16 : 32), 1, (cuuint32_t)(A1 == 16 ? 2 : 1)};
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, a0_count * p->b[0], &tmap, kUSplit);
+  rsft_status s = make_map(&tmap, d_x, 5, dims, str, box);
   if (s) return s;
   s = check(cudaFuncSetAttribute(k_split_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
