@@ -1251,7 +1251,12 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
 #ifndef RSFT_MMA_SP
 #define RSFT_MMA_SP 4
 #endif
+#ifndef RSFT_MMA_QB
+#define RSFT_MMA_QB 2
+#endif
 constexpr int kMmaSX = RSFT_MMA_SX, kMmaSP = RSFT_MMA_SP, kMmaThreads = 448, kMmaLP = 16, kMmaEStride = 144;
+constexpr int kMmaQB = RSFT_MMA_QB;                  // stages per TMA box (2: one pair, 4: two pairs)
+constexpr int kMmaNB = kMmaSX / kMmaQB;              // box slots in the X ring
 constexpr int kMmaWorkers = 8, kMmaProd = 8, kMmaTmem = 9, kMmaEpi0 = 10;   // warp roles
 constexpr int kMmaWStage = 2048;                                           // (Wh | Wl) per stage
 static_assert(128 + kMmaSP * 2 * 32 <= 512, "TMEM columns");
@@ -1353,7 +1358,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
   // zero both class-table buffers (padded loops stay zero; cp.async writes l < nl)
   for (int i = t; i < 2 * ly.tab_stride / 4; i += blockDim.x) reinterpret_cast<float*>(smem + ly.tab)[i] = 0.f;
   if (t == 0) {
-    for (int i = 0; i < kMmaSX / 2; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4); }   // 4 warps of a group
+    for (int i = 0; i < kMmaNB; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4 * (kMmaQB / 2)); }  // consuming warps
     for (int i = 0; i < kMmaSP; ++i) mbar_init(&opempty[i], 1);                              // MMA commit
     for (int i = 0; i < 2; ++i) { mbar_init(&accfull[i], 2); mbar_init(&accempty[i], 4); }  // 2 groups / 4 epi warps
     fence_mbar_init();
@@ -1428,8 +1433,9 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
       const int pl0 = (int)((grp + ci * npairs) & 1);
       for (int pl = pl0; pl < npairs; pl += 2) {
         const uint32_t P = (uint32_t)(ci * npairs + pl);
-        const int px = (int)(P % (kMmaSX / 2)), x = 2 * px, op = (int)(P % kMmaSP);
-        const uint32_t xph = (P / (kMmaSX / 2)) & 1, oph = (P / kMmaSP) & 1;
+        const uint32_t bx = P / (kMmaQB / 2);         // TMA box of this pair
+        const int px = (int)(bx % kMmaNB), x = px * kMmaQB + 2 * (int)(P % (kMmaQB / 2)), op = (int)(P % kMmaSP);
+        const uint32_t xph = (bx / kMmaNB) & 1, oph = (P / kMmaSP) & 1;
         float* wsl = reinterpret_cast<float*>(smem + ly.op + op * 2 * kMmaWStage);
         const uint32_t acol = taddr + 128 + (uint32_t)(op * 2) * 32;
         mbar_wait(&opempty[op], oph ^ 1);
@@ -1496,26 +1502,27 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
     }
   } else if (warp == kMmaProd) {
     // ---------------- TMA producer ----------------
-    // map dims {N_last, r1, a1, r0, frame * a0_count + a0}; a pair = 2 a0 x 16 a1 (A_1 == 16)
-    // or 1 a0 x 32 a1 (A_1 >= 32)
+    // map dims {N_last, r1, a1, r0, frame * a0_count + a0}; a box = kMmaQB stages = 16 kMmaQB
+    // rows: (16 kMmaQB / A_1) a0 x A_1 a1, or 1 a0 x 16 kMmaQB a1 when A_1 is larger
     if (lane == 0) {
       int px = 0;
       uint32_t ph = 0;
       const uint64_t tm = reinterpret_cast<uint64_t>(&tmap);
-      const int lgJ = A1 == 16 ? 0 : __ffs(A1 >> 4) - 1;
+      const int lgJ = __ffs(A1 >> 4) - 1;
+      const int nbox = nst / kMmaQB;
       for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int frame = (int)(u / bouter), kappa = (int)(u % bouter);
         const int r0 = kappa >> lgb1, r1 = kappa & (B1 - 1);
-        for (int pl = 0; pl < npairs; ++pl) {
-          const int gl = 2 * pl, a0l = gl >> lgJ, a1b = (gl & ((1 << lgJ) - 1)) << 4;
+        for (int bi = 0; bi < nbox; ++bi) {
+          const int gl = kMmaQB * bi, a0l = gl >> lgJ, a1b = (gl & ((1 << lgJ) - 1)) << 4;
           mbar_wait(&xempty[px], ph ^ 1);
 #if RSFT_MMA_DEBUG == 2                               // compute ceiling: no HBM traffic
           mbar_arrive(&xfull[px]);
 #else
-          mbar_expect_tx(&xfull[px], 16384u);
-          tma_load_5d(smem + ly.x + px * 16384, tm, 0, r1, a1b, r0, frame * a0_count + a0l, &xfull[px]);
+          mbar_expect_tx(&xfull[px], 8192u * kMmaQB);
+          tma_load_5d(smem + ly.x + px * 8192 * kMmaQB, tm, 0, r1, a1b, r0, frame * a0_count + a0l, &xfull[px]);
 #endif
-          if (++px == kMmaSX / 2) { px = 0; ph ^= 1; }
+          if (++px == kMmaNB) { px = 0; ph ^= 1; }
         }
       }
     }
@@ -2052,7 +2059,7 @@ static bool mma_fold_ok(const rsft_plan_s* p, int64_t batch, int l0, int nl, int
   static const bool off = getenv("RSFT_NO_MMA") != nullptr;
   if (off || p->D != 3 || p->n[2] != 64 || p->a[1] % 16 != 0 || nl > kMmaLP || (nl | l0 | p->L) % 4 != 0) return false;
   const int64_t nst = a0_count * (p->a[1] / 16);                   // 16-row stages per class
-  if (nst % 2 != 0 || nst < 4) return false;                        // stage pairs, both worker groups busy
+  if (nst % kMmaQB != 0 || nst < 4) return false;                  // whole boxes of stage pairs, both groups busy
   const int64_t blast = p->b[2];
   if ((int64_t)kMmaLP * blast * blast * 16 > kSplitDftBytes) return false;
   if (batch * nl * p->btot > p->dev.fbuf_capacity) return false;
@@ -2067,7 +2074,8 @@ static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t bat
   const int64_t N1 = p->n[1], B1 = p->b[1], A1 = p->a[1], B0 = p->b[0];
   cuuint64_t dims[5] = {64, (cuuint64_t)B1, (cuuint64_t)A1, (cuuint64_t)B0, (cuuint64_t)(batch * a0_count)};
   cuuint64_t str[4] = {row, (cuuint64_t)(B1 * row), (cuuint64_t)(N1 * row), (cuuint64_t)(B0 * N1 * row)};
-  cuuint32_t box[5] = {64, 1, (cuuint32_t)(A1 == 16 ? 16 : 32), 1, (cuuint32_t)(A1 == 16 ? 2 : 1)};
+  const int64_t rows = 16 * kMmaQB, ba1 = A1 < rows ? A1 : rows;
+  cuuint32_t box[5] = {64, 1, (cuuint32_t)ba1, 1, (cuuint32_t)(rows / ba1)};
   CUtensorMap tmap;
   rsft_status s = make_map(&tmap, d_x, 5, dims, str, box);
   if (s) return s;
