@@ -420,7 +420,8 @@ def bench_c5(a, wl, rank, world, dev):
                                    f"loops sharded {world} ways + NCCL all-gather of bitmaps")},
         "roofline": {"bound": "hbm", "achieved": algo / (k1 / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": algo / (k1 / 1000.0) / 1e9 / peak, "traffic": load_traffic(wl.name),
-                     "kernel": "k_split_fold + k_split_fft (first stage of this rank)",
+                     "kernel": ("k_split_fold" if os.environ.get("RSFT_NO_MMA") else "k_split_mma (3xTF32 tcgen05)")
+                               + " + k_split_fft (first stage of this rank)",
                      "algorithmic_bytes_per_launch": algo, "avg_launch_ms": k1,
                      "share_of_step": k1 / step_ms, "peak_source": peak_src},
         "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None, "e2e": None,

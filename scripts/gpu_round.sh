@@ -1,6 +1,6 @@
 #!/bin/bash
 # Full GPU session: smoke, full parity, bench (+e2e, cpu baseline), c5 benches, reference arm,
-# launch lists (c4, c5), ncu --set full of the dominant kernels (k_fused at c4, k_split_fold at c5).
+# launch lists (c4, c5), ncu --set full of the dominant kernels (k_fused at c4, k_split_mma at c5).
 set -u
 mkdir -p gpurun_out
 OUT=gpurun_out
@@ -20,5 +20,6 @@ done
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 -o $OUT/prof_k_fused -f $CMD > $OUT/ncu_full_c4.log 2>&1
 CMD5="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --workload c5_cube"
-ncu --set full --clock-control none --import-source on -k regex:k_split_fold -s 1 -c 1 -o $OUT/prof_k_split_fold -f $CMD5 > $OUT/ncu_full_c5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_split_mma -s 1 -c 1 -o $OUT/prof_k_split_mma -f $CMD5 > $OUT/ncu_full_c5.log 2>&1
+RSFT_NO_MMA=1 ncu --set full --clock-control none --import-source on -k regex:k_split_fold -s 1 -c 1 -o $OUT/prof_k_split_fold -f $CMD5 > $OUT/ncu_full_c5_ffma.log 2>&1
 echo done
