@@ -2056,8 +2056,8 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
 // into residue sums R [batch][nl][B_outer][B_last]; zeroes zero_words bitmap words.
 // Tensor-core split fold (k_split_mma): c5-like shapes, one class per CTA iteration (no chunks).
 static bool mma_fold_ok(const rsft_plan_s* p, int64_t batch, int l0, int nl, int64_t a0_count) {
-  static const bool off = getenv("RSFT_NO_MMA") != nullptr;
-  if (off || p->D != 3 || p->n[2] != 64 || p->a[1] % 16 != 0 || nl > kMmaLP || (nl | l0 | p->L) % 4 != 0) return false;
+  const char* off = getenv("RSFT_NO_MMA");          // read per launch: tests select either kernel
+  if ((off && off[0] && off[0] != '0') || p->D != 3 || p->n[2] != 64 || p->a[1] % 16 != 0 || nl > kMmaLP || (nl | l0 | p->L) % 4 != 0) return false;
   const int64_t nst = a0_count * (p->a[1] / 16);                   // 16-row stages per class
   if (nst % kMmaQB != 0 || nst < 4) return false;                  // whole boxes of stage pairs, both groups busy
   const int64_t blast = p->b[2];

@@ -73,6 +73,22 @@ def test_parity_ci_sizes(case):
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
+MMA_CASES = [c for c in CASES if c[0].startswith("3d_mma")]
+
+
+@pytest.mark.parametrize("case", MMA_CASES, ids=[c[0] for c in MMA_CASES])
+def test_parity_ffma_fold_on_mma_shapes(case, monkeypatch):
+    """The shapes the tensor-core fold (k_split_mma) takes, forced through the FFMA2 split
+    fold (RSFT_NO_MMA=1, read per launch): both kernels stay parity-green."""
+    monkeypatch.setenv("RSFT_NO_MMA", "1")
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
 def test_parity_persistent_many_frames():
     """More frames than resident CTAs: each persistent CTA loops over several frames."""
     op = oracle_params((64, 64), (8, 8), 3, p_fa=1e-3, seed=5)
