@@ -132,6 +132,9 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.region_state = reinterpret_cast<unsigned long long*>(base + p->ws.region_off);
   pd.region_capacity = p->ws.region_capacity;
   pd.region_slots = p->ws.slots_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.slots_off) : nullptr;
+  pd.etab = p->ws.etab_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.etab_off) : nullptr;
+  pd.etab_frames = p->ws.etab_bytes
+                       ? (int64_t)(p->ws.etab_bytes / ((size_t)p->L * p->b[0] * p->b[1] * (p->n[2] / 32) * 4)) : 0;
   for (int d = 0; d < 3; ++d) pd.bwin[d] = d < p->D ? reinterpret_cast<const float*>(base + p->ws.bwin_off[d]) : nullptr;
   pd.bone = reinterpret_cast<const float*>(base + p->ws.bone_off);
   pd.btw = reinterpret_cast<const float2*>(base + p->ws.btw_off);

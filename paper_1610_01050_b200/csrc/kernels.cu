@@ -394,7 +394,7 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
                            const uint32_t* Xs, const uint32_t* NT, const int* kpre_s, const int* sig_ld,
                            int64_t frame, int64_t i0,
                            int64_t d0b, int64_t d0e, uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
-                           int* wsum = nullptr, uint32_t* __restrict__ slot = nullptr) {
+                           bool ebuilt, int* wsum = nullptr, uint32_t* __restrict__ slot = nullptr) {
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
   const int ld = D - 1;
   const int nld = pd.n[ld], lga_ld = pd.lga[ld];
@@ -416,7 +416,9 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
   (void)wpl;
     // E[l][krd][w] (all loops at once).  With nibble tables NT[l][g][n][w] = OR of the X masks
     // of the set bits of n in bucket group g (4 buckets), one entry costs B_last/4 lookups.
-    if (pd.xmask) {
+    // (ebuilt: the caller copied E from the precomputed table, k_etab.)
+    if (ebuilt) {
+    } else if (pd.xmask) {
       const int lg_rw = (brd > 1 ? __ffs(brd) - 1 : 0) + lgW;
       for (int j = tid; j < L * brd * W; j += blockDim.x) {
         const int l = j >> lg_rw, rem = j & ((1 << lg_rw) - 1);
@@ -1665,11 +1667,47 @@ __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bo
 // count (rcount[region]) for the offset scan of rsft_detect_compact.
 // smem: bm [L][lw] | E [L][B_rd][W] | sig_rd [32] | X [L][B_last][W]
 // ------------------------------------------------------------------------------------
+// D == 3 vote, E words for every dim-0 bucket (computed once per frame instead of once per
+// region: N_0 regions share B_0 distinct k_pre): etab[frame][l][k0][k1][w] = OR over the set
+// last-dim buckets k2 of bucket row (k0, k1) of loop l's bitmap of the plan-constant X masks
+// X[l][k2][w] (bit j of X = location 32 w + j of the last dim hashes to k2; Def. 3 / I1).
+__global__ void __launch_bounds__(kThreads) k_etab(PlanDev pd, const uint32_t* __restrict__ bitmaps, int64_t batch) {
+  const int L = pd.L, B0 = pd.b[0], B1 = pd.b[1], W = pd.n[2] >> 5, blast = pd.blast, wpl = pd.wpl;
+  const int64_t rows = (int64_t)L * B0 * B1;       // bucket rows (l, k0, k1) per frame
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < batch * rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t frame = i / rows;
+    const int r = (int)(i - frame * rows);
+    const int l = r / (B0 * B1), k01 = r - l * B0 * B1;   // k01 = k0 B1 + k1
+    const int flat = k01 * blast;
+    const uint32_t* b = bitmaps + ((size_t)frame * L + l) * wpl;
+    const uint32_t* X = pd.xmask + (size_t)l * blast * W;
+    uint32_t* dst = pd.etab + (size_t)i * W;
+    uint32_t lo, hi = 0;
+    if (blast <= 32) lo = (__ldg(b + (flat >> 5)) >> (flat & 31)) & (blast == 32 ? 0xffffffffu : ((1u << blast) - 1u));
+    else { lo = __ldg(b + (flat >> 5)); hi = __ldg(b + (flat >> 5) + 1); }
+    for (int w0 = 0; w0 < W; w0 += 4) {            // W is a power of two (1, 2, 4, ...)
+      const int nw = W - w0 < 4 ? W - w0 : 4;
+      uint32_t e[4] = {0u, 0u, 0u, 0u};
+      uint32_t pl = lo, ph = hi;
+      while (pl) {
+        const int k = __ffs(pl) - 1; pl &= pl - 1;
+        for (int q = 0; q < nw; ++q) e[q] |= __ldg(X + (size_t)k * W + w0 + q);
+      }
+      while (ph) {
+        const int k = __ffs(ph) + 31; ph &= ph - 1;
+        for (int q = 0; q < nw; ++q) e[q] |= __ldg(X + (size_t)k * W + w0 + q);
+      }
+      for (int q = 0; q < nw; ++q) dst[w0 + q] = e[q];
+    }
+  }
+}
+
 template <int CW, int MODE, bool COUNT, bool LIST>
 __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
                                                    int64_t d0b, int64_t d0e, int lw, int64_t np, int64_t nregions,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
-                                                   unsigned long long* __restrict__ rcount) {
+                                                   unsigned long long* __restrict__ rcount, int use_etab) {
   extern __shared__ __align__(16) uint32_t vsm[];
   __shared__ int wsum[kListIpt * kThreads / 32];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
@@ -1721,9 +1759,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
       for (int l = tid; l < L; l += blockDim.x)
         kpre_s[l] = (int)(((int64_t)pd.loops[l].sig[0] * i0) & (pd.n[0] - 1)) >> pd.lga[0];
 
+    if (use_etab) {                                  // D == 3: E rows of this region's dim-0 buckets
+      __syncthreads();
+      const int rw = brd * W, lg_rw = __ffs(rw) - 1;
+      const uint32_t* et = pd.etab + (size_t)frame * L * pd.b[0] * rw;
+      if ((rw & 3) == 0) {                           // 16-B copies, one L2 round trip per thread
+        const int rw4 = rw >> 2, lg4 = lg_rw - 2;
+        for (int j = tid; j < L * rw4; j += blockDim.x) {
+          const int l = j >> lg4, rem = j & (rw4 - 1);
+          reinterpret_cast<uint4*>(E)[j] =
+              __ldg(reinterpret_cast<const uint4*>(et + ((size_t)l * pd.b[0] + kpre_s[l]) * rw) + rem);
+        }
+      } else {
+        for (int j = tid; j < L * rw; j += blockDim.x) {
+          const int l = j >> lg_rw, rem = j & (rw - 1);
+          E[j] = __ldg(et + ((size_t)l * pd.b[0] + kpre_s[l]) * rw + rem);
+        }
+      }
+    }
     // this region's slice of every loop's first-stage bitmap
     const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
-    for (int i = tid; i < L * lw; i += blockDim.x) {
+    for (int i = use_etab ? L * lw : tid; i < L * lw; i += blockDim.x) {
       const int l = i / lw, w = i - l * lw;
       int start = 0;
       if (D == 3 && lw < wpl) {
@@ -1735,12 +1791,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
     __syncthreads();
     if (LIST) {                                      // region-local index list + count
       const int t = vote_region<CW, MODE, true>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, sig_ld, frame, i0, d0b, d0e,
-                                                detect, counts, wsum, pd.region_slots + (size_t)region * kListCap);
+                                                detect, counts, use_etab, wsum,
+                                                pd.region_slots + (size_t)region * kListCap);
       if (tid == 0) rcount[region] = (unsigned long long)t;
       continue;
     }
     int cnt = vote_region<CW, MODE>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, sig_ld, frame, i0, d0b, d0e, detect,
-                                    counts);
+                                    counts, use_etab);
     if (COUNT) {                                     // this region's detection count
 #pragma unroll
       for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
@@ -2276,8 +2333,17 @@ static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   if (nb < 1) { set_error("k_vote: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > nregions) grid = nregions;
+  // D == 3: E words of every dim-0 bucket once per frame (k_etab), copied per region
+  const int use_etab = p->D == 3 && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
+                       (d0e - d0b) > p->b[0];
+  if (use_etab) {
+    const int64_t ne = batch * p->L * p->b[0] * p->b[1];
+    const int64_t eg = (ne + kThreads - 1) / kThreads;
+    k_etab<<<(unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st>>>(p->dev, bm, batch);
+    p->last_launches += 1;
+  }
   kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, np, nregions, det, counts,
-                                               p->dev.region_state);
+                                               p->dev.region_state, use_etab);
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_vote launch");
 }

@@ -201,6 +201,15 @@ void layout_workspace(rsft_plan_s* p) {
   w.slots_off = off;                               // vote index lists (kListCap per region)
   w.slots_bytes = (size_t)w.region_capacity * kListCap * 4;
   off = align256(off + w.slots_bytes);
+  w.etab_off = off;                                // D == 3 vote: E words for every dim-0 bucket
+  w.etab_bytes = 0;
+  if (p->D == 3 && w.xmask_bytes) {
+    const size_t per = (size_t)p->L * p->b[0] * p->b[1] * (p->n[2] / 32) * 4;
+    size_t fr = (size_t)p->P.max_batch;
+    while (fr > 1 && fr * per > kMaxEtabBytes) fr >>= 1;
+    if (fr * per <= kMaxEtabBytes) w.etab_bytes = fr * per;
+    off = align256(off + w.etab_bytes);
+  }
   for (int d = 0; d < 3; ++d) {                    // Bartlett baseline tables
     w.bwin_off[d] = off;
     if (d < p->D) off = align256(off + 4 * (size_t)p->n[d]);

@@ -117,6 +117,8 @@ struct PlanDev {
   unsigned long long* region_state; // per-region detection counts -> offsets (rsft_detect_compact)
   int64_t region_capacity;
   uint32_t* region_slots;          // per-region local index lists [region_capacity][kListCap] (or null)
+  uint32_t* etab;                  // D == 3 vote: E words for every dim-0 bucket [batch][L][B0][B1][W] (or null)
+  int64_t etab_frames;             // frames etab holds
   const float* bwin[kMaxDim];      // Bartlett: fp32 pre-windows w_d [N_d]
   const float* bone;               // 1.0f (window of an absent dimension)
   const float2* btw;               // e^{-j 2 pi k / 4096}, k < 2048 (Bartlett FFTs)
@@ -124,9 +126,10 @@ struct PlanDev {
 
 constexpr size_t kMaxXmaskBytes = 48 * 1024;   // vote expansion masks kept in smem
 constexpr size_t kMaxNibbleBytes = 64 * 1024;  // vote nibble tables (4x the masks) kept in smem
+constexpr size_t kMaxEtabBytes = 64ull << 20;  // D == 3 vote: precomputed E table for all dim-0 buckets, up to this
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, bwin_off[kMaxDim], bone_off, btw_off, total;
+  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, etab_off, etab_bytes, bwin_off[kMaxDim], bone_off, btw_off, total;
   int64_t region_capacity;
   int64_t chunk_capacity;
 };
