@@ -224,6 +224,14 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
 // their 16 B with LDS.128 and run the FFMA2 fold.  Bytes in flight per warp are explicit
 // ((kStages-1) x U x 512 B), independent of registers and of ptxas scheduling.
 // ------------------------------------------------------------------------------------
+// Programmatic dependent launch: every hot-path kernel is launched with programmatic stream
+// serialization and starts with griddepcontrol.wait (before any global access: the previous
+// kernel's writes are visible after it) + launch_dependents, so the next kernel's CTAs are
+// scheduled while this one drains instead of after a full launch round trip.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -653,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_
                                                     uint32_t* __restrict__ bitmaps,
                                                     float2* __restrict__ spectra, int64_t bm_stride,
                                                     int64_t sp_stride) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int S = kStages;
   const int D = pd.D;
@@ -906,6 +915,7 @@ __global__ void __launch_bounds__(kThreadsSplit, LP >= 24 ? 1 : kCtasSplit)
 k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch,
              int a0_base, int a0_count, int lg_chunk, float2* __restrict__ R, uint32_t* __restrict__ zero_bm,
              int64_t zero_words) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int S = kStagesSplit;
   constexpr int BR = U * RPW;                        // run rows per TMA box
@@ -1329,6 +1339,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 __global__ void __launch_bounds__(kMmaThreads, 1)
 k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch, int a0_base,
             int a0_count, float2* __restrict__ R, uint32_t* __restrict__ zero_bm, int64_t zero_words) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int LP = kMmaLP;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -1598,6 +1609,7 @@ __global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const flo
                                                            int rnl, int nchunk, int l0, int nl,
                                                            uint32_t* __restrict__ bitmaps,
                                                            float2* __restrict__ spectra) {
+  pdl_enter();
   extern __shared__ float4 smem_f4[];
   float2* tw = reinterpret_cast<float2*>(smem_f4);
   float2* V = tw + 128;
@@ -1644,6 +1656,7 @@ __global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const flo
 // Variant B helper: sum the dim-0 chunks of the folded spectra F [L][B_last][nchunk][B_outer]
 // into the canonical partial [L][B_last][B_outer] (in chunk order).
 __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bouter, int64_t n, float2* __restrict__ out) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / bouter, o = i - row * bouter;
     const float2* s = F + row * nchunk * bouter + o;
@@ -1672,6 +1685,7 @@ __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bo
 // last-dim buckets k2 of bucket row (k0, k1) of loop l's bitmap of the plan-constant X masks
 // X[l][k2][w] (bit j of X = location 32 w + j of the last dim hashes to k2; Def. 3 / I1).
 __global__ void __launch_bounds__(kThreads) k_etab(PlanDev pd, const uint32_t* __restrict__ bitmaps, int64_t batch) {
+  pdl_enter();
   const int L = pd.L, B0 = pd.b[0], B1 = pd.b[1], W = pd.n[2] >> 5, blast = pd.blast, wpl = pd.wpl;
   const int64_t rows = (int64_t)L * B0 * B1;       // bucket rows (l, k0, k1) per frame
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < batch * rows;
@@ -1708,6 +1722,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
                                                    int64_t d0b, int64_t d0e, int lw, int64_t np, int64_t nregions,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
                                                    unsigned long long* __restrict__ rcount, int use_etab) {
+  pdl_enter();
   extern __shared__ __align__(16) uint32_t vsm[];
   __shared__ int wsum[kListIpt * kThreads / 32];
   const int D = pd.D, L = pd.L, wpl = pd.wpl;
@@ -1815,6 +1830,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
 // Exclusive scan of the per-region detection counts (one CTA); total -> *d_count.
 __global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __restrict__ counts, int64_t n,
                                                       long long* __restrict__ d_count) {
+  pdl_enter();
   __shared__ long long part[1024];
   const int t = threadIdx.x;
   const int64_t per = (n + 1023) / 1024;
@@ -1848,6 +1864,7 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
                                                            const long long* __restrict__ d_count, int64_t nregions,
                                                            const uint32_t* __restrict__ slots,
                                                            long long* __restrict__ idx, int64_t capacity) {
+  pdl_enter();
   __shared__ int wsum[kThreads / 32];
   __shared__ long long s_idx[kStageIdx];
   const int tid = threadIdx.x;
@@ -1921,6 +1938,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict
                                                       int64_t nchunks, unsigned long long* state,
                                                       unsigned int* ticket, long long* __restrict__ idx,
                                                       int64_t capacity, long long* __restrict__ d_count) {
+  pdl_enter();
   __shared__ int s_chunk;
   __shared__ long long s_prefix;
   __shared__ int wsum[kThreads / 32];
@@ -2046,6 +2064,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Tensor map over complex64 x (8-byte elements, no swizzle, OOB -> zeros).
+template <typename... KArgs, typename... Args>
+static cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 static rsft_status make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
                             const cuuint64_t* strides, const cuuint32_t* box) {
   auto fn = encode_fn();
@@ -2103,8 +2137,9 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
   if (nb < 1) { set_error("k_fused: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > batch) grid = batch;
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra),
-                                               bm_stride, sp_stride);
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreads, smem, st, p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra),
+                                               bm_stride, sp_stride); le_ != cudaSuccess)
+    return check(le_, "kern launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_fused launch");
 }
@@ -2140,8 +2175,9 @@ static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t bat
   if (s) return s;
   const int64_t units = batch * p->dev.bouter;
   const int64_t grid = units < p->num_sms ? units : p->num_sms;
-  k_split_mma<<<(unsigned)grid, kMmaThreads, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count,
-                                                         p->dev.fbuf, zero_bm, zero_words);
+  if (cudaError_t le_ = pdl_launch(k_split_mma, (unsigned)grid, kMmaThreads, smem, st, p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count,
+                                                         p->dev.fbuf, zero_bm, zero_words); le_ != cudaSuccess)
+    return check(le_, "k_split_mma launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_mma launch");
 }
@@ -2179,8 +2215,9 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
   int64_t grid = (int64_t)nb * p->num_sms;
   const int64_t need = (wunits + kThreadsSplit / 32 - 1) / (kThreadsSplit / 32);
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kThreadsSplit, smem, st>>>(p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg,
-                                                    p->dev.fbuf, zero_bm, zero_words);
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreadsSplit, smem, st, p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg,
+                                                    p->dev.fbuf, zero_bm, zero_words); le_ != cudaSuccess)
+    return check(le_, "kern launch");
   p->last_launches += 1;
   *lg_out = lg;
   return check(cudaGetLastError(), "k_split_fold launch");
@@ -2197,8 +2234,9 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
                         "smem attr");
   if (s) return s;
   dim3 grid2((unsigned)(nl * blast), (unsigned)batch);
-  k_split_fft<<<grid2, kThreadsFft, smem2, st>>>(p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
-                                                 reinterpret_cast<float2*>(spectra));
+  if (cudaError_t le_ = pdl_launch(k_split_fft, grid2, kThreadsFft, smem2, st, p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
+                                                 reinterpret_cast<float2*>(spectra)); le_ != cudaSuccess)
+    return check(le_, "k_split_fft launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_fft launch");
 }
@@ -2234,8 +2272,8 @@ static rsft_status launch_partial_t(rsft_plan_s* p, const void* d_x, int64_t off
   if (s) return s;
   const int64_t bouter = p->dev.bouter;
   const int64_t n = (int64_t)p->L * p->btot;
-  k_chunk_sum<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * p->num_sms), 256, 0, st>>>(
-      p->dev.fbuf, 1 << lg, bouter, n, reinterpret_cast<float2*>(d_partial));
+  if (cudaError_t le_ = pdl_launch(k_chunk_sum, (unsigned)std::min<int64_t>((n + 255) / 256, 4 * p->num_sms), 256, 0, st, p->dev.fbuf, 1 << lg, bouter, n, reinterpret_cast<float2*>(d_partial)); le_ != cudaSuccess)
+    return check(le_, "k_chunk_sum launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_chunk_sum launch");
 }
@@ -2339,11 +2377,13 @@ static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   if (use_etab) {
     const int64_t ne = batch * p->L * p->b[0] * p->b[1];
     const int64_t eg = (ne + kThreads - 1) / kThreads;
-    k_etab<<<(unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st>>>(p->dev, bm, batch);
+    if (cudaError_t le_ = pdl_launch(k_etab, (unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st, p->dev, bm, batch); le_ != cudaSuccess)
+      return check(le_, "k_etab launch");
     p->last_launches += 1;
   }
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(p->dev, bm, d0b, d0e, lw, np, nregions, det, counts,
-                                               p->dev.region_state, use_etab);
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreads, smem, st, p->dev, bm, d0b, d0e, lw, np, nregions, det, counts,
+                                               p->dev.region_state, use_etab); le_ != cudaSuccess)
+    return check(le_, "kern launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_vote launch");
 }
@@ -2386,11 +2426,13 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
-  k_region_scan<<<1, 1024, 0, st>>>(p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count));
-  k_region_write<<<(unsigned)nregions, kThreads, 0, st>>>(det, rwords, p->dev.region_state,
+  if (cudaError_t le_ = pdl_launch(k_region_scan, 1, 1024, 0, st, p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
+    return check(le_, "k_region_scan launch");
+  if (cudaError_t le_ = pdl_launch(k_region_write, (unsigned)nregions, kThreads, 0, st, det, rwords, p->dev.region_state,
                                                           reinterpret_cast<long long*>(d_count), nregions,
                                                           list ? p->dev.region_slots : nullptr,
-                                                          reinterpret_cast<long long*>(idx), capacity);
+                                                          reinterpret_cast<long long*>(idx), capacity); le_ != cudaSuccess)
+    return check(le_, "k_region_write launch");
   p->last_launches += 2;
   return check(cudaGetLastError(), "region scan/write launch");
 }
@@ -2414,9 +2456,10 @@ rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, i
   unsigned int* ticket = reinterpret_cast<unsigned int*>(state + nchunks);
   rsft_status s = check(cudaMemsetAsync(state, 0, (size_t)(nchunks + 1) * 8, st), "compaction state reset");
   if (s) return s;
-  k_compact<<<(unsigned)nchunks, kThreads, 0, st>>>(det, nwords, nchunks, state, ticket,
+  if (cudaError_t le_ = pdl_launch(k_compact, (unsigned)nchunks, kThreads, 0, st, det, nwords, nchunks, state, ticket,
                                                    reinterpret_cast<long long*>(idx), capacity,
-                                                   reinterpret_cast<long long*>(d_count));
+                                                   reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
+    return check(le_, "k_compact launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_compact launch");
 }
