@@ -93,6 +93,10 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.bone_off, &tw[4096], 4, cudaMemcpyHostToDevice, st),
                         "upload one"))) return s;
   }
+  if (!p->ntab.empty() && p->ws.ntab_bytes == p->ntab.size() * 4)
+    if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.ntab_off, p->ntab.data(), p->ws.ntab_bytes,
+                                        cudaMemcpyHostToDevice, st), "ntab upload")))
+      return s;
   if (!p->xmask.empty() && p->ws.xmask_bytes == p->xmask.size() * 4)
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
                                         cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
@@ -129,6 +133,8 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.chunk_counts = reinterpret_cast<long long*>(base + p->ws.chunk_off);
   pd.chunk_capacity = p->ws.chunk_capacity;
   pd.xmask = p->ws.xmask_bytes ? reinterpret_cast<const uint32_t*>(base + p->ws.xmask_off) : nullptr;
+  pd.ntab = (p->ws.ntab_bytes && p->ntab.size() * 4 == p->ws.ntab_bytes)
+                ? reinterpret_cast<const uint32_t*>(base + p->ws.ntab_off) : nullptr;
   pd.region_state = reinterpret_cast<unsigned long long*>(base + p->ws.region_off);
   pd.region_capacity = p->ws.region_capacity;
   pd.region_slots = p->ws.slots_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.slots_off) : nullptr;

@@ -1753,7 +1753,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
       for (int i = tid; i < nx; i += blockDim.x) Xs[i] = __ldg(pd.xmask + i);
   }
 
-  if (NT) {                                          // nibble tables from the X masks (once)
+  if (NT && pd.ntab) {                               // plan-constant nibble tables (bind time)
+    const int n4 = (L * (blast >> 2) * 16 * W) >> 2;
+    for (int i = tid; i < n4; i += blockDim.x)
+      reinterpret_cast<uint4*>(NT)[i] = __ldg(reinterpret_cast<const uint4*>(pd.ntab) + i);
+  } else if (NT) {                                   // nibble tables from the X masks (once)
     __syncthreads();
     const int ng = blast >> 2;
     for (int i = tid; i < L * ng * 16 * W; i += blockDim.x) {

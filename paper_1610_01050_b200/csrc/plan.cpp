@@ -145,6 +145,22 @@ rsft_status rebuild_tables(rsft_plan_s* p) {
         }
       }
     }
+    // nibble tables NT[l][g][m][w] = OR of X[l][4 g + q][w] over the set bits q of m (the vote
+    // expands 4 buckets per lookup); plan-constant, copied into shared memory by k_vote
+    p->ntab.clear();
+    if (!p->xmask.empty() && b >= 4 && 16 * p->xmask.size() <= kMaxNibbleBytes) {
+      const int64_t ng = b / 4;
+      p->ntab.assign((size_t)L * ng * 16 * W, 0u);
+      for (int l = 0; l < L; ++l)
+        for (int64_t g = 0; g < ng; ++g)
+          for (int m = 0; m < 16; ++m)
+            for (int64_t w = 0; w < W; ++w) {
+              uint32_t e = 0;
+              for (int q = 0; q < 4; ++q)
+                if ((m >> q) & 1) e |= p->xmask[((size_t)l * b + 4 * g + q) * W + w];
+              p->ntab[(((size_t)l * ng + g) * 16 + m) * W + w] = e;
+            }
+    }
   }
   for (int l = 0; l < L; ++l)        // Eq. tpd with P~_fa = P_fa per loop (L8)
     p->gamma[l] = p->P.gamma_override > 0 ? p->P.gamma_override
@@ -196,6 +212,8 @@ void layout_workspace(rsft_plan_s* p) {
     if (w.xmask_bytes > kMaxXmaskBytes) w.xmask_bytes = 0;
   }
   w.xmask_off = off; off = align256(off + w.xmask_bytes);
+  w.ntab_bytes = (w.xmask_bytes && p->b[p->D - 1] >= 4 && 4 * w.xmask_bytes <= kMaxNibbleBytes) ? 4 * w.xmask_bytes : 0;
+  w.ntab_off = off; off = align256(off + w.ntab_bytes);
   w.region_capacity = p->P.max_batch * (p->D == 3 ? p->n[0] : 1) + 2;
   w.region_off = off; off = align256(off + 8 * (size_t)w.region_capacity);
   w.slots_off = off;                               // vote index lists (kListCap per region)

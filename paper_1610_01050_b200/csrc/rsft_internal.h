@@ -114,6 +114,7 @@ struct PlanDev {
   long long* chunk_counts;         // compaction scratch
   int64_t chunk_capacity;
   const uint32_t* xmask;           // [L][B_last][N_last/32] last-dim bucket masks, or null
+  const uint32_t* ntab;            // nibble tables of the masks [L][B_last/4][16][N_last/32], or null
   unsigned long long* region_state; // per-region detection counts -> offsets (rsft_detect_compact)
   int64_t region_capacity;
   uint32_t* region_slots;          // per-region local index lists [region_capacity][kListCap] (or null)
@@ -129,7 +130,7 @@ constexpr size_t kMaxNibbleBytes = 64 * 1024;  // vote nibble tables (4x the mas
 constexpr size_t kMaxEtabBytes = 64ull << 20;  // D == 3 vote: precomputed E table for all dim-0 buckets, up to this
 
 struct Workspace {
-  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, etab_off, etab_bytes, bwin_off[kMaxDim], bone_off, btw_off, total;
+  size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, etab_off, etab_bytes, ntab_off, ntab_bytes, bwin_off[kMaxDim], bone_off, btw_off, total;
   int64_t region_capacity;
   int64_t chunk_capacity;
 };
@@ -147,6 +148,7 @@ struct rsft_plan_s {
   std::vector<float> hf[3];                       // fp32 weights [L][N_d]
   std::vector<double> beta, gamma;                // [L]
   std::vector<uint32_t> xmask;                    // [L][B_last][N_last/32] (may be empty)
+  std::vector<uint32_t> ntab;                     // vote nibble tables [L][B_last/4][16][N_last/32] (may be empty)
   rsft::Workspace ws{};
   // binding
   bool bound = false;
