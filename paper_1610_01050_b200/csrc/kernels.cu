@@ -505,22 +505,32 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
 #pragma unroll
         for (int b = 0; b < 6; ++b) pl[c][b] = 0u;
       }
+      // shared-window byte addresses (32-bit arithmetic; E row of loop l, bucket k_rd at
+      // e_l + k_rd W 4; k_rd from the low bits of sigma * row mod N_rd (power of two: the
+      // 32-bit product is exact mod 2^32)
+      const uint32_t e_w0 = smem_u32(E) + (uint32_t)w0 * 4u;
+      const uint32_t rowu = (uint32_t)row, nrdm = (uint32_t)(nrd - 1);
+      const uint32_t sig_base = smem_u32(sig_rd);
       for (int l = 0; l < L; ++l) {
-        // low bits of sigma * row mod N_rd (power of two): 32-bit product is exact mod 2^32
-        const int krd = D >= 2 ? (int)(((uint32_t)sig_rd[l] * (uint32_t)row) & (uint32_t)(nrd - 1)) >> lga_rd : 0;
-        const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
+        uint32_t sg;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sg) : "r"(sig_base + 4u * (uint32_t)l));
+        const uint32_t krd = D >= 2 ? ((sg * rowu) & nrdm) >> lga_rd : 0u;
+        const uint32_t ea = e_w0 + (((uint32_t)l * (uint32_t)brd + krd) * (uint32_t)W) * 4u;
         uint32_t m[CW];
         if (CW % 4 == 0) {
 #pragma unroll
           for (int q = 0; q < CW; q += 4) {
-            const uint4 v = *reinterpret_cast<const uint4*>(e + q);
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ea + 4u * (uint32_t)q));
             m[q] = v.x; m[(q + 1) % CW] = v.y; m[(q + 2) % CW] = v.z; m[(q + 3) % CW] = v.w;
           }
         } else if (CW == 2) {
+          const uint32_t* e = E + ((size_t)l * brd + krd) * W + w0;
           const uint2 v = *reinterpret_cast<const uint2*>(e);
           m[0] = v.x; m[CW > 1 ? 1 : 0] = v.y;
         } else {
-          m[0] = e[0];
+          m[0] = E[((size_t)l * brd + krd) * W + w0];
         }
         uint32_t any = 0;
 #pragma unroll
