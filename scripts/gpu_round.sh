@@ -11,6 +11,9 @@ python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/
 python bench.py --workload c5_cube --no-cpu --no-e2e > $OUT/bench_c5.json 2> $OUT/bench_c5.err
 python bench.py --workload c5_cube --no-cpu --no-e2e --c5-variant A > $OUT/bench_c5A.json 2> $OUT/bench_c5A.err
 python bench.py --impl reference --steps 2 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+python bench.py --workload c1_1d --frames 131072 --steps 10 --no-cpu --no-e2e > $OUT/bench_c1.json 2> $OUT/bench_c1.err
+python bench.py --workload c2_2d --frames 8192 --steps 10 --no-cpu --no-e2e > $OUT/bench_c2.json 2> $OUT/bench_c2.err
+python bench.py --workload c3_3d --frames 256 --steps 10 --no-cpu --no-e2e > $OUT/bench_c3.json 2> $OUT/bench_c3.err
 for wl in c4_batched_2d c5_cube; do
   CMD="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --workload $wl"
   $CMD > $OUT/plain_$wl.log 2>&1 && \
