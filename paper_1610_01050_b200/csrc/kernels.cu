@@ -219,10 +219,10 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
 
 // ------------------------------------------------------------------------------------
 // TMA bulk-copy pipeline (per warp): lane 0 streams row segments of x global -> shared
-// with cp.async.bulk (SASS UBLKCP) into a kStages-deep ring, completion tracked by one
+// with cp.async.bulk (SASS UBLKCP) into an S-deep ring, completion tracked by one
 // mbarrier per stage (expect_tx / complete_tx); all lanes wait on the stage's phase, read
 // their 16 B with LDS.128 and run the FFMA2 fold.  Bytes in flight per warp are explicit
-// ((kStages-1) x U x 512 B), independent of registers and of ptxas scheduling.
+// ((S-1) x U x 512 B), independent of registers and of ptxas scheduling.
 // ------------------------------------------------------------------------------------
 // Programmatic dependent launch: every hot-path kernel is launched with programmatic stream
 // serialization and starts with griddepcontrol.wait (before any global access: the previous
@@ -665,15 +665,14 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
 // smem: ring [nwarps][S][U][32] float4 | bars [nwarps][S] | F [G][nl][bouter][blast+1] |
 //       tw[128] | rowW [N0+1][LP] float (row N0 = zeros)
 // ------------------------------------------------------------------------------------
-template <int LP, int U>
-__global__ void __launch_bounds__(kThreads, 2) k_fused(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
+template <int LP, int U, int S, int T, int C>
+__global__ void __launch_bounds__(T, C) k_fused(PlanDev pd, const __grid_constant__ CUtensorMap tmap,
                                                     int64_t batch, int l0, int nl,
                                                     uint32_t* __restrict__ bitmaps,
                                                     float2* __restrict__ spectra, int64_t bm_stride,
                                                     int64_t sp_stride) {
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int S = kStages;
   const int D = pd.D;
   const int blast = pd.blast, nlast = pd.nlast, bouter = pd.bouter;
   const int fstride = blast + 1;
@@ -2136,22 +2135,24 @@ template <int LP>
 static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                   uint32_t* bm, void* spectra, cudaStream_t st, int64_t frame_stride = 0,
                                   int64_t bm_stride = 0, int64_t sp_stride = 0) {
-  auto kern = k_fused<LP, kU>;
+  constexpr FusedCfg F2 = kFused2D, F1 = kFused1D;
+  const FusedCfg fc = fused_cfg(p->D);
+  auto kern = p->D == 2 ? k_fused<LP, F2.u, F2.stages, F2.threads, F2.ctas> : k_fused<LP, F1.u, F1.stages, F1.threads, F1.ctas>;
   const size_t smem = fused_smem_bytes(p, nl, LP);
   if (bm_stride == 0) bm_stride = (int64_t)nl * p->dev.wpl;
   if (sp_stride == 0) sp_stride = (int64_t)nl * p->btot;
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, kU, frame_stride);
+  rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, fc.u, frame_stride);
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   int nb = 0;
-  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem), "occupancy");
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, fc.threads, smem), "occupancy");
   if (s) return s;
   if (nb < 1) { set_error("k_fused: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > batch) grid = batch;
-  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreads, smem, st, p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra),
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, fc.threads, smem, st, p->dev, tmap, batch, l0, nl, bm, reinterpret_cast<float2*>(spectra),
                                                bm_stride, sp_stride); le_ != cudaSuccess)
     return check(le_, "kern launch");
   p->last_launches += 1;

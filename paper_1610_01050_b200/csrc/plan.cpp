@@ -239,13 +239,14 @@ void layout_workspace(rsft_plan_s* p) {
 
 // Shared-memory footprints (must match the carve-up at the top of k_fused / k_split_fold).
 size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
-  const int nwarps = kThreads / 32;
+  const FusedCfg fc = fused_cfg(p->D);
+  const int nwarps = fc.threads / 32;
   int64_t blast = p->b[p->D - 1], nlast = p->n[p->D - 1];
   int64_t bouter = p->btot / blast;
   int64_t nseg = nlast / 64;
   int64_t groups = p->D == 1 ? (nseg < 8 ? nseg : 8) : 1;
   int64_t n0 = p->D == 2 ? p->n[0] : 1;
-  size_t ring = (size_t)nwarps * kStages * kU * 512 + (size_t)nwarps * kStages * 8;
+  size_t ring = (size_t)nwarps * fc.stages * fc.u * 512 + (size_t)nwarps * fc.stages * 8;
   size_t fbytes = (((size_t)groups * nl * bouter * (blast + 1) + 1) & ~size_t(1)) * 8 + 128 * 8;
   return ring + fbytes + (size_t)(n0 + 1) * lpad * 4;
 }
@@ -292,7 +293,7 @@ int resolve_mode(const rsft_plan_s* p, int64_t batch) {
   const int64_t nlast = p->n[p->D - 1];
   const int lp = loop_pad(p->L);
   bool fused_ok = p->D <= 2 && nlast >= 64 && p->btot <= 8 * kThreads &&
-                  fused_smem_bytes(p, p->L, lp) <= 110 * 1024;
+                  fused_smem_bytes(p, p->L, lp) <= (fused_cfg(p->D).ctas == 1 ? 220 : 110) * 1024;
   // split mode chunks dim 0 as far as needed to fit the per-warp tables (launch_split_fold_t)
   const int64_t amin = p->D == 3 ? 1 : std::min<int64_t>(p->a[0], (int64_t)kUSplit * (nlast >= 64 ? 1 : 64 / nlast));
   bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp, amin) <= 220 * 1024;

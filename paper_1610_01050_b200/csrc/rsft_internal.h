@@ -18,8 +18,13 @@ constexpr int kMaxB = 64;          // register FFT lines and lane folds support 
 constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detection bitmap
 constexpr int kThreads = 256;          // CTA size of most kernels
 constexpr int kThreadsFft = 1024;      // split-mode outer FFT: one L2 round trip per thread
-constexpr int kStages = 3;             // TMA ring depth per warp (fold kernels)
-constexpr int kU = 4;                  // 512 B row slots per ring stage
+// Fused fold kernel shapes (threads per CTA, CTAs per SM, ring stages per warp, 512-B rows per
+// stage), chosen by dimension (fused_cfg): D = 2 frames stream long residue classes, so one
+// 16-warp CTA per SM with 4-KiB boxes (2 stages) keeps the most bytes in flight per box issued
+// (c4: 1.40 vs 1.44 ms); D = 1 frames are short and favour two 8-warp CTAs with 2-KiB boxes.
+struct FusedCfg { int threads, ctas, stages, u; };
+constexpr FusedCfg kFused2D = {512, 1, 2, 8};
+constexpr FusedCfg kFused1D = {256, 2, 3, 4};
 #ifndef RSFT_NO_TMA
 #define RSFT_NO_TMA 0
 #endif
@@ -166,6 +171,7 @@ void layout_workspace(rsft_plan_s* p);
 int resolve_mode(const rsft_plan_s* p, int64_t batch);
 int loop_pad(int nl);
 size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
+inline FusedCfg fused_cfg(int D) { return D == 2 ? kFused2D : kFused1D; }
 size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c);
 int split_lg_chunks(const rsft_plan_s* p, int64_t batch, int nl, int64_t a0_count, int64_t warps_total);
 void set_error(const std::string& s);
