@@ -23,7 +23,10 @@ constexpr int kThreadsFft = 1024;      // split-mode outer FFT: one L2 round tri
 // 16-warp CTA per SM with 4-KiB boxes (2 stages) keeps the most bytes in flight per box issued
 // (c4: 1.40 vs 1.44 ms); D = 1 frames are short and favour two 8-warp CTAs with 2-KiB boxes.
 struct FusedCfg { int threads, ctas, stages, u; };
-constexpr FusedCfg kFused2D = {512, 1, 2, 8};
+#ifndef RSFT_F2
+#define RSFT_F2 512, 1, 2, 8
+#endif
+constexpr FusedCfg kFused2D = {RSFT_F2};
 constexpr FusedCfg kFused1D = {256, 2, 3, 4};
 #ifndef RSFT_NO_TMA
 #define RSFT_NO_TMA 0
