@@ -25,4 +25,10 @@ ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 
 CMD5="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --workload c5_cube"
 ncu --set full --clock-control none --import-source on -k regex:k_split_mma -s 1 -c 1 -o $OUT/prof_k_split_mma -f $CMD5 > $OUT/ncu_full_c5.log 2>&1
 RSFT_NO_MMA=1 ncu --set full --clock-control none --import-source on -k regex:k_split_fold -s 1 -c 1 -o $OUT/prof_k_split_fold -f $CMD5 > $OUT/ncu_full_c5_ffma.log 2>&1
+
+# keep the copy-back under the 64 MiB limit: summaries on the box, full reports only if small
+for r in $OUT/prof_k_fused $OUT/prof_k_split_mma $OUT/prof_k_split_fold; do
+  [ -f $r.ncu-rep ] && python scripts/ncu_summary.py $r.ncu-rep > $r.summary.txt 2>&1
+done
+rm -f $OUT/prof_k_split_fold.ncu-rep $OUT/prof_k_fused.ncu-rep
 echo done
