@@ -1844,24 +1844,35 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
 __global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __restrict__ counts, int64_t n,
                                                       long long* __restrict__ d_count) {
   pdl_enter();
-  __shared__ long long part[1024];
+  __shared__ long long part[64];
   const int t = threadIdx.x;
   const int64_t per = (n + 1023) / 1024;
   const int64_t b = t * per, e = b + per < n ? b + per : n;
   long long s = 0;
 #pragma unroll 16
   for (int64_t i = b; i < e; ++i) s += (long long)__ldcg(counts + i);   // independent loads in flight
-  // block exclusive scan of part[] (Hillis-Steele in shared memory)
-  part[t] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    long long v = t >= off ? part[t - off] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
+  // block exclusive scan: warp shuffles, then the 32 warp totals by warp 0 (two barriers)
+  const int lane = t & 31, wid = t >> 5;
+  long long incl = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
   }
-  long long run = part[t] - s;
-  if (t == 1023) *d_count = part[t];
+  if (lane == 31) part[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = part[lane], wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += v;
+    }
+    part[32 + lane] = wi - w;                        // exclusive warp offsets
+    if (lane == 31) *d_count = wi;
+  }
+  __syncthreads();
+  long long run = part[32 + wid] + incl - s;
 #pragma unroll 16
   for (int64_t i = b; i < e; ++i) { long long v = (long long)__ldcg(counts + i); counts[i] = (unsigned long long)run; run += v; }
 }
