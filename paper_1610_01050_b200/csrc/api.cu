@@ -138,6 +138,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   pd.region_state = reinterpret_cast<unsigned long long*>(base + p->ws.region_off);
   pd.region_capacity = p->ws.region_capacity;
   pd.region_slots = p->ws.slots_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.slots_off) : nullptr;
+  pd.list_cap = (int32_t)p->ws.list_cap;
   pd.etab = p->ws.etab_bytes ? reinterpret_cast<uint32_t*>(base + p->ws.etab_off) : nullptr;
   pd.etab_frames = p->ws.etab_bytes
                        ? (int64_t)(p->ws.etab_bytes / ((size_t)p->L * p->b[0] * p->b[1] * (p->n[2] / 32) * 4)) : 0;

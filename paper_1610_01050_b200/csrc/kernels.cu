@@ -626,7 +626,7 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
         pos[k] = total + before + incl[k] - ck[k];
         total += tk;
       }
-      if (total <= kListCap) {
+      if (total <= pd.list_cap) {
 #pragma unroll
         for (int k = 0; k < kListIpt; ++k) {
           const int64_t it = tid + (int64_t)k * blockDim.x;
@@ -1820,7 +1820,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t
     if (LIST) {                                      // region-local index list + count
       const int t = vote_region<CW, MODE, true>(pd, bm, lw, E, sig_rd, Xs, NT, kpre_s, sig_ld, frame, i0, d0b, d0e,
                                                 detect, counts, use_etab, wsum,
-                                                pd.region_slots + (size_t)region * kListCap);
+                                                pd.region_slots + (size_t)region * pd.list_cap);
       if (tid == 0) rcount[region] = (unsigned long long)t;
       continue;
     }
@@ -1887,7 +1887,8 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
                                                            const unsigned long long* __restrict__ offsets,
                                                            const long long* __restrict__ d_count, int64_t nregions,
                                                            const uint32_t* __restrict__ slots,
-                                                           long long* __restrict__ idx, int64_t capacity) {
+                                                           long long* __restrict__ idx, int64_t capacity,
+                                                           int list_cap) {
   pdl_enter();
   __shared__ int wsum[kThreads / 32];
   __shared__ long long s_idx[kStageIdx];
@@ -1897,8 +1898,8 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
   long long run = (long long)offsets[r];
   if (slots) {                                       // the vote left a region-local index list
     const long long n = (r + 1 < nregions ? (long long)offsets[r + 1] : *d_count) - run;
-    if (n <= kListCap) {
-      const uint32_t* sl = slots + (size_t)r * kListCap;
+    if (n <= list_cap) {
+      const uint32_t* sl = slots + (size_t)r * list_cap;
       const long long g0 = r * rwords * 32;
       for (long long i = tid; i < n; i += blockDim.x)
         if (run + i < capacity) idx[run + i] = g0 + (long long)sl[i];
@@ -2457,7 +2458,7 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   if (cudaError_t le_ = pdl_launch(k_region_write, (unsigned)nregions, kThreads, 0, st, det, rwords, p->dev.region_state,
                                                           reinterpret_cast<long long*>(d_count), nregions,
                                                           list ? p->dev.region_slots : nullptr,
-                                                          reinterpret_cast<long long*>(idx), capacity); le_ != cudaSuccess)
+                                                          reinterpret_cast<long long*>(idx), capacity, (int)p->dev.list_cap); le_ != cudaSuccess)
     return check(le_, "k_region_write launch");
   p->last_launches += 2;
   return check(cudaGetLastError(), "region scan/write launch");

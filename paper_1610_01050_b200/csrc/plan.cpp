@@ -216,8 +216,13 @@ void layout_workspace(rsft_plan_s* p) {
   w.ntab_off = off; off = align256(off + w.ntab_bytes);
   w.region_capacity = p->P.max_batch * (p->D == 3 ? p->n[0] : 1) + 2;
   w.region_off = off; off = align256(off + 8 * (size_t)w.region_capacity);
-  w.slots_off = off;                               // vote index lists (kListCap per region)
-  w.slots_bytes = (size_t)w.region_capacity * kListCap * 4;
+  w.slots_off = off;                               // vote index lists (list_cap per region)
+  {
+    int64_t cap = kListCapMax;
+    while (cap > kListCapMin && (size_t)w.region_capacity * cap * 4 > kListSlotsBytes) cap >>= 1;
+    w.list_cap = cap;
+  }
+  w.slots_bytes = (size_t)w.region_capacity * w.list_cap * 4;
   off = align256(off + w.slots_bytes);
   w.etab_off = off;                                // D == 3 vote: E words for every dim-0 bucket
   w.etab_bytes = 0;

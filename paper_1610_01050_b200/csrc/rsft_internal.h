@@ -54,7 +54,9 @@ constexpr int kUSplit = RSFT_SPLIT_U;             // ... U-slot (U x 512 B) TMA 
 constexpr int kThreadsSplit = RSFT_SPLIT_THREADS; // threads per CTA ...
 constexpr int kCtasSplit = RSFT_SPLIT_CTAS;       // ... and CTAs per SM the kernel is built for
 constexpr int kSplitUnitsPerWarp = 4;
-constexpr int kListCap = 2048;                   // vote: region-local index slots per region
+constexpr int kListCapMin = 2048;                // vote: region-local index slots per region, at least ...
+constexpr int kListCapMax = 8192;                // ... and at most (as many as 256 MiB of slots allow)
+constexpr size_t kListSlotsBytes = 256ull << 20;
 constexpr int kSplitDftBytes = 16384;            // split-mode last-dim DFT factor table [r][l][k] (float4) up to this size
 constexpr int kSplitHlastBytes = 16384;          // column-weight table kept in smem up to this size             // chunking target: >= this many units per warp
 
@@ -125,7 +127,8 @@ struct PlanDev {
   const uint32_t* ntab;            // nibble tables of the masks [L][B_last/4][16][N_last/32], or null
   unsigned long long* region_state; // per-region detection counts -> offsets (rsft_detect_compact)
   int64_t region_capacity;
-  uint32_t* region_slots;          // per-region local index lists [region_capacity][kListCap] (or null)
+  uint32_t* region_slots;          // per-region local index lists [region_capacity][list_cap] (or null)
+  int32_t list_cap;                // index slots per region
   uint32_t* etab;                  // D == 3 vote: E words for every dim-0 bucket [batch][L][B0][B1][W] (or null)
   int64_t etab_frames;             // frames etab holds
   const float* bwin[kMaxDim];      // Bartlett: fp32 pre-windows w_d [N_d]
@@ -140,6 +143,7 @@ constexpr size_t kMaxEtabBytes = 64ull << 20;  // D == 3 vote: precomputed E tab
 struct Workspace {
   size_t loops_off, h_off[kMaxDim], ht_off[kMaxDim], fbuf_off, fbuf_bytes, chunk_off, xmask_off, xmask_bytes, region_off, slots_off, slots_bytes, etab_off, etab_bytes, ntab_off, ntab_bytes, bwin_off[kMaxDim], bone_off, btw_off, total;
   int64_t region_capacity;
+  int64_t list_cap;
   int64_t chunk_capacity;
 };
 
