@@ -170,10 +170,14 @@ def test_compaction_capacity_overflow():
     np.testing.assert_array_equal(res["idx"], full["idx"][:10])
 
 
-def test_determinism_bitwise():
+@pytest.mark.parametrize("n,b,L", [((64, 32, 32), (8, 4, 8), 4),       # FFMA2 split fold
+                                   ((16, 128, 64), (4, 8, 8), 8)])    # tensor-core fold (k_split_mma)
+def test_determinism_bitwise(n, b, L):
+    """Bitwise-reproducible spectra (fixed reduction orders; the tensor-core fold sums its two
+    worker groups' accumulators in a fixed order)."""
     import torch
-    op = oracle_params((64, 32, 32), (8, 4, 8), 4, p_fa=1e-3, seed=3)
-    wl = synth.Workload("det", (64, 32, 32), (8, 4, 8), 4, 1e-3, 1.0, (4, 8), (0.0, 20.0), 1, data_seed=8)
+    op = oracle_params(n, b, L, p_fa=1e-3, seed=3)
+    wl = synth.Workload("det", n, b, L, 1e-3, 1.0, (4, 8), (0.0, 20.0), 1, data_seed=8)
     x = frames(wl, 1)
     plan = make_plan(op).bind()
     a = gpu_run(plan, x)
