@@ -1727,7 +1727,10 @@ __global__ void __launch_bounds__(kThreads) k_etab(PlanDev pd, const uint32_t* _
 }
 
 template <int CW, int MODE, bool COUNT, bool LIST>
-__global__ void __launch_bounds__(kThreads, 4) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
+#ifndef RSFT_VOTE_CTAS
+#define RSFT_VOTE_CTAS 4
+#endif
+__global__ void __launch_bounds__(kThreads, RSFT_VOTE_CTAS) k_vote(PlanDev pd, const uint32_t* __restrict__ bitmaps,
                                                    int64_t d0b, int64_t d0e, int lw, int64_t np, int64_t nregions,
                                                    uint32_t* __restrict__ detect, uint8_t* __restrict__ counts,
                                                    unsigned long long* __restrict__ rcount, int use_etab) {
