@@ -114,13 +114,6 @@ def dist_env():
     return rank, world, local
 
 
-def host_frames(wl, rank, frames, pool):
-    """`frames` frames for this rank: a pool of `pool` distinct seeded frames tiled."""
-    base = synth.gen_batch(wl, range(rank * pool, rank * pool + pool))
-    reps = (frames + pool - 1) // pool
-    return np.concatenate([base] * reps, axis=0)[:frames]
-
-
 # ----------------------------------------------------------------------------- reference arm
 def oracle_worker(args):
     """Run the oracle on the given frames; inputs are generated before the clock starts."""
@@ -158,7 +151,16 @@ def oracle_rate(wl, budget_s=12.0, max_cores=32):
         with ctx.Pool(cores) as pool:
             el = max(pool.map(oracle_worker, chunks))
     return nframes / el, cores, (f"{nframes} frames of {wl.name}: oracle rsft_run (fp64, literal Alg. 1), "
-                                 f"{cores} processes x 1 thread, input generation untimed")
+                                 f"{cores} processes x 1 thread, input generation untimed"), one
+
+
+def ref_config(wl, a):
+    """Same config dict as the GPU arm's line for this workload (bench.py workload_config)."""
+    if wl.name == "c5_cube":
+        return workload_config(wl, 1, variant=a.c5_variant if a.gpus > 1 else "A", world=a.gpus)
+    cfg = workload_config(wl, a.frames or wl.batch)
+    cfg["mode"] = "fused" if len(wl.n) <= 2 else "split"
+    return cfg
 
 
 def run_reference(a):
@@ -171,35 +173,115 @@ def run_reference(a):
     cores = 1
     steps = max(1, a.steps)
     budget = max(2.0, min(20.0, 150.0 / steps))         # whole run within a few minutes
+    ones = []
     for _ in range(steps):
-        r, cores, sample = oracle_rate(wl, budget_s=budget)
+        r, cores, sample, one = oracle_rate(wl, budget_s=budget)
         rates.append(r)
+        ones.append(one)
     value = float(statistics.median(rates))
     frames_per_step = wl.batch
+    unit = "cubes/s" if wl.name == "c5_cube" else "frames/s"
     out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": a.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": a.gpus,
         "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * frames_per_step / value,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if wl.name == "c5_cube" else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Eq. sig_model frames)",
-        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": wl.loops, "p_fa": wl.p_fa},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
-        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": ref_config(wl, a),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample,
+                         "one_core_s_per_frame": statistics.median(ones)},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
     return 0
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def workload_config(wl, frames, mode=None, variant=None, world=1):
+    """The `config` dict of a bench line; identical in both arms (ours / reference)."""
+    cfg = {"workload": wl.name, "frames_per_gpu": frames, "n": list(wl.n), "b": list(wl.b), "loops": wl.loops,
+           "p_fa": wl.p_fa, "mu": wl.mu or wl.loops}
+    if wl.name == "c5_cube":
+        cfg["variant"] = variant
+        cfg["l2"] = "cube 512 MiB >> 126 MB L2 (no flush needed)"
+    else:
+        cfg["l2"] = f"inputs {frames * wl.ntot * 8 / 2**30:.1f} GiB per GPU >> 126 MB L2 (no flush needed)"
+        cfg["parallelism"] = "frames sharded over the GPUs (weak scaling), no data-path collective"
+    return cfg
+
+
+def step_stats(step_ms):
+    s = sorted(step_ms)
+    p90 = s[min(len(s) - 1, int(math.ceil(0.9 * len(s))) - 1)]
+    return {"median": statistics.median(s), "p90": p90, "min": s[0], "max": s[-1]}
+
+
+def digest(*tensors):
+    """sha1 over the bytes of device tensors (run-to-run / collective-vs-not bit identity)."""
+    import hashlib
+    h = hashlib.sha1()
+    for t in tensors:
+        h.update(t.contiguous().view(-1).view(__import__("torch").uint8).cpu().numpy().tobytes())
+    return h.hexdigest()[:16]
+
+
+def init_dist(a):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if a.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world} (launch with torchrun "
+                         f"--nproc-per-node {a.gpus}, or without WORLD_SIZE to self-launch)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 or a.force_collectives:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+    return rank, world, local, dev, dist.is_initialized()
+
+
+def timed_steps(a, step, stream, local, pg):
+    """W warm-up steps, then K timed steps between barrier + synchronize on both sides.
+    Returns (elapsed ms max over ranks, per-step ms, per-step (k1 begin, k1 end) events,
+    launches, clocks)."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    if pg:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches = 0
+    for k in range(a.steps):
+        marks[k].record(stream)
+        launches += step(ev[k])
+    marks[-1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if pg:
+        dist.barrier()
+    el = torch.tensor([marks[0].elapsed_time(marks[-1])], device="cuda")
+    if pg:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    per_step = [marks[k].elapsed_time(marks[k + 1]) for k in range(a.steps)]
+    return float(el.item()), per_step, ev, launches, clocks
+
+
 def main_gpu(a):
     import torch
     import torch.distributed as dist
     from paper_1610_01050_b200 import rsft as B
 
-    rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    rank, world, local, dev, pg = init_dist(a)
     wl = synth.WORKLOADS[a.workload]
     stream = torch.cuda.current_stream()
 
@@ -208,13 +290,18 @@ def main_gpu(a):
     if a.segments:
         return bench_segments(a, wl, rank, world, dev)
     if wl.name == "c5_cube":
-        return bench_c5(a, wl, rank, world, dev)
+        return bench_c5(a, wl, rank, world, dev, pg)
 
     frames = a.frames or wl.batch
     plan = B.Plan(wl.n, wl.b, wl.loops, support=wl.support, p_fa=wl.p_fa, noise_var=wl.noise_var,
                   seed=wl.sched_seed, random_tau=wl.random_tau, mu=wl.mu, max_batch=frames).bind()
-    hx = host_frames(wl, rank, frames, a.pool)
-    x = torch.from_numpy(hx).to(dev)
+    pool = min(a.pool, frames)
+    base = torch.from_numpy(synth.gen_batch(wl, range(rank * pool, rank * pool + pool)))
+    x = torch.empty((frames,) + tuple(wl.n), dtype=torch.complex64, device=dev)
+    base_d = base.to(dev)
+    for f0 in range(0, frames, pool):                      # tile the pool on the device
+        x[f0:f0 + pool].copy_(base_d[:frames - f0])
+    del base_d
     bm = plan.new_bitmaps(frames)
     det = torch.empty((frames, plan.detect_words), dtype=torch.int32, device=dev)
     cap = frames * 4096
@@ -233,41 +320,21 @@ def main_gpu(a):
         plan.detect_compact(bm, cap, detect=det, idx=idx, count=cnt)
         return n + plan.last_launch_count()
 
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    launches = 0
-    t0.record(stream)
-    for k in range(a.steps):
-        launches += step(ev[k])
-    t1.record(stream)
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    if world > 1:
-        dist.barrier()
-    elapsed_ms = t0.elapsed_time(t1)
+    elapsed_ms, per_step, ev, launches, clocks = timed_steps(a, step, stream, local, pg)
     k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    el = torch.tensor([elapsed_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(el.item())
     detections = int(cnt.item())
+    dig = digest(bm, det, idx[:min(detections, cap)])
 
     # e2e through the C ABI on HOST buffers (H2D copy + kernels + D2H of count and indices)
     e2e = None
     if not a.no_e2e:
-        hpin = torch.from_numpy(hx).pin_memory()
+        hpin = torch.empty((frames,) + tuple(wl.n), dtype=torch.complex64, pin_memory=True)
+        for f0 in range(0, frames, pool):
+            hpin[f0:f0 + pool].copy_(base[:frames - f0])
         scratch = torch.empty(plan.host_scratch_bytes(frames, cap), dtype=torch.uint8, device=dev)
         plan.run_host(hpin, cap, scratch)
         e_steps = max(1, min(a.steps, 5))
-        if world > 1:
+        if pg:
             dist.barrier()
         tt0, tt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -279,15 +346,19 @@ def main_gpu(a):
         tt1.record(stream)
         torch.cuda.synchronize()
         e_ms = torch.tensor([tt0.elapsed_time(tt1) / e_steps], device=dev)
-        if world > 1:
+        if pg:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": world * frames / (float(e_ms.item()) / 1000.0), "unit": "frames/s",
                "h2d_bytes_per_step": int(hpin.numel() * 8), "d2h_bytes_per_step": int(8 + 8 * nidx)}
         del scratch, hpin
 
+    ranks = None
+    if pg:          # report gather (outside the timed region): per-rank detections and digests
+        ranks = [None] * world
+        dist.all_gather_object(ranks, {"rank": rank, "detections": detections, "digest": dig,
+                                       "ms": elapsed_ms})
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return 0
 
     # roofline of the dominant kernel (fused fold + FFT + threshold, one launch per step):
@@ -300,18 +371,15 @@ def main_gpu(a):
     value = world * frames / (step_ms / 1000.0)
     cpu = None
     if not a.no_cpu:
-        r, cores, sample = oracle_rate(wl, budget_s=a.cpu_budget)
-        cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline(wl, a.cpu_budget)
+    cfg = workload_config(wl, frames)
+    cfg["mode"] = {1: "fused", 2: "split"}.get(plan.mode, plan.mode)
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
-        "data": f"synthetic: {a.pool} distinct seeded Eq. sig_model frames per GPU tiled to {frames}",
-        "config": {"workload": wl.name, "frames_per_gpu": frames, "n": list(wl.n), "b": list(wl.b),
-                   "loops": wl.loops, "p_fa": wl.p_fa, "mu": plan.loops if not wl.mu else wl.mu,
-                   "mode": {1: "fused", 2: "split"}.get(plan.mode, plan.mode),
-                   "l2": f"inputs {frames * plan.ntot * 8 / 2**30:.1f} GiB per GPU >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"frames sharded over {world} GPU(s), no data-path collective"},
+        "warmup": a.warmup, "ms_per_step": step_ms, "step_ms": step_stats(per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic: {pool} distinct seeded Eq. sig_model frames per GPU tiled to {frames}",
+        "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(wl.name),
                      "kernel": "k_fused (pre-window+permute+flat window+fold+FFT+threshold)",
@@ -320,22 +388,32 @@ def main_gpu(a):
         "gpu_launches": launches,
         "clocks": clocks,
         "detections_per_step": detections,
+        "digest": dig,
+        "collectives": {"process_group": pg, "backend": "nccl" if pg else None, "ranks": ranks},
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if pg:
         dist.destroy_process_group()
     return 0
 
 
-def bench_c5(a, wl, rank, world, dev):
+def cpu_baseline(wl, budget):
+    r, cores, sample, one = oracle_rate(wl, budget_s=budget)
+    return {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "one_core_s_per_frame": one}
+
+
+def bench_c5(a, wl, rank, world, dev, pg):
     """Single 512 MiB cube, L=16 loops sharded over ranks, NCCL all-gather of the per-loop
     bitmaps (2 KiB/loop), then voting on this rank's dim-0 slab (BASELINE configs[4]).
     Variant B (default): each rank folds only its dim-0 slab for all loops
     (rsft_bucketize_partial), the partial folded spectra are reduce-scattered over loops
     (NCCL), each rank finalizes its loops (rsft_finalize).  Variant A: each rank reads the
-    whole cube for its loops (rsft_execute loop range)."""
+    whole cube for its loops (rsft_execute loop range).  Without a process group (one GPU,
+    no --force-collectives) variant B's collectives are identities: B == A's computation
+    is then run as A (rsft_execute), and the line says so."""
     import torch
     import torch.distributed as dist
     from paper_1610_01050_b200 import rsft as B
@@ -349,9 +427,10 @@ def bench_c5(a, wl, rank, world, dev):
     n0 = wl.n[0]
     d0b, d0e = shard.slab_range(rank, world, n0, plan.ntot // n0)
     hx = synth.gen_batch(wl, [0])
-    if a.c5_variant == "B" and world == 1:
-        a.c5_variant = "A"          # one GPU: the slab is the whole cube; rsft_execute is the same computation
-    if a.c5_variant == "B":
+    variant = a.c5_variant
+    if variant == "B" and not pg:
+        variant = "A"
+    if variant == "B":
         x = torch.from_numpy(np.ascontiguousarray(hx[0, d0b:d0e])).to(dev)     # this rank's slab only
         partial = torch.empty((L, plan.btot), dtype=torch.complex64, device=dev)
     else:
@@ -360,11 +439,12 @@ def bench_c5(a, wl, rank, world, dev):
     mine = plan.new_bitmaps(1, le - lb)
     slab_words = (d0e - d0b) * (plan.ntot // n0) // 32
     det = torch.empty((1, slab_words), dtype=torch.int32, device=dev)
+    keep = {}
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        if a.c5_variant == "B":
+        if variant == "B":
             plan.bucketize_partial(x, d0b, partial=partial)
             n = plan.last_launch_count()
             folded = shard.reduce_scatter_loops(partial, world)
@@ -376,58 +456,52 @@ def bench_c5(a, wl, rank, world, dev):
         if ev is not None:
             ev[1].record(stream)
         src = shard.gather_loop_bitmaps(mine[0], world).reshape(1, L, plan.bitmap_words)
+        keep["src"] = src
         plan.detect(src, dim0=(d0b, d0e), detect=det)
         n += plan.last_launch_count()
         return n
 
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    launches = 0
-    t0.record(stream)
-    for k in range(a.steps):
-        launches += step(ev[k])
-    t1.record(stream)
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    el = torch.tensor([t0.elapsed_time(t1)], device=dev)
-    if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed_ms, per_step, ev, launches, clocks = timed_steps(a, step, stream, int(os.environ.get("LOCAL_RANK", 0)), pg)
+    dig = digest(keep["src"], det)
+    ranks = None
+    if pg:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, {"rank": rank, "loops": [lb, le], "slab": [d0b, d0e], "digest": dig,
+                                       "detections": int(B.bitmap_to_bool(det.cpu().numpy().ravel(), slab_words * 32).sum())})
     if rank != 0:
         dist.destroy_process_group()
         return 0
-    step_ms = float(el.item()) / a.steps
+    step_ms = elapsed_ms / a.steps
     k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     peak, peak_src = load_peaks()
     cube_bytes = 8 * plan.ntot
-    algo = (cube_bytes // world if a.c5_variant == "B" else cube_bytes) + (le - lb) * plan.bitmap_words * 4
+    algo = (cube_bytes // world if variant == "B" else cube_bytes) + (le - lb) * plan.bitmap_words * 4
+    cfg = workload_config(wl, 1, variant=variant, world=world)
+    cfg["parallelism"] = (f"dim-0 slabs over {world} GPU(s), partial folds reduce-scattered over loops "
+                          f"(NCCL), loops finalized per rank, NCCL all-gather of bitmaps"
+                          if variant == "B" else
+                          f"loops sharded {world} way(s)" + (" + NCCL all-gather of bitmaps" if pg else
+                                                               " (one GPU, no process group: no collective)"))
+    mma = not os.environ.get("RSFT_NO_MMA")
     out = {
-        "metric": METRIC, "value": 1000.0 / step_ms, "unit": "cubes/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic: 1 seeded Eq. sig_model cube",
-        "config": {"workload": wl.name, "n": list(wl.n), "b": list(wl.b), "loops": L, "variant": a.c5_variant,
-                   "l2": "cube 512 MiB >> 126 MB L2 (no flush needed)",
-                   "parallelism": (f"dim-0 slabs over {world} GPU(s), partial folds reduce-scattered over loops "
-                                   f"(NCCL), loops finalized per rank, NCCL all-gather of bitmaps"
-                                   if a.c5_variant == "B" else
-                                   f"loops sharded {world} ways + NCCL all-gather of bitmaps")},
+        "metric": METRIC, "value": 1000.0 / step_ms, "unit": "cubes/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_ms, "step_ms": step_stats(per_step),
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (fold: 3xTF32 tcgen05, ~2^-20 rel.)" if mma else "f32",
+        "data": "synthetic: 1 seeded Eq. sig_model cube",
+        "config": cfg,
         "roofline": {"bound": "hbm", "achieved": algo / (k1 / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": algo / (k1 / 1000.0) / 1e9 / peak, "traffic": load_traffic(wl.name),
-                     "kernel": ("k_split_fold" if os.environ.get("RSFT_NO_MMA") else "k_split_mma (3xTF32 tcgen05)")
+                     "kernel": ("k_split_mma (3xTF32 tcgen05)" if mma else "k_split_fold")
                                + " + k_split_fft (first stage of this rank)",
                      "algorithmic_bytes_per_launch": algo, "avg_launch_ms": k1,
                      "share_of_step": k1 / step_ms, "peak_source": peak_src},
-        "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None, "e2e": None,
+        "gpu_launches": launches, "clocks": clocks, "digest": dig,
+        "collectives": {"process_group": pg, "backend": "nccl" if pg else None, "ranks": ranks},
+        "cpu_baseline": None, "e2e": None,
     }
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if pg:
         dist.destroy_process_group()
     return 0
 
@@ -537,12 +611,30 @@ def main():
     ap.add_argument("--bartlett", action="store_true", help="time the Bartlett baseline (Alg. 2) instead")
     ap.add_argument("--segments", action="store_true", help="time the RSFT in segment mode (P:204)")
     ap.add_argument("--c5-variant", default="B", choices=["A", "B"], help="c5 multi-GPU scheme (DESIGN.md §8)")
+    ap.add_argument("--force-collectives", action="store_true",
+                    help="initialise an NCCL process group even with one rank, so the multi-GPU code path "
+                         "(barriers, max-over-ranks timing, c5 reduce-scatter + all-gather) runs on a 1-GPU lease")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3
     if a.impl == "reference":
         return run_reference(a)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(a.gpus)
     return main_gpu(a)
+
+
+def relaunch(n):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run with N
+    ranks (one per GPU, rendezvous on 127.0.0.1) so --gpus N always measures N GPUs."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 if __name__ == "__main__":

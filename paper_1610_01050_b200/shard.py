@@ -38,35 +38,52 @@ def slab_range(rank: int, world: int, n0: int, locs_per_row: int):
     return b, e
 
 
-def gather_loop_bitmaps(local, world: int, group=None):
-    """All-gather per-loop bitmaps.  local: int32 tensor [loops_per_rank, words] (contiguous).
+def _world(group):
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0
+    return dist.get_world_size(group)
+
+
+def gather_loop_bitmaps(local, world: int = None, group=None):
+    """All-gather per-loop bitmaps.  local: int32 tensor [loops_per_rank, words].
     Returns [world * loops_per_rank, words] in loop order (rank-major = loop order because
-    each rank owns a contiguous loop range)."""
+    each rank owns a contiguous loop range).  Runs the collective whenever a process group is
+    initialised -- also with ONE rank (bench --force-collectives), so the NCCL path is the
+    one measured on a 1-GPU lease; without a process group the input is returned."""
     import torch
     import torch.distributed as dist
-    if world == 1:
+    w = _world(group)
+    if w == 0:
         return local
-    out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
+    if world is not None and world != w:
+        raise ValueError(f"world={world} but the process group has {w} ranks")
+    out = torch.empty((w * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     return out
 
 
-def reduce_scatter_loops(partial, world: int, group=None):
-    """Sum the slab partials [L, B_tot] over ranks and keep this rank's loop block
-    [L / world, B_tot] (loop order = rank order).  NCCL: reduce_scatter_tensor; backends
-    without it (gloo, CPU tests): all_reduce + slice."""
+def reduce_scatter_loops(partial, world: int = None, group=None):
+    """Sum the slab partials [L, ...] (complex64) over ranks and keep this rank's loop block
+    [L / world, ...] (loop order = rank order) with ONE reduce_scatter_tensor.
+    NCCL has no complex dtype and torch's reduce_scatter_tensor does not convert complex
+    tensors, so the message is sent as its float32 view (torch.view_as_real: re/im summed
+    independently, which is the complex sum).  The same call runs on gloo (CPU tests) and
+    NCCL.  Without a process group the input is returned."""
     import torch
     import torch.distributed as dist
-    if world == 1:
+    w = _world(group)
+    if w == 0:
         return partial
+    if world is not None and world != w:
+        raise ValueError(f"world={world} but the process group has {w} ranks")
     L = partial.shape[0]
-    if L % world:
-        raise ValueError(f"loops={L} must divide evenly over {world} ranks")
-    rank = dist.get_rank(group)
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((L // world,) + tuple(partial.shape[1:]), dtype=partial.dtype, device=partial.device)
-        dist.reduce_scatter_tensor(out, partial.contiguous(), group=group)
-        return out
-    full = partial.clone()
-    dist.all_reduce(full, group=group)
-    return full[rank * L // world:(rank + 1) * L // world].contiguous()
+    if L % w:
+        raise ValueError(f"loops={L} must divide evenly over {w} ranks")
+    src = partial.contiguous()
+    out = torch.empty((L // w,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    if src.is_complex():
+        dist.reduce_scatter_tensor(torch.view_as_real(out), torch.view_as_real(src), group=group)
+    else:
+        dist.reduce_scatter_tensor(out, src, group=group)
+    return out

@@ -201,13 +201,29 @@ def test_parity_full_size_single_frame(name):
 
 def test_parity_c4_full_batch_sampled():
     """c4 at full size in the bench launch configuration (4096 frames, fused persistent
-    kernel); sampled frames checked against the oracle one by one.  The batch tiles 64
-    distinct seeded frames (bench.py uses the same recipe with a larger pool)."""
+    kernel).  The batch tiles 64 distinct seeded frames (bench.py uses the same recipe with a
+    larger pool): every one of the 64 distinct frames is checked against the oracle (buckets,
+    bits, vote counts, detection set), and every tiled copy f + 64 k must give bit-identical
+    spectra, bitmaps, counts and detections on the GPU (all 4096 frames covered)."""
     wl = synth.C4
     pool = frames(wl, 64)
     x = np.concatenate([pool] * (wl.batch // 64), axis=0)
-    _, res, reps = run_case(wl_params(wl), x, check=[0, 1, 63, 2047, 4095])
-    assert reps[0]["max_ratio"] < 1e-4
+    _, res, reps = run_case(wl_params(wl), x, check=range(64))
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+    for key in ("spectra", "bm", "det", "counts"):
+        a = res[key].reshape((wl.batch // 64, 64) + res[key].shape[1:])
+        assert (a == a[:1]).all(), key
+
+
+@pytest.mark.parametrize("batch", [1, 8])
+def test_parity_c2_shape_fused_batch(batch):
+    """c2's exact shape (256x256, B=16x16, L=6, P_fa=1e-5) in FUSED mode (the kernel the c2
+    batched bench line runs), multi-frame, every frame against the oracle."""
+    wl = synth.C2.with_(batch=batch)
+    x = frames(wl, batch)
+    plan, _, reps = run_case(wl_params(wl), x, mode="fused")
+    assert plan.mode == 1
+    assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
 def test_parity_c5_full_cube():

@@ -118,3 +118,44 @@ def test_two_rank_slab_partials_reduce_scatter():
         ret = mgr.dict()
         mp.spawn(_worker_b, args=(world, free_port(), ret), nprocs=world, join=True)
         assert ret["err"] < 1e-12
+
+
+def _worker_c64(rank, world, port, ret):
+    """The complex64 message of variant B (the GPU dtype) through the one reduce_scatter_tensor
+    call shard.py also issues on NCCL (float32 view), at world 1 and 2."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L, bt = 8, 96
+        g = torch.Generator().manual_seed(5)
+        parts = [torch.complex(torch.randn(L, bt, generator=g), torch.randn(L, bt, generator=g))
+                 for _ in range(world)]
+        mine = shard.reduce_scatter_loops(parts[rank], world)
+        lb, le = shard.loop_range(rank, world, L)
+        want = sum(p.to(torch.complex128) for p in parts)[lb:le]
+        assert mine.dtype == torch.complex64 and mine.shape == (L // world, bt)
+        err = float((mine.to(torch.complex128) - want).abs().max())
+        bits = torch.arange(2 * 3, dtype=torch.int32).reshape(2, 3) + 100 * rank
+        allb = shard.gather_loop_bitmaps(bits, world)
+        okg = bool(torch.equal(allb, torch.cat([torch.arange(6, dtype=torch.int32).reshape(2, 3) + 100 * r
+                                                for r in range(world)])))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (err, okg))
+        if rank == 0:
+            ret["err"] = max(e for e, _ in gathered)
+            ret["gather_ok"] = all(o for _, o in gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_complex64_reduce_scatter_and_gather_through_collectives(world):
+    with mp.Manager() as mgr:
+        ret = mgr.dict()
+        mp.spawn(_worker_c64, args=(world, free_port(), ret), nprocs=world, join=True)
+        assert ret["err"] < 1e-5 and ret["gather_ok"]
+
+
+def test_no_process_group_passthrough():
+    x = torch.ones(4, 3, dtype=torch.complex64)
+    assert shard.reduce_scatter_loops(x) is x and shard.gather_loop_bitmaps(x) is x
