@@ -283,6 +283,9 @@ __device__ __forceinline__ void tma_load_4d_lane0(int lane, void* dst, uint64_t 
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
@@ -898,6 +901,165 @@ __global__ void __launch_bounds__(T, C) k_fused(PlanDev pd, const __grid_constan
 }
 
 // ------------------------------------------------------------------------------------
+// Fused mode, D == 1 with a short flat-window support (W <= 1024; c1: N = 4096, W = 512):
+// GATHER form of Alg. 1 l.5-10.  Per loop only the W permuted times t with |t_c| <= W/2
+// carry a non-zero flat-window weight, so the fold is f_l[b] = sum over the W/B taps
+// t = b (mod B) of h_l[s] x[s], s = sigma_l t + tau_l (mod N) (Def. 1, Def. 2
+// P:89-91, Eqs. z/l P:272-279; h = w g (-1)^floor(t/B) as in I3): L W complex x real MACs per
+// frame instead of L N.  Each warp owns one loop (two when L > 16); lane j owns taps
+// i = j + 32 k (t_c = i - W/2), whose sources s sit in registers with their weights for the
+// whole kernel (they depend on the loop only).  Consecutive t across the lanes of a warp map
+// to s = sigma t + tau with sigma odd, i.e. to 32 distinct banks mod 32: every gather from the
+// shared-memory frame is bank-conflict free.
+// A producer warp streams whole frames (N x 8 B, one cp.async.bulk each; SASS UBLKCP) into an
+// S-slot ring; a slot is released as soon as every loop warp has gathered from it, and the
+// warp then runs its loop's half-bucket twiddle (L1), B-point FFT (radix-2 DIF with xor
+// shuffles, no barrier), |.|^2 > gamma_l and the ballot to bitmap words in registers
+// (Alg. 1 l.9-10; Eq. tpd).  No CTA barrier after the prologue.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 shfl_xor2(float2 v, int m) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+// 2^lgb-point DIF across lanes (x = element lane mod 2^lgb, lgb <= 5): lane p ends with
+// X[brev(p mod 2^lgb)].  stw[q] = W_{2h}^{lane & (h-1)} for h = 16 >> q.
+__device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const float2 (&stw)[5]) {
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int h = 16 >> q;
+    if ((2 * h) > (1 << lgb)) continue;           // warp-uniform
+    const float2 p = shfl_xor2(x, h);
+    x = (lane & h) ? cmul(csub(p, x), stw[q]) : cadd(x, p);
+  }
+  return x;
+}
+
+template <int TAPS, int LPW>
+__global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
+                                                      int l0, int nl, int W, int S, uint32_t* __restrict__ bitmaps,
+                                                      float2* __restrict__ spectra, int64_t bm_stride,
+                                                      int64_t sp_stride) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int N = pd.n[0], B = pd.b[0], lgb = pd.lgb[0];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncw = (blockDim.x >> 5) - 1;            // loop warps; the last warp produces
+  const uint32_t fbytes = (uint32_t)N * 8u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + S;
+  float2* tw = reinterpret_cast<float2*>(smem + 16 * S + 128 - ((16 * S) & 127));  // 128-B aligned
+  unsigned char* ring = reinterpret_cast<unsigned char*>(tw + 128);
+  if (tid < 128) tw[tid] = c_tw128[tid];
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], ncw); }
+    fence_mbar_init();
+  }
+  pdl_enter();
+  __syncthreads();
+  const int64_t nfr = batch > (int64_t)blockIdx.x ? (batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == ncw) {                                // ---- producer: whole frames, S-deep ring
+    if (lane == 0) {
+      for (int64_t fi = 0; fi < nfr; ++fi) {
+        const int s = (int)(fi % S);
+        if (fi >= S) mbar_wait(&empty[s], (uint32_t)(((fi / S) - 1) & 1));
+        mbar_expect_tx(&full[s], fbytes);
+        tma_load_1d(ring + (size_t)s * fbytes, x + (size_t)(blockIdx.x + fi * gridDim.x) * N, fbytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- loop warps: taps, weights and twiddles in registers for the whole kernel
+  const bool shift = pd.shift[0] != 0;
+  uint32_t off[LPW][TAPS];
+  float wt[LPW][TAPS];
+  int lid[LPW];
+#pragma unroll
+  for (int q = 0; q < LPW; ++q) {
+    const int l = warp + q * ncw;
+    lid[q] = l < nl ? l : -1;
+    const LoopDev& lp = pd.loops[l0 + (l < nl ? l : 0)];
+    const float* __restrict__ h = pd.h[0] + (size_t)(l0 + (l < nl ? l : 0)) * N;
+#pragma unroll
+    for (int k = 0; k < TAPS; ++k) {
+      const int i = lane + 32 * k;
+      const uint32_t t = shift ? (uint32_t)(i - W / 2) & (uint32_t)(N - 1) : (uint32_t)i;
+      const uint32_t s = ((uint32_t)lp.sig[0] * t + (uint32_t)lp.tau[0]) & (uint32_t)(N - 1);
+      const bool ok = l < nl && i < W;
+      off[q][k] = ok ? s * 8u : 0u;
+      wt[q][k] = ok ? h[s] : 0.f;
+    }
+  }
+  float2 stw[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int hh = 16 >> q;
+    stw[q] = tw[((lane & (hh - 1)) * 64) / hh];
+  }
+  // half-bucket twiddles e^{-j pi b / B} of the lane's buckets (L1), stage-1 twiddle (B = 64)
+  const float2 sh0 = shift ? tw[(lane & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
+  const float2 sh1 = shift ? tw[((lane + 32) & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
+  const float2 w64 = tw[2 * lane];
+  const int wpl = pd.wpl;
+
+  for (int64_t fi = 0; fi < nfr; ++fi) {
+    const int s = (int)(fi % S);
+    const int64_t frame = blockIdx.x + fi * gridDim.x;
+    mbar_wait(&full[s], (uint32_t)((fi / S) & 1));
+    const unsigned char* xs = ring + (size_t)s * fbytes;
+    float2 acc[LPW][2];
+#pragma unroll
+    for (int q = 0; q < LPW; ++q) {
+      acc[q][0] = acc[q][1] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < TAPS; ++k) {
+        const float2 v = *reinterpret_cast<const float2*>(xs + off[q][k]);
+        float2& a = acc[q][(B == 64) ? (k & 1) : 0];
+        a = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, a);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);          // slot free: the rest is in registers
+
+#pragma unroll
+    for (int q = 0; q < LPW; ++q) {
+      if (lid[q] < 0) continue;                     // warp-uniform
+      const int l = lid[q];
+      const float gamma = pd.loops[l0 + l].gamma;
+      uint32_t* bmw = bitmaps + (size_t)frame * bm_stride + (size_t)l * wpl;
+      float2* sp = spectra ? spectra + (size_t)frame * sp_stride + (size_t)l * pd.btot : nullptr;
+      if (B == 64) {
+        const float2 a = cmul(acc[q][0], sh0), c = cmul(acc[q][1], sh1);
+        float2 u = cadd(a, c), v = cmul(csub(a, c), w64);   // X[2k] <- u, X[2k+1] <- v
+        u = warp_dif(u, lane, 5, stw);
+        v = warp_dif(v, lane, 5, stw);
+        const int kb = 2 * brev(lane, 5);                   // lane p holds X[kb], X[kb + 1]
+        if (sp) { sp[kb] = u; sp[kb + 1] = v; }
+        const int val = (u.x * u.x + u.y * u.y > gamma ? 1 : 0) | (v.x * v.x + v.y * v.y > gamma ? 2 : 0);
+        const int sl = brev(lane >> 1, 5);
+        const int va = __shfl_sync(0xffffffffu, val, sl), vb = __shfl_sync(0xffffffffu, val, sl ^ 1);
+        const uint32_t w0 = __ballot_sync(0xffffffffu, (va >> (lane & 1)) & 1);
+        const uint32_t w1 = __ballot_sync(0xffffffffu, (vb >> (lane & 1)) & 1);
+        if (lane == 0) *reinterpret_cast<uint2*>(bmw) = make_uint2(w0, w1);
+      } else {
+        float2 a = acc[q][0];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+          if (o >= B) a = cadd(a, shfl_xor2(a, o));         // lanes with equal lane mod B
+        a = cmul(a, sh0);
+        a = warp_dif(a, lane, lgb, stw);
+        const int kb = brev(lane & (B - 1), lgb);
+        if (sp && lane < B) sp[kb] = a;
+        const int val = a.x * a.x + a.y * a.y > gamma ? 1 : 0;
+        const int vq = __shfl_sync(0xffffffffu, val, brev(lane & (B - 1), lgb));
+        const uint32_t w0 = __ballot_sync(0xffffffffu, lane < B && vq);
+        if (lane == 0) bmw[0] = w0;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // Split mode, kernel 1: persistent, per-WARP work units (frame, outer residue class kappa,
 // dim-0 chunk c); D in {2, 3}.  Unit u of warp gw = blockIdx.x * nwarps + warp is
 // gw + i * (gridDim.x * nwarps).  Each warp streams its unit's rows through its own TMA ring
@@ -1303,9 +1465,6 @@ RSFT_HD inline MmaLayout mma_layout(int a0c, int a1, int nlast, int blast) {
   return L;
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   // no swizzle, K-major canonical layout; version 1 (sm_100)
   return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
@@ -2144,6 +2303,56 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
   return make_map(m, d_x, 4, dims, str, box);
 }
 
+// D == 1 gather-form fold (k_gather1d): eligible when the taps of a loop fit the registers.
+static int gather1d_taps(const rsft_plan_s* p) {
+  const int64_t W = p->b[0] < p->n[0] ? p->W[0] : p->n[0];
+  if (p->D != 1 || W % 32 != 0 || W > 1024 || p->n[0] * 8 > 64 * 1024) return 0;
+  const int t = (int)(W / 32);
+  return t <= 4 ? 4 : t <= 8 ? 8 : t <= 16 ? 16 : 32;
+}
+
+template <int TAPS, int LPW>
+static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                                     void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride) {
+  auto kern = k_gather1d<TAPS, LPW>;
+  const int ncw = (nl + LPW - 1) / LPW;
+  const int threads = 32 * (ncw + 1);
+  const int W = (int)(p->b[0] < p->n[0] ? p->W[0] : p->n[0]);
+  const size_t fbytes = (size_t)p->n[0] * 8;
+  const char* env_s = getenv("RSFT_G1_STAGES");
+  const char* env_c = getenv("RSFT_G1_CTAS");
+  int ctas = env_c && env_c[0] ? atoi(env_c) : 2;
+  int S = env_s && env_s[0] ? atoi(env_s) : 0;
+  if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048) / fbytes));
+  const size_t smem = 16 * S + 128 + 1024 + S * fbytes;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem), "occupancy");
+  if (s) return s;
+  if (nb < 1) { set_error("k_gather1d: zero occupancy"); return RSFT_E_UNSUPPORTED; }
+  int64_t grid = (int64_t)std::min(nb, ctas) * p->num_sms;
+  if (grid > batch) grid = batch;
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, (unsigned)threads, smem, st, p->dev,
+                                   reinterpret_cast<const float2*>(d_x), batch, l0, nl, W, S, bm,
+                                   reinterpret_cast<float2*>(spectra), bm_stride, sp_stride); le_ != cudaSuccess)
+    return check(le_, "k_gather1d launch");
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_gather1d launch");
+}
+
+static rsft_status launch_gather1d(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                                   void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride) {
+  const int taps = gather1d_taps(p);
+  const int lpw = nl > 16 ? 2 : 1;
+#define RSFT_G1(T) \
+  if (taps == T) return lpw == 1 ? launch_gather1d_t<T, 1>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride) \
+                                 : launch_gather1d_t<T, 2>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride);
+  RSFT_G1(4) RSFT_G1(8) RSFT_G1(16) RSFT_G1(32)
+#undef RSFT_G1
+  return RSFT_E_UNSUPPORTED;
+}
+
 // frame_stride (complex elements between frames), bm_stride (words) and sp_stride (complex)
 // default to the dense layouts; segment mode (rsft_execute_segments) strides over segments.
 template <int LP>
@@ -2152,6 +2361,12 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
                                   int64_t bm_stride = 0, int64_t sp_stride = 0) {
   constexpr FusedCfg F2 = kFused2D, F1 = kFused1D;
   const FusedCfg fc = fused_cfg(p->D);
+  {
+    const char* g1 = getenv("RSFT_NO_GATHER1D");      // read per launch: tests select either kernel
+    if (p->D == 1 && (frame_stride == 0 || frame_stride == p->ntot) && gather1d_taps(p) && !(g1 && g1[0] && g1[0] != '0'))
+      return launch_gather1d(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride ? bm_stride : (int64_t)nl * p->dev.wpl,
+                             sp_stride ? sp_stride : (int64_t)nl * p->btot);
+  }
   auto kern = p->D == 2 ? k_fused<LP, F2.u, F2.stages, F2.threads, F2.ctas> : k_fused<LP, F1.u, F1.stages, F1.threads, F1.ctas>;
   const size_t smem = fused_smem_bytes(p, nl, LP);
   if (bm_stride == 0) bm_stride = (int64_t)nl * p->dev.wpl;

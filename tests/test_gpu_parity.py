@@ -39,6 +39,14 @@ CASES = [
     # name, n, b, loops, extra oracle params, batch, mode
     ("1d_w256_tau", (1024,), (32,), 5, dict(support=(256,), random_tau=True, p_fa=1e-3), 3, "fused"),
     ("1d_b64_full", (2048,), (64,), 3, dict(p_fa=1e-3), 2, "fused"),
+    # D = 1 gather-form fold (k_gather1d): W <= 1024, taps in registers
+    ("1d_g_c1like", (4096,), (64,), 8, dict(support=(512,), random_tau=True, p_fa=1e-3), 5, "fused"),
+    ("1d_g_b16_w128", (2048,), (16,), 6, dict(support=(128,), random_tau=True, p_fa=1e-3), 3, "fused"),
+    ("1d_g_b8_w384", (1024,), (8,), 3, dict(support=(384,), p_fa=1e-3), 3, "fused"),
+    ("1d_g_L20_w1024", (8192,), (64,), 20, dict(support=(1024,), random_tau=True, p_fa=1e-3, mu=15), 2, "fused"),
+    ("1d_g_B_eq_N", (64,), (64,), 4, dict(p_fa=1e-2), 3, "fused"),
+    ("1d_g_B1", (256,), (1,), 3, dict(p_fa=1e-2), 3, "fused"),
+    ("1d_g_b32_dense", (512,), (32,), 7, dict(p_fa=1e-3, random_tau=True), 4, "fused"),
     ("2d_fused", (128, 128), (16, 8), 6, dict(p_fa=1e-4, random_tau=True), 5, "fused"),
     ("2d_fused_mu", (128, 64), (8, 16), 7, dict(p_fa=1e-3, mu=4), 4, "fused"),
     ("2d_fused_mu1", (128, 64), (8, 16), 3, dict(p_fa=1e-3, mu=1), 2, "fused"),
@@ -86,6 +94,31 @@ def test_parity_ffma_fold_on_mma_shapes(case, monkeypatch):
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
     x = frames(wl, batch)
     plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+G1_CASES = [c for c in CASES if c[0].startswith("1d_")]
+
+
+@pytest.mark.parametrize("case", G1_CASES, ids=[c[0] for c in G1_CASES])
+def test_parity_1d_streaming_fold_forced(case, monkeypatch):
+    """The 1-D shapes forced through the streaming fused fold (RSFT_NO_GATHER1D=1, read per
+    launch) instead of the gather-form kernel: both stay parity-green."""
+    monkeypatch.setenv("RSFT_NO_GATHER1D", "1")
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+def test_parity_1d_gather_many_frames_ring_wrap():
+    """c1's shape with many more frames than resident CTAs x ring slots: every CTA wraps its
+    frame ring several times (producer/consumer phases); sampled frames vs the oracle."""
+    wl = synth.C1.with_(batch=3000)
+    x = frames(wl, 3000)
+    plan, res, reps = run_case(wl_params(wl), x, check=[0, 1, 295, 296, 297, 1500, 2999])
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
