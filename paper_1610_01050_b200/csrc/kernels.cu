@@ -936,7 +936,7 @@ __device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const fl
 
 template <int TAPS, int LPW>
 __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
-                                                      int l0, int nl, int W, int S, uint32_t* __restrict__ bitmaps,
+                                                      int l0, int nl, int W, int S, int chunk, uint32_t* __restrict__ bitmaps,
                                                       float2* __restrict__ spectra, int64_t bm_stride,
                                                       int64_t sp_stride) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -959,11 +959,15 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
 
   if (warp == ncw) {                                // ---- producer: whole frames, S-deep ring
     if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;                              // empty-barrier parity of slot s's previous use
       for (int64_t fi = 0; fi < nfr; ++fi) {
-        const int s = (int)(fi % S);
-        if (fi >= S) mbar_wait(&empty[s], (uint32_t)(((fi / S) - 1) & 1));
+        if (fi >= S) mbar_wait(&empty[s], ph);
         mbar_expect_tx(&full[s], fbytes);
-        tma_load_1d(ring + (size_t)s * fbytes, x + (size_t)(blockIdx.x + fi * gridDim.x) * N, fbytes, &full[s]);
+        const char* src = reinterpret_cast<const char*>(x + (size_t)(blockIdx.x + fi * gridDim.x) * N);
+        for (uint32_t o = 0; o < fbytes; o += (uint32_t)chunk)
+          tma_load_1d(ring + (size_t)s * fbytes + o, src + o, (uint32_t)chunk, &full[s]);
+        if (++s == S) { s = 0; if (fi >= 2 * S - 1) ph ^= 1u; }   // use u + 1 waits for parity u & 1
       }
     }
     return;
@@ -974,10 +978,12 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
   uint32_t off[LPW][TAPS];
   float wt[LPW][TAPS];
   int lid[LPW];
+  float gam[LPW];
 #pragma unroll
   for (int q = 0; q < LPW; ++q) {
     const int l = warp + q * ncw;
     lid[q] = l < nl ? l : -1;
+    gam[q] = pd.loops[l0 + (l < nl ? l : 0)].gamma;
     const LoopDev& lp = pd.loops[l0 + (l < nl ? l : 0)];
     const float* __restrict__ h = pd.h[0] + (size_t)(l0 + (l < nl ? l : 0)) * N;
 #pragma unroll
@@ -1002,11 +1008,14 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
   const float2 w64 = tw[2 * lane];
   const int wpl = pd.wpl;
 
+  int s = 0;
+  uint32_t ph = 0;
   for (int64_t fi = 0; fi < nfr; ++fi) {
-    const int s = (int)(fi % S);
     const int64_t frame = blockIdx.x + fi * gridDim.x;
-    mbar_wait(&full[s], (uint32_t)((fi / S) & 1));
+    mbar_wait(&full[s], ph);
     const unsigned char* xs = ring + (size_t)s * fbytes;
+    // even taps k -> bucket lane, odd taps -> bucket lane + 32 (B = 64); for B <= 32 both
+    // parities land in bucket lane mod B and are added below (compile-time register indices)
     float2 acc[LPW][2];
 #pragma unroll
     for (int q = 0; q < LPW; ++q) {
@@ -1014,18 +1023,18 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
 #pragma unroll
       for (int k = 0; k < TAPS; ++k) {
         const float2 v = *reinterpret_cast<const float2*>(xs + off[q][k]);
-        float2& a = acc[q][(B == 64) ? (k & 1) : 0];
-        a = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, a);
+        acc[q][k & 1] = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, acc[q][k & 1]);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);          // slot free: the rest is in registers
+    if (++s == S) { s = 0; ph ^= 1u; }
 
 #pragma unroll
     for (int q = 0; q < LPW; ++q) {
       if (lid[q] < 0) continue;                     // warp-uniform
       const int l = lid[q];
-      const float gamma = pd.loops[l0 + l].gamma;
+      const float gamma = gam[q];
       uint32_t* bmw = bitmaps + (size_t)frame * bm_stride + (size_t)l * wpl;
       float2* sp = spectra ? spectra + (size_t)frame * sp_stride + (size_t)l * pd.btot : nullptr;
       if (B == 64) {
@@ -1042,7 +1051,7 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
         const uint32_t w1 = __ballot_sync(0xffffffffu, (vb >> (lane & 1)) & 1);
         if (lane == 0) *reinterpret_cast<uint2*>(bmw) = make_uint2(w0, w1);
       } else {
-        float2 a = acc[q][0];
+        float2 a = cadd(acc[q][0], acc[q][1]);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
           if (o >= B) a = cadd(a, shfl_xor2(a, o));         // lanes with equal lane mod B
@@ -2111,6 +2120,248 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
 }
 
 // ------------------------------------------------------------------------------------
+// K3 for D == 1 (c1-like: many short frames): one WARP per frame, no CTA barrier.
+// Reverse mapping + accumulation + second stage (Alg. 1 l.11-14) through the
+// hash-lookup form (identity I1, Props. 3-4 P:437-450): abar[i] = sum_l c_l[M_l(i)],
+// M_l(i) = floor(B [sigma_l i]_N / N) (Def. 3).  The L first-stage bitmaps of the frame
+// (<= 64 buckets each) live in registers as 64-bit masks.
+// Candidate mode: a location with abar >= mu has a vote in at least one of ANY L - mu + 1
+// loops, so the candidates are the reverse maps R(k, sigma_l^{-1}) (Def. 4, A = N/B locations
+// each) of the set buckets of loops 0..L-mu; each candidate is tested against all loops
+// (early exit once mu is out of reach) and sets its bit in a per-warp shared bitmap.
+// Used when the candidates are fewer than N/2; otherwise dense mode tests every location.
+// Outputs: detection words, and (list mode) the frame's count + ascending local index list
+// for k_region_write.
+// ------------------------------------------------------------------------------------
+constexpr int kVote1dWarps = 8;
+
+template <int LP>
+__global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const uint32_t* __restrict__ bitmaps,
+                                                               int64_t batch, uint32_t* __restrict__ detect,
+                                                               unsigned long long* __restrict__ rcount,
+                                                               uint32_t* __restrict__ slots, int list_cap) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint32_t v1s[];
+  __shared__ int sig_s[LP], sinv_s[LP];
+  __shared__ int ent_s[kVote1dWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int N = pd.n[0], L = pd.L, mu = pd.mu, wpl = pd.wpl, lga = pd.lga[0];
+  const int A = 1 << lga, nw = N >> 5;
+  const uint32_t nm = (uint32_t)(N - 1);
+  for (int l = threadIdx.x; l < LP; l += blockDim.x) {
+    sig_s[l] = l < L ? pd.loops[l].sig[0] : 0;
+    sinv_s[l] = l < L ? pd.loops[l].sinv[0] : 0;
+  }
+  uint32_t* dw = v1s + (size_t)warp * nw;            // this warp's detection words (kept zero)
+  for (int w = lane; w < nw; w += 32) dw[w] = 0u;
+  __syncthreads();
+  int sg[LP];
+#pragma unroll
+  for (int l = 0; l < LP; ++l) sg[l] = sig_s[l];
+  const int ncand_loops = L - mu + 1;
+
+  const int64_t gw = (int64_t)blockIdx.x * kVote1dWarps + warp, TW = (int64_t)gridDim.x * kVote1dWarps;
+  for (int64_t frame = gw; frame < batch; frame += TW) {
+    // the frame's L masks (bit k <-> bucket k) in registers
+    const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
+    const uint32_t v0 = lane < L * wpl ? __ldg(src + lane) : 0u;
+    const uint32_t v1 = lane + 32 < L * wpl ? __ldg(src + lane + 32) : 0u;
+    uint32_t mlo[LP], mhi[LP];
+#pragma unroll
+    for (int l = 0; l < LP; ++l) {
+      const int a = l * wpl, b = l * wpl + 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, a < 32 ? v0 : v1, a & 31);
+      const uint32_t y = __shfl_sync(0xffffffffu, b < 32 ? v0 : v1, b & 31);
+      mlo[l] = l < L ? x : 0u;
+      mhi[l] = (l < L && wpl > 1) ? y : 0u;
+    }
+    // one vote: bit M_l(i) of loop l
+    auto vote = [&](int l, uint32_t i) -> uint32_t {
+      const uint32_t k = (((uint32_t)sg[l] * i) & nm) >> lga;
+      return ((k < 32 ? mlo[l] : mhi[l]) >> (k & 31)) & 1u;
+    };
+    int ncand = 0;
+#pragma unroll
+    for (int l = 0; l < LP; ++l)
+      if (l < ncand_loops) ncand += __popc(mlo[l]) + __popc(mhi[l]);
+    if (2 * ncand * A <= N) {                         // ---- candidate mode
+      // entries (loop, bucket) of the set buckets of loops 0..L-mu, in this warp's list
+      int base = 0;
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        if (l >= ncand_loops) break;
+        const bool b0 = (mlo[l] >> lane) & 1u, b1 = (mhi[l] >> lane) & 1u;
+        const uint32_t bl0 = __ballot_sync(0xffffffffu, b0), bl1 = __ballot_sync(0xffffffffu, b1);
+        const uint32_t lt = (1u << lane) - 1u;
+        if (b0) ent_s[warp][base + __popc(bl0 & lt)] = (l << 8) | lane;
+        base += __popc(bl0);
+        if (b1) ent_s[warp][base + __popc(bl1 & lt)] = (l << 8) | (lane + 32);
+        base += __popc(bl1);
+      }
+      __syncwarp();
+      const int T = ncand * A;
+      for (int c0 = 0; c0 < T; c0 += 32) {
+        const int c = c0 + lane;
+        const bool valid = c < T;
+        const int e = ent_s[warp][valid ? (c >> lga) : 0];
+        const uint32_t u = ((uint32_t)(e & 255) << lga) | (uint32_t)(c & (A - 1));
+        const uint32_t i = ((uint32_t)sinv_s[e >> 8] * u) & nm;          // Def. 4
+        int cnt = 0;
+        bool alive = valid;
+#pragma unroll
+        for (int l = 0; l < LP; ++l) {
+          if (l >= L) break;
+          cnt += (int)vote(l, i);
+          alive = alive && (cnt + (L - 1 - l) >= mu);
+          if (!__any_sync(0xffffffffu, alive)) break;
+        }
+        if (alive && cnt >= mu) atomicOr(&dw[i >> 5], 1u << (i & 31));
+      }
+    } else {                                          // ---- dense mode
+      for (int w = 0; w < nw; ++w) {
+        const uint32_t i = (uint32_t)(w << 5) | (uint32_t)lane;
+        int cnt = 0;
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          if (l < L) cnt += (int)vote(l, i);
+        const uint32_t word = __ballot_sync(0xffffffffu, cnt >= mu);
+        if (lane == 0) dw[w] = word;
+      }
+    }
+    __syncwarp();
+    // read-out: detection words (coalesced), count, ascending local index list
+    uint32_t* det = detect + (size_t)frame * nw;
+    uint32_t* sl = slots ? slots + (size_t)frame * list_cap : nullptr;
+    int run = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t v = 0u;
+      if (w < nw) { v = dw[w]; dw[w] = 0u; det[w] = v; }
+      const int c = __popc(v);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (sl) {
+        int q = run + incl - c;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          if (q < list_cap) sl[q] = (uint32_t)((w << 5) + bit);
+          ++q;
+        }
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (rcount && lane == 0) rcount[frame] = (unsigned long long)run;
+    __syncwarp();
+  }
+}
+
+// Exclusive scan of the per-region detection counts in place (one CTA of 1024 threads,
+// coalesced tiles of 4096 counts staged in shared memory); total -> *d_count.
+constexpr int kScanTile = 4096;
+__global__ void __launch_bounds__(1024) k_region_scan_tiled(unsigned long long* __restrict__ counts, int64_t n,
+                                                            long long* __restrict__ d_count) {
+  pdl_enter();
+  __shared__ unsigned long long tile[kScanTile];
+  __shared__ long long part[64];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  constexpr int PER = kScanTile / 1024;
+  long long carry = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += kScanTile) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {                  // coalesced load of the tile
+      const int64_t i = t0 + j * 1024 + t;
+      tile[j * 1024 + t] = i < n ? __ldcg(counts + i) : 0ull;
+    }
+    __syncthreads();
+    long long v[PER], s = 0;                          // thread t scans tile[t*PER .. +PER)
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { v[j] = (long long)tile[t * PER + j]; s += v[j]; }
+    long long incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += u;
+    }
+    if (lane == 31) part[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const long long w = part[lane];
+      long long wi = w;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const long long u = __shfl_up_sync(0xffffffffu, wi, off);
+        if (lane >= off) wi += u;
+      }
+      part[32 + lane] = wi - w;
+      if (lane == 31) part[0] = wi;                   // tile total (part[0] already consumed)
+    }
+    __syncthreads();
+    long long run = carry + part[32 + wid] + incl - s;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { tile[t * PER + j] = (unsigned long long)run; run += v[j]; }
+    carry += part[0];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int64_t i = t0 + j * 1024 + t;
+      if (i < n) counts[i] = tile[j * 1024 + t];
+    }
+    __syncthreads();
+  }
+  if (t == 0) *d_count = carry;
+}
+
+// Warp per region (regions of <= 32 x kRwWarpWords detection words): copies the vote's
+// region-local index list, or -- when the list overflowed -- re-reads the region's detection
+// words in order (warp prefix sums), writing flat indices at the region's offset.
+__global__ void __launch_bounds__(256) k_region_write_warp(const uint32_t* __restrict__ det, int64_t rwords,
+                                                            const unsigned long long* __restrict__ offsets,
+                                                            const long long* __restrict__ d_count, int64_t nregions,
+                                                            const uint32_t* __restrict__ slots,
+                                                            long long* __restrict__ idx, int64_t capacity,
+                                                            int list_cap) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= nregions) return;
+  const long long run0 = (long long)offsets[r];
+  const long long n = (r + 1 < nregions ? (long long)offsets[r + 1] : *d_count) - run0;
+  const long long g0 = r * rwords * 32;
+  if (slots && n <= list_cap) {
+    const uint32_t* sl = slots + (size_t)r * list_cap;
+    for (long long i = lane; i < n; i += 32)
+      if (run0 + i < capacity) idx[run0 + i] = g0 + (long long)sl[i];
+    return;
+  }
+  const uint32_t* src = det + r * rwords;
+  long long run = run0;
+  for (int64_t w0 = 0; w0 < rwords; w0 += 32) {
+    const int64_t w = w0 + lane;
+    uint32_t v = w < rwords ? src[w] : 0u;
+    const int c = __popc(v);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    long long q = run + incl - c;
+    while (v) {
+      const int bit = __ffs(v) - 1;
+      v &= v - 1;
+      if (q < capacity) idx[q] = g0 + (w << 5) + bit;
+      ++q;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K4 compaction: detection bitmap -> ascending flat indices, single pass.  Chunks of
 // kChunkWords words are taken in ticket order (atomic counter), so a chunk's predecessors
 // are always resident or done; each chunk publishes its popcount (flag A) and, once its
@@ -2303,13 +2554,6 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
   return make_map(m, d_x, 4, dims, str, box);
 }
 
-// D == 1 gather-form fold (k_gather1d): eligible when the taps of a loop fit the registers.
-static int gather1d_taps(const rsft_plan_s* p) {
-  const int64_t W = p->b[0] < p->n[0] ? p->W[0] : p->n[0];
-  if (p->D != 1 || W % 32 != 0 || W > 1024 || p->n[0] * 8 > 64 * 1024) return 0;
-  const int t = (int)(W / 32);
-  return t <= 4 ? 4 : t <= 8 ? 8 : t <= 16 ? 16 : 32;
-}
 
 template <int TAPS, int LPW>
 static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
@@ -2325,6 +2569,9 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   int S = env_s && env_s[0] ? atoi(env_s) : 0;
   if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048) / fbytes));
   const size_t smem = 16 * S + 128 + 1024 + S * fbytes;
+  const char* env_k = getenv("RSFT_G1_CHUNK");        // bytes per bulk copy (divides the frame)
+  int chunk = env_k && env_k[0] ? atoi(env_k) : (int)std::min<size_t>(fbytes, 8192);
+  if (chunk <= 0 || chunk % 16 || fbytes % chunk) chunk = (int)fbytes;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   int nb = 0;
@@ -2334,7 +2581,7 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   int64_t grid = (int64_t)std::min(nb, ctas) * p->num_sms;
   if (grid > batch) grid = batch;
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, (unsigned)threads, smem, st, p->dev,
-                                   reinterpret_cast<const float2*>(d_x), batch, l0, nl, W, S, bm,
+                                   reinterpret_cast<const float2*>(d_x), batch, l0, nl, W, S, chunk, bm,
                                    reinterpret_cast<float2*>(spectra), bm_stride, sp_stride); le_ != cudaSuccess)
     return check(le_, "k_gather1d launch");
   p->last_launches += 1;
@@ -2648,8 +2895,36 @@ static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t 
   return RSFT_E_UNSUPPORTED;
 }
 
+// D == 1 warp-per-frame vote (k_vote1d): full range, no abar output, frame words in smem.
+static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
+  const char* off = getenv("RSFT_NO_VOTE1D");        // read per launch: tests select either kernel
+  if (off && off[0] && off[0] != '0') return false;
+  return p->D == 1 && !counts && p->n[0] >= 32 && p->n[0] <= 32768;
+}
+
+static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
+                                 unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
+  const size_t smem = (size_t)kVote1dWarps * (p->n[0] / 32) * 4;
+  auto kern = p->L <= 8 ? k_vote1d<8> : p->L <= 16 ? k_vote1d<16> : k_vote1d<32>;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * kVote1dWarps, smem), "occupancy");
+  if (s) return s;
+  if (nb < 1) { set_error("k_vote1d: zero occupancy"); return RSFT_E_UNSUPPORTED; }
+  int64_t grid = (int64_t)nb * p->num_sms;
+  const int64_t need = (batch + kVote1dWarps - 1) / kVote1dWarps;
+  if (grid > need) grid = need;
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, 32 * kVote1dWarps, smem, st, p->dev, bm, batch, det, rcount, slots,
+                                   list_cap); le_ != cudaSuccess)
+    return check(le_, "k_vote1d launch");
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_vote1d launch");
+}
+
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st) {
+  if (vote1d_ok(p, counts)) return launch_vote1d(p, bm, batch, det, nullptr, nullptr, 0, st);
   return launch_vote_mode<false, false>(p, bm, batch, d0b, d0e, det, counts, st);
 }
 
@@ -2664,16 +2939,27 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
   const int64_t cw = (W % 8 == 0 && mode != 2) ? 8 : W % 4 == 0 ? 4 : W % 2 == 0 ? 2 : 1;
   const int64_t rows = D == 3 ? p->n[1] : D == 2 ? n0 : 1;
-  const bool list = p->dev.region_slots && rows * (W / cw) <= (int64_t)kListIpt * kThreads;
-  rsft_status s = list ? launch_vote_mode<true, true>(p, bm, batch, 0, n0, det, nullptr, st)
-                       : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);
-  if (s) return s;
+  const bool v1 = vote1d_ok(p, nullptr);
+  const bool list = p->dev.region_slots && (v1 || rows * (W / cw) <= (int64_t)kListIpt * kThreads);
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
+  if (nregions > p->dev.region_capacity) return RSFT_E_WORKSPACE;
+  rsft_status s = v1 ? launch_vote1d(p, bm, batch, det, p->dev.region_state, list ? p->dev.region_slots : nullptr,
+                                     (int)p->dev.list_cap, st)
+                : list ? launch_vote_mode<true, true>(p, bm, batch, 0, n0, det, nullptr, st)
+                       : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);
+  if (s) return s;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
-  if (cudaError_t le_ = pdl_launch(k_region_scan, 1, 1024, 0, st, p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
+  if (cudaError_t le_ = pdl_launch(k_region_scan_tiled, 1, 1024, 0, st, p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
     return check(le_, "k_region_scan launch");
-  if (cudaError_t le_ = pdl_launch(k_region_write, (unsigned)nregions, kThreads, 0, st, det, rwords, p->dev.region_state,
+  // small regions (c1: one 4096-location frame, c3: one dim-0 plane): a warp per region
+  const bool warp_writer = rwords <= 1024;
+  if (warp_writer) {
+    if (cudaError_t le_ = pdl_launch(k_region_write_warp, (unsigned)((nregions + 7) / 8), 256, 0, st, det, rwords, p->dev.region_state,
+                                     reinterpret_cast<long long*>(d_count), nregions, list ? p->dev.region_slots : nullptr,
+                                     reinterpret_cast<long long*>(idx), capacity, (int)p->dev.list_cap); le_ != cudaSuccess)
+      return check(le_, "k_region_write_warp launch");
+  } else if (cudaError_t le_ = pdl_launch(k_region_write, (unsigned)nregions, kThreads, 0, st, det, rwords, p->dev.region_state,
                                                           reinterpret_cast<long long*>(d_count), nregions,
                                                           list ? p->dev.region_slots : nullptr,
                                                           reinterpret_cast<long long*>(idx), capacity, (int)p->dev.list_cap); le_ != cudaSuccess)

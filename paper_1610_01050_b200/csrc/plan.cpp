@@ -294,11 +294,22 @@ int split_lg_chunks(const rsft_plan_s* p, int64_t batch, int nl, int64_t a0_coun
   return best;
 }
 
+// D == 1 gather-form fold (k_gather1d): eligible when a loop's W taps fit the registers
+// (W <= 1024) and a whole frame fits a shared-memory ring slot; returns the per-lane tap
+// count the kernel is instantiated for, or 0.
+int gather1d_taps(const rsft_plan_s* p) {
+  const int64_t W = p->b[0] < p->n[0] ? p->W[0] : p->n[0];
+  if (p->D != 1 || W % 32 != 0 || W > 1024 || p->n[0] * 8 > 64 * 1024) return 0;
+  const int t = (int)(W / 32);
+  return t <= 4 ? 4 : t <= 8 ? 8 : t <= 16 ? 16 : 32;
+}
+
 int resolve_mode(const rsft_plan_s* p, int64_t batch) {
   const int64_t nlast = p->n[p->D - 1];
   const int lp = loop_pad(p->L);
   bool fused_ok = p->D <= 2 && nlast >= 64 && p->btot <= 8 * kThreads &&
-                  fused_smem_bytes(p, p->L, lp) <= (fused_cfg(p->D).ctas == 1 ? 220 : 110) * 1024;
+                  (fused_smem_bytes(p, p->L, lp) <= (fused_cfg(p->D).ctas == 1 ? 220 : 110) * 1024 ||
+                   gather1d_taps(p) > 0);
   // split mode chunks dim 0 as far as needed to fit the per-warp tables (launch_split_fold_t)
   const int64_t amin = p->D == 3 ? 1 : std::min<int64_t>(p->a[0], (int64_t)kUSplit * (nlast >= 64 ? 1 : 64 / nlast));
   bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp, amin) <= 220 * 1024;

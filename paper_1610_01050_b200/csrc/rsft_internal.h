@@ -176,6 +176,7 @@ namespace rsft {
 rsft_status rebuild_tables(rsft_plan_s* p);
 void layout_workspace(rsft_plan_s* p);
 int resolve_mode(const rsft_plan_s* p, int64_t batch);
+int gather1d_taps(const rsft_plan_s* p);
 int loop_pad(int nl);
 size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
 inline FusedCfg fused_cfg(int D) { return D == 2 ? kFused2D : kFused1D; }
