@@ -283,6 +283,16 @@ __device__ __forceinline__ void tma_load_4d_lane0(int lane, void* dst, uint64_t 
                : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d_lane0(int lane, void* dst, uint64_t tmap, int c0, int c1, int c2, int c3,
+                                                  int c4, uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0;\n\t"
+               "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%8], %9;\n\t"
+               "@p cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%1], [%2, {%3, %4, %5, %6, %7}], [%8];\n\t}"
+               :: "r"(lane), "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+                  "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
@@ -1115,6 +1125,10 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   const int AR = D == 3 ? A1 : A0c;                  // run length: a1 (D == 3) or the chunk's a0
   const int nb_run = AR > BR ? AR / BR : 1;
   const int per_a0 = D == 3 ? A0c : 1;               // a0 groups per segment
+  // D == 3 with short a1 runs (A1 < BR, e.g. c3: A1 = 8, 32-row boxes): each box spans
+  // G = BR / A1 whole a0 groups (5-D tensor map {N_last, r1, a1, r0, frame a0_count + a0}), so
+  // no box row is out of bounds (the 4-D map zero-filled BR - A1 rows per box and folded them)
+  const int MG = split_multi_g(D, LP, A1, A0c, RPW, nseg);
   const int plane_stride = a0_count * B0;            // dim-0 planes per frame in this launch
 
   const SplitWarpLayout wl = split_warp_layout(D, LP, nl, A0c, A1, blast, nseg, RPW);
@@ -1245,6 +1259,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
     p_c1 = D == 3 ? t.r1 : t.r0;
     p_c2b = D == 3 ? 0 : t.chunk * A0c;
     p_c3b = D == 3 ? t.frame * plane_stride + t.r0 + B0 * t.chunk * A0c : t.frame;
+    if (MG) { p_c2b = t.r0; p_c3b = t.frame * a0_count + t.chunk * A0c; }   // 5-D: (0, r1, 0, r0, a0)
     p_c2 = p_c2b;
     p_c3 = p_c3b;
     p_rb = p_a0l = p_seg = 0;
@@ -1253,6 +1268,15 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   const uint64_t tmap_ptr = reinterpret_cast<uint64_t>(&tmap);
   auto issue_next = [&]() {                         // run by all lanes; lane 0 issues
     if (p_ui >= my_units) return;
+    if (MG) {
+      tma_load_5d_lane0(lane, ring + (size_t)p_st * U * 32, tmap_ptr, 0, p_c1, 0, p_c2, p_c3, &bars[p_st],
+                        (uint32_t)U * 512u);
+      if (++p_st == S) p_st = 0;
+      p_c3 += MG;
+      if (++p_a0l < A0c / MG) return;
+      if (++p_ui < my_units) p_unit();
+      return;
+    }
     tma_load_4d_lane0(lane, ring + (size_t)p_st * U * 32, tmap_ptr, p_c0, p_c1, p_c2, p_c3, &bars[p_st],
                       (uint32_t)U * 512u);
     if (++p_st == S) p_st = 0;
@@ -1283,7 +1307,44 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
     for (int seg = 0; seg < nseg; ++seg) {
 #pragma unroll
       for (int l = 0; l < LP; ++l) acc[l][0] = acc[l][1] = make_float2(0.f, 0.f);
-      for (int a0l = 0; a0l < per_a0; ++a0l) {
+      if constexpr (LP <= 16) {
+        if (MG) {                                    // boxes of MG whole a0 groups (A1 rows each)
+          const int UA = A1 / RPW;                   // ring slots per a0 group
+          const float* h1b = hcur + (A0c + lane_row) * LP;
+          for (int bx = 0; bx < A0c / MG; ++bx) {
+            issue_next();
+            mbar_wait(&bars[c_st], c_ph);
+            const float4* buf = ring + (size_t)c_st * U * 32;
+            for (int g = 0; g < MG; ++g) {
+              float2 inn[LP][2];
+              const float4* gb = buf + g * UA * 32;
+              switch (UA) {                          // warp-uniform; h1 rows a1 = u RPW + lane_row
+                case 1: { const float* w[1] = {h1b}; fold_group<LP, 1, true>(inn, gb, lane, w); break; }
+                case 2: { const float* w[2] = {h1b, h1b + RPW * LP}; fold_group<LP, 2, true>(inn, gb, lane, w); break; }
+                case 4: { const float* w[4] = {h1b, h1b + RPW * LP, h1b + 2 * RPW * LP, h1b + 3 * RPW * LP};
+                          fold_group<LP, 4, true>(inn, gb, lane, w); break; }
+                default: { const float* w[8];
+#pragma unroll
+                           for (int u = 0; u < 8; ++u) w[u] = h1b + u * RPW * LP;
+                           fold_group<LP, 8, true>(inn, gb, lane, w); break; }
+              }
+              const float2* h0r = reinterpret_cast<const float2*>(hcur + (bx * MG + g) * LP);
+#pragma unroll
+              for (int l2 = 0; l2 < LP / 2; ++l2) {
+                const float2 w = h0r[l2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  acc[2 * l2][e] = __ffma2_rn(make_float2(w.x, w.x), inn[2 * l2][e], acc[2 * l2][e]);
+                  acc[2 * l2 + 1][e] = __ffma2_rn(make_float2(w.y, w.y), inn[2 * l2 + 1][e], acc[2 * l2 + 1][e]);
+                }
+              }
+            }
+            __syncwarp();
+            if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
+          }
+        }
+      }
+      for (int a0l = 0; a0l < (MG ? 0 : per_a0); ++a0l) {
         // D == 3: rows (a0, a1) carry h0[a0][l] h1[a1][l] (I3).  LP <= 16: fold the a1 rows
         // with h1 into `inn`, then acc += h0[a0] * inn (two-level, +1/A1 FMAs); LP > 16: the
         // product weight is formed per row (registers do not hold two accumulator sets).
@@ -2011,43 +2072,6 @@ __global__ void __launch_bounds__(kThreads, RSFT_VOTE_CTAS) k_vote(PlanDev pd, c
   }
 }
 
-// Exclusive scan of the per-region detection counts (one CTA); total -> *d_count.
-__global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* __restrict__ counts, int64_t n,
-                                                      long long* __restrict__ d_count) {
-  pdl_enter();
-  __shared__ long long part[64];
-  const int t = threadIdx.x;
-  const int64_t per = (n + 1023) / 1024;
-  const int64_t b = t * per, e = b + per < n ? b + per : n;
-  long long s = 0;
-#pragma unroll 16
-  for (int64_t i = b; i < e; ++i) s += (long long)__ldcg(counts + i);   // independent loads in flight
-  // block exclusive scan: warp shuffles, then the 32 warp totals by warp 0 (two barriers)
-  const int lane = t & 31, wid = t >> 5;
-  long long incl = s;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const long long v = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += v;
-  }
-  if (lane == 31) part[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    long long w = part[lane], wi = w;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const long long v = __shfl_up_sync(0xffffffffu, wi, off);
-      if (lane >= off) wi += v;
-    }
-    part[32 + lane] = wi - w;                        // exclusive warp offsets
-    if (lane == 31) *d_count = wi;
-  }
-  __syncthreads();
-  long long run = part[32 + wid] + incl - s;
-#pragma unroll 16
-  for (int64_t i = b; i < e; ++i) { long long v = (long long)__ldcg(counts + i); counts[i] = (unsigned long long)run; run += v; }
-}
-
 // One CTA per region: each thread owns 32 consecutive detection words of a pass of
 // 32 x blockDim words (8 x 16-B loads in flight), one block scan of the per-thread counts
 // gives every thread its output position in word order; ascending indices are staged in
@@ -2260,60 +2284,90 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
   }
 }
 
-// Exclusive scan of the per-region detection counts in place (one CTA of 1024 threads,
-// coalesced tiles of 4096 counts staged in shared memory); total -> *d_count.
+// Exclusive scan of the per-region detection counts in place, in two fully parallel passes
+// over tiles of kScanTile counts: k_scan_tiles writes each tile's total; k_scan_apply sums the
+// totals of the preceding tiles (block reduce), scans its own tile (coalesced, staged in
+// shared memory) and writes the offsets; the last tile writes the grand total to *d_count.
 constexpr int kScanTile = 4096;
-__global__ void __launch_bounds__(1024) k_region_scan_tiled(unsigned long long* __restrict__ counts, int64_t n,
-                                                            long long* __restrict__ d_count) {
+__global__ void __launch_bounds__(1024) k_scan_tiles(const unsigned long long* __restrict__ counts, int64_t n,
+                                                     long long* __restrict__ tile_sum) {
+  pdl_enter();
+  __shared__ long long red[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
+  long long s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanTile / 1024; ++j) {
+    const int64_t i = t0 + j * 1024 + t;
+    if (i < n) s += (long long)__ldcg(counts + i);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[wid] = s;
+  __syncthreads();
+  if (wid == 0) {
+    long long v = red[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) tile_sum[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_apply(unsigned long long* __restrict__ counts, int64_t n,
+                                                     const long long* __restrict__ tile_sum,
+                                                     long long* __restrict__ d_count) {
   pdl_enter();
   __shared__ unsigned long long tile[kScanTile];
   __shared__ long long part[64];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   constexpr int PER = kScanTile / 1024;
+  const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {                    // coalesced load of the tile
+    const int64_t i = t0 + j * 1024 + t;
+    tile[j * 1024 + t] = i < n ? __ldcg(counts + i) : 0ull;
+  }
+  long long before = 0;                              // totals of the preceding tiles
+  for (int64_t q = t; q < blockIdx.x; q += 1024) before += __ldcg(tile_sum + q);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+  if (lane == 0) part[wid] = before;
+  __syncthreads();
   long long carry = 0;
-  for (int64_t t0 = 0; t0 < n; t0 += kScanTile) {
+  for (int w = 0; w < 32; ++w) carry += part[w];
+  long long v[PER], s = 0;                           // thread t scans tile[t PER .. + PER)
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {                  // coalesced load of the tile
-      const int64_t i = t0 + j * 1024 + t;
-      tile[j * 1024 + t] = i < n ? __ldcg(counts + i) : 0ull;
-    }
-    __syncthreads();
-    long long v[PER], s = 0;                          // thread t scans tile[t*PER .. +PER)
+  for (int j = 0; j < PER; ++j) { v[j] = (long long)tile[t * PER + j]; s += v[j]; }
+  long long incl = s;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) { v[j] = (long long)tile[t * PER + j]; s += v[j]; }
-    long long incl = s;
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += u;
+  }
+  __syncthreads();                                   // part[] reads of the carry are done
+  if (lane == 31) part[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const long long w = part[lane];
+    long long wi = w;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const long long u = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += u;
+      const long long u = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += u;
     }
-    if (lane == 31) part[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      const long long w = part[lane];
-      long long wi = w;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const long long u = __shfl_up_sync(0xffffffffu, wi, off);
-        if (lane >= off) wi += u;
-      }
-      part[32 + lane] = wi - w;
-      if (lane == 31) part[0] = wi;                   // tile total (part[0] already consumed)
-    }
-    __syncthreads();
-    long long run = carry + part[32 + wid] + incl - s;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) { tile[t * PER + j] = (unsigned long long)run; run += v[j]; }
-    carry += part[0];
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int64_t i = t0 + j * 1024 + t;
-      if (i < n) counts[i] = tile[j * 1024 + t];
-    }
-    __syncthreads();
+    part[32 + lane] = wi - w;
+    if (lane == 31 && blockIdx.x == gridDim.x - 1) *d_count = carry + wi;
   }
-  if (t == 0) *d_count = carry;
+  __syncthreads();
+  long long run = carry + part[32 + wid] + incl - s;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { tile[t * PER + j] = (unsigned long long)run; run += v[j]; }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int64_t i = t0 + j * 1024 + t;
+    if (i < n) counts[i] = tile[j * 1024 + t];
+  }
 }
 
 // Warp per region (regions of <= 32 x kRwWarpWords detection words): copies the vote's
@@ -2695,7 +2749,21 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
   const size_t smem = split_smem_bytes(p, nl, LP, a0_count >> lg);
   if (smem > 227 * 1024) { set_error("k_split_fold: tables beyond shared memory"); return RSFT_E_UNSUPPORTED; }
   CUtensorMap tmap;
-  rsft_status s = fold_map(p, d_x, batch, a0_count * p->b[0], &tmap, kUSplit);
+  const int rpw = p->n[p->D - 1] >= 64 ? 1 : (int)(64 / p->n[p->D - 1]);
+  const int nseg = rpw == 1 ? (int)(p->n[p->D - 1] >> 6) : 1;
+  const int mg = split_multi_g(p->D, LP, p->D == 3 ? (int)p->a[1] : 1, (int)(a0_count >> lg), rpw, nseg);
+  rsft_status s;
+  if (mg) {                // 5-D map {N_last, r1, a1, r0, frame a0_count + a0}, box {N_last, 1, A1, 1, mg}
+    const uint64_t e = 8, nl = (uint64_t)p->n[2];
+    cuuint64_t dims[5] = {(cuuint64_t)nl, (cuuint64_t)p->b[1], (cuuint64_t)p->a[1], (cuuint64_t)p->b[0],
+                          (cuuint64_t)(batch * a0_count)};
+    cuuint64_t str[4] = {nl * e, (cuuint64_t)(p->b[1] * nl * e), (cuuint64_t)(p->n[1] * nl * e),
+                         (cuuint64_t)(p->b[0] * p->n[1] * nl * e)};
+    cuuint32_t box[5] = {(cuuint32_t)nl, 1, (cuuint32_t)p->a[1], 1, (cuuint32_t)mg};
+    s = make_map(&tmap, d_x, 5, dims, str, box);
+  } else {
+    s = fold_map(p, d_x, batch, a0_count * p->b[0], &tmap, kUSplit);
+  }
   if (s) return s;
   s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
@@ -2950,8 +3018,17 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
                        : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);
   if (s) return s;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
-  if (cudaError_t le_ = pdl_launch(k_region_scan_tiled, 1, 1024, 0, st, p->dev.region_state, nregions, reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
-    return check(le_, "k_region_scan launch");
+  {
+    const int64_t ntiles = (nregions + kScanTile - 1) / kScanTile;
+    if (ntiles > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;
+    long long* tsum = p->dev.chunk_counts;
+    if (cudaError_t le_ = pdl_launch(k_scan_tiles, (unsigned)ntiles, 1024, 0, st, p->dev.region_state, nregions, tsum); le_ != cudaSuccess)
+      return check(le_, "k_scan_tiles launch");
+    if (cudaError_t le_ = pdl_launch(k_scan_apply, (unsigned)ntiles, 1024, 0, st, p->dev.region_state, nregions, tsum,
+                                     reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
+      return check(le_, "k_scan_apply launch");
+    p->last_launches += 1;
+  }
   // small regions (c1: one 4096-location frame, c3: one dim-0 plane): a warp per region
   const bool warp_writer = rwords <= 1024;
   if (warp_writer) {

@@ -92,6 +92,16 @@ RSFT_HD inline SplitWarpLayout split_warp_layout(int D, int lpad, int nl, int a0
   return w;
 }
 
+// Split fold, D == 3 with short a1 runs: a TMA box of BR = kUSplit * rpw rows spans
+// G = BR / A1 whole a0 groups (returns G, or 0 when the 4-D a1-run boxes are used).
+RSFT_HD inline int split_multi_g(int D, int lpad, int a1, int a0c, int rpw, int nseg) {
+  const int br = kUSplit * rpw;
+  if (D != 3 || lpad > 16 || nseg != 1 || a1 >= br || br % a1 != 0 || a1 % rpw != 0) return 0;
+  const int g = br / a1;
+  if (a1 / rpw > 8 || a0c % g != 0) return 0;
+  return g;
+}
+
 // Per-loop device record: schedule + threshold (Def. 1; Eq. tpd).
 struct LoopDev {
   int32_t sig[kMaxDim];
