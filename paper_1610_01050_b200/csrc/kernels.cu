@@ -2151,8 +2151,10 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
 // (<= 64 buckets each) live in registers as 64-bit masks.
 // Candidate mode: a location with abar >= mu has a vote in at least one of ANY L - mu + 1
 // loops, so the candidates are the reverse maps R(k, sigma_l^{-1}) (Def. 4, A = N/B locations
-// each) of the set buckets of loops 0..L-mu; each candidate is tested against all loops
-// (early exit once mu is out of reach) and sets its bit in a per-warp shared bitmap.
+// each) of the set buckets of the L - mu + 1 loops with the fewest set buckets; for mu = L a
+// candidate must also vote in a filter loop (one cheap test), the survivors are compacted
+// into a per-warp queue and tested against all loops 32 at a time, setting their bits in a
+// per-warp shared bitmap.
 // Used when the candidates are fewer than N/2; otherwise dense mode tests every location.
 // Outputs: detection words, and (list mode) the frame's count + ascending local index list
 // for k_region_write.
@@ -2168,10 +2170,11 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
   extern __shared__ __align__(16) uint32_t v1s[];
   __shared__ int sig_s[LP], sinv_s[LP];
   __shared__ int ent_s[kVote1dWarps][32];
+  __shared__ uint32_t q_s[kVote1dWarps][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int N = pd.n[0], L = pd.L, mu = pd.mu, wpl = pd.wpl, lga = pd.lga[0];
   const int A = 1 << lga, nw = N >> 5;
-  const uint32_t nm = (uint32_t)(N - 1);
+  const uint32_t nm = (uint32_t)(N - 1), lt = (1u << lane) - 1u;
   for (int l = threadIdx.x; l < LP; l += blockDim.x) {
     sig_s[l] = l < L ? pd.loops[l].sig[0] : 0;
     sinv_s[l] = l < L ? pd.loops[l].sinv[0] : 0;
@@ -2182,47 +2185,80 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
   int sg[LP];
 #pragma unroll
   for (int l = 0; l < LP; ++l) sg[l] = sig_s[l];
-  const int ncand_loops = L - mu + 1;
+  const int ncl = L - mu + 1;                        // candidate loops needed
+  const bool vec = ((L * wpl) & 3) == 0;
+  uint32_t* q = q_s[warp];
 
   const int64_t gw = (int64_t)blockIdx.x * kVote1dWarps + warp, TW = (int64_t)gridDim.x * kVote1dWarps;
   for (int64_t frame = gw; frame < batch; frame += TW) {
-    // the frame's L masks (bit k <-> bucket k) in registers
+    // the frame's L masks (bit k <-> bucket k) in registers (same address on every lane)
     const uint32_t* src = bitmaps + (size_t)frame * L * wpl;
-    const uint32_t v0 = lane < L * wpl ? __ldg(src + lane) : 0u;
-    const uint32_t v1 = lane + 32 < L * wpl ? __ldg(src + lane + 32) : 0u;
     uint32_t mlo[LP], mhi[LP];
+    if (vec && wpl == 2) {
 #pragma unroll
-    for (int l = 0; l < LP; ++l) {
-      const int a = l * wpl, b = l * wpl + 1;
-      const uint32_t x = __shfl_sync(0xffffffffu, a < 32 ? v0 : v1, a & 31);
-      const uint32_t y = __shfl_sync(0xffffffffu, b < 32 ? v0 : v1, b & 31);
-      mlo[l] = l < L ? x : 0u;
-      mhi[l] = (l < L && wpl > 1) ? y : 0u;
+      for (int l = 0; l < LP; l += 2) {
+        const uint4 v = l < L ? __ldg(reinterpret_cast<const uint4*>(src) + (l >> 1)) : make_uint4(0u, 0u, 0u, 0u);
+        mlo[l] = v.x; mhi[l] = v.y;
+        if (l + 1 < LP) { mlo[l + 1] = l + 1 < L ? v.z : 0u; mhi[l + 1] = l + 1 < L ? v.w : 0u; }
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        mlo[l] = l < L ? __ldg(src + l * wpl) : 0u;
+        mhi[l] = (l < L && wpl > 1) ? __ldg(src + l * wpl + 1) : 0u;
+      }
     }
-    // one vote: bit M_l(i) of loop l
+    // one vote: bit M_l(i) of loop l (Def. 3)
     auto vote = [&](int l, uint32_t i) -> uint32_t {
       const uint32_t k = (((uint32_t)sg[l] * i) & nm) >> lga;
       return ((k < 32 ? mlo[l] : mhi[l]) >> (k & 31)) & 1u;
     };
+    // candidate loops: the ncl loops with the fewest set buckets (bit l of cmask); for
+    // mu = L also a filter loop lf (fewest set buckets among the others)
+    uint32_t cmask = 0u;
     int ncand = 0;
-#pragma unroll
-    for (int l = 0; l < LP; ++l)
-      if (l < ncand_loops) ncand += __popc(mlo[l]) + __popc(mhi[l]);
-    if (2 * ncand * A <= N) {                         // ---- candidate mode
-      // entries (loop, bucket) of the set buckets of loops 0..L-mu, in this warp's list
-      int base = 0;
+    for (int t = 0; t < ncl; ++t) {
+      int best = 1 << 30, bl = 0;
 #pragma unroll
       for (int l = 0; l < LP; ++l) {
-        if (l >= ncand_loops) break;
+        const int pc = __popc(mlo[l]) + __popc(mhi[l]);
+        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; bl = l; }
+      }
+      cmask |= 1u << bl;
+      ncand += best;
+    }
+    int lf = -1;
+    if (mu == L && L > 1) {
+      int best = 1 << 30;
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        const int pc = __popc(mlo[l]) + __popc(mhi[l]);
+        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; lf = l; }
+      }
+    }
+    if (2 * ncand * A <= N) {                         // ---- candidate mode
+      int base = 0;                                   // entries (loop, bucket), ascending loops
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        if (!((cmask >> l) & 1u)) continue;
         const bool b0 = (mlo[l] >> lane) & 1u, b1 = (mhi[l] >> lane) & 1u;
         const uint32_t bl0 = __ballot_sync(0xffffffffu, b0), bl1 = __ballot_sync(0xffffffffu, b1);
-        const uint32_t lt = (1u << lane) - 1u;
         if (b0) ent_s[warp][base + __popc(bl0 & lt)] = (l << 8) | lane;
         base += __popc(bl0);
         if (b1) ent_s[warp][base + __popc(bl1 & lt)] = (l << 8) | (lane + 32);
         base += __popc(bl1);
       }
       __syncwarp();
+      // full test of up to 32 queued locations (lane per location), all loops
+      auto drain = [&](int n) {
+        const uint32_t i = lane < n ? q[lane] : 0u;
+        int cnt = 0;
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          if (l < L) cnt += (int)vote(l, i);
+        if (lane < n && cnt >= mu) atomicOr(&dw[i >> 5], 1u << (i & 31));
+      };
+      int qn = 0;
       const int T = ncand * A;
       for (int c0 = 0; c0 < T; c0 += 32) {
         const int c = c0 + lane;
@@ -2230,17 +2266,26 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
         const int e = ent_s[warp][valid ? (c >> lga) : 0];
         const uint32_t u = ((uint32_t)(e & 255) << lga) | (uint32_t)(c & (A - 1));
         const uint32_t i = ((uint32_t)sinv_s[e >> 8] * u) & nm;          // Def. 4
-        int cnt = 0;
-        bool alive = valid;
+        // mu = L: a location needs the filter loop's vote too (cheap pre-test, then queue)
+        bool pass = valid;
 #pragma unroll
-        for (int l = 0; l < LP; ++l) {
-          if (l >= L) break;
-          cnt += (int)vote(l, i);
-          alive = alive && (cnt + (L - 1 - l) >= mu);
-          if (!__any_sync(0xffffffffu, alive)) break;
+        for (int l = 0; l < LP; ++l)
+          if (l == lf) pass = pass && vote(l, i);
+        const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+        if (pass) q[qn + __popc(bal & lt)] = i;
+        qn += __popc(bal);
+        __syncwarp();
+        if (qn >= 32) {
+          drain(32);
+          __syncwarp();
+          const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
+          __syncwarp();
+          if (lane + 32 < qn) q[lane] = rest;
+          qn -= 32;
+          __syncwarp();
         }
-        if (alive && cnt >= mu) atomicOr(&dw[i >> 5], 1u << (i & 31));
       }
+      if (qn > 0) drain(qn);
     } else {                                          // ---- dense mode
       for (int w = 0; w < nw; ++w) {
         const uint32_t i = (uint32_t)(w << 5) | (uint32_t)lane;
@@ -2269,18 +2314,278 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
         if (lane >= o) incl += t;
       }
       if (sl) {
-        int q = run + incl - c;
+        int qq = run + incl - c;
         while (v) {
           const int bit = __ffs(v) - 1;
           v &= v - 1;
-          if (q < list_cap) sl[q] = (uint32_t)((w << 5) + bit);
-          ++q;
+          if (qq < list_cap) sl[qq] = (uint32_t)((w << 5) + bit);
+          ++qq;
         }
       }
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (rcount && lane == 0) rcount[frame] = (unsigned long long)run;
     __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 for D == 3 with small vote regions (c3: region = one dim-0 plane of N1 x N2 = 128 x 32
+// locations): one WARP per region (frame, i0), no CTA barrier.  Identity I1 (Props. 3-4,
+// P:437-450): abar[i] = sum_l c_l[M_l(i)]; with k_etab's expansions E[frame][l][k0][k1][w]
+// (the last-dim masks of the set buckets of bucket row (k0, k1), OR-ed) the votes of the 32
+// locations of detection word (i0, i1, w) in loop l are ONE word,
+// E[frame][l][k0_l(i0)][k1_l(i1)][w], k_d = floor(B_d [sigma_{l,d} i_d]_{N_d} / N_d) (Def. 3).
+// Lanes take consecutive words (coalesced detection stores); MODE 0 ANDs the L words
+// (mu = L), 1 ORs them (mu = 1), 2 counts them in bit-sliced planes and tests >= mu
+// (Alg. 1 l.11-14).  The L loads of a word are independent (all in flight).
+// Outputs: detection words, and (list mode) the region count + ascending local index list.
+// ------------------------------------------------------------------------------------
+template <int LP, int MODE>
+__global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64_t d0b, int64_t d0e,
+                                                 uint32_t* __restrict__ detect, unsigned long long* __restrict__ rcount,
+                                                 uint32_t* __restrict__ slots, int list_cap) {
+  pdl_enter();
+  __shared__ int s0[LP], s1[LP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int L = pd.L, B0 = pd.b[0], B1 = pd.b[1], W = pd.n[2] >> 5, N1 = pd.n[1];
+  const uint32_t n0m = (uint32_t)(pd.n[0] - 1), n1m = (uint32_t)(N1 - 1);
+  const int lga0 = pd.lga[0], lga1 = pd.lga[1];
+  for (int l = threadIdx.x; l < LP; l += blockDim.x) {
+    s0[l] = l < L ? pd.loops[l].sig[0] : 0;
+    s1[l] = l < L ? pd.loops[l].sig[1] : 0;
+  }
+  __syncthreads();
+  int sg1[LP];
+#pragma unroll
+  for (int l = 0; l < LP; ++l) sg1[l] = s1[l];
+  const int64_t slab = d0e - d0b;
+  const int64_t nregions = batch * slab;
+  const int items = N1 * W;                          // detection words per region
+  const int lgW = __ffs(W) - 1;
+  const int64_t slab_words = slab * items;
+  const int mu = pd.mu;
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, TW = (int64_t)gridDim.x * nwarps;
+  for (int64_t r = gw; r < nregions; r += TW) {
+    const int64_t frame = r / slab, i0 = d0b + (r - frame * slab);
+    const uint32_t* et[LP];                          // E rows of this region's dim-0 buckets
+#pragma unroll
+    for (int l = 0; l < LP; ++l) {
+      const int k0 = (int)((((uint32_t)s0[l < L ? l : 0] * (uint32_t)i0) & n0m) >> lga0);
+      et[l] = pd.etab + (((size_t)frame * L + (l < L ? l : 0)) * B0 + k0) * (size_t)B1 * W;
+    }
+    uint32_t* det = detect + (size_t)frame * slab_words + (size_t)(i0 - d0b) * items;
+    uint32_t* sl = slots ? slots + (size_t)r * list_cap : nullptr;
+    int run = 0;
+    for (int it0 = 0; it0 < items; it0 += 32) {
+      const int it = it0 + lane;
+      uint32_t word = 0u;
+      if (it < items) {
+        const uint32_t i1 = (uint32_t)(it >> lgW), w = (uint32_t)(it & (W - 1));
+        uint32_t e[LP];
+#pragma unroll
+        for (int l = 0; l < LP; ++l)
+          e[l] = l < L ? __ldg(et[l] + ((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w) : 0u;
+        if (MODE == 0) {
+          word = 0xffffffffu;
+#pragma unroll
+          for (int l = 0; l < LP; ++l) if (l < L) word &= e[l];
+        } else if (MODE == 1) {
+#pragma unroll
+          for (int l = 0; l < LP; ++l) word |= e[l];
+        } else {
+          uint32_t pl[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+          for (int l = 0; l < LP; ++l) {
+            uint32_t carry = e[l];
+#pragma unroll
+            for (int b = 0; b < 6; ++b) { const uint32_t t = pl[b] & carry; pl[b] ^= carry; carry = t; }
+          }
+          uint32_t gt = 0u, eq = 0xffffffffu;          // bit-sliced count >= mu
+#pragma unroll
+          for (int b = 5; b >= 0; --b) {
+            const uint32_t mb = ((mu >> b) & 1) ? 0xffffffffu : 0u;
+            gt |= eq & pl[b] & ~mb;
+            eq &= ~(pl[b] ^ mb);
+          }
+          word = gt | eq;
+        }
+        det[it] = word;
+      }
+      const int c = __popc(word);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (sl) {
+        int q = run + incl - c;
+        uint32_t v = word;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          if (q < list_cap) sl[q] = (uint32_t)((it << 5) + bit);
+          ++q;
+        }
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (rcount && lane == 0) rcount[r] = (unsigned long long)run;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 for D == 2 (c2/c4 frames): persistent CTAs, one frame per CTA iteration, rows of the
+// frame split over the threads (R consecutive rows each).  Identity I1 (Props. 3-4)
+// in word-parallel form: for loop l the 32 locations of detection word (i0, w) vote with ONE
+// word E[l][k0_l(i0)][w], E[l][k0] = OR of the last-dim masks X[l][k1] of the set buckets
+// (k0, k1) of loop l (built per frame from the plan-constant nibble tables: B1/4 lookups per
+// word), k0_l(i0) = floor(B0 [sigma_{l,0} i0]_{N0} / N0) (Def. 3).  MODE 0 ANDs the L words
+// (mu = L), 1 ORs them (mu = 1), 2 counts in bit-sliced planes and tests >= mu (Alg. 1
+// l.11-14).  Each thread writes its rows' detection words (contiguous) and, after a
+// block scan of the per-thread popcounts, the frame's ascending local index list; the frame
+// count goes to rcount for the offset scan.  4 barriers per frame.
+// ------------------------------------------------------------------------------------
+template <int LP, int MODE, int R>
+__global__ void __launch_bounds__(512) k_vote2d(PlanDev pd, const uint32_t* __restrict__ bitmaps, int64_t batch,
+                                                 uint32_t* __restrict__ detect, unsigned long long* __restrict__ rcount,
+                                                 uint32_t* __restrict__ slots, int list_cap) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint32_t v2s[];
+  __shared__ int wsum[16];
+  __shared__ int s0[LP];
+  const int tid = threadIdx.x;
+  const int L = pd.L, N0 = pd.n[0], N1 = pd.n[1], B0 = pd.b[0], B1 = pd.b[1], wpl = pd.wpl;
+  const int W = N1 >> 5, lgW = __ffs(W) - 1, ng = B1 >> 2, lga0 = pd.lga[0];
+  const uint32_t n0m = (uint32_t)(N0 - 1);
+  uint32_t* NT = v2s;                                // [L][ng][16][W]
+  uint32_t* E = NT + (size_t)L * ng * 16 * W;        // [L][B0][W] (16-B aligned: W % 4 == 0)
+  uint32_t* bm = E + (size_t)L * B0 * W;             // [L][wpl]
+  {
+    const int n4 = (L * ng * 16 * W) >> 2;
+    for (int i = tid; i < n4; i += blockDim.x)
+      reinterpret_cast<uint4*>(NT)[i] = __ldg(reinterpret_cast<const uint4*>(pd.ntab) + i);
+    for (int l = tid; l < LP; l += blockDim.x) s0[l] = l < L ? pd.loops[l].sig[0] : 0;
+  }
+  __syncthreads();
+  int sg0[LP];
+#pragma unroll
+  for (int l = 0; l < LP; ++l) sg0[l] = s0[l];
+  const int lgbw = (__ffs(B0) - 1) + lgW;
+  const int mu = pd.mu;
+  const int64_t fwords = (int64_t)N0 * W;
+
+  for (int64_t frame = blockIdx.x; frame < batch; frame += gridDim.x) {
+    for (int i = tid; i < L * wpl; i += blockDim.x) bm[i] = __ldg(bitmaps + (size_t)frame * L * wpl + i);
+    __syncthreads();
+    for (int j = tid; j < L * B0 * W; j += blockDim.x) {       // E rows of every dim-0 bucket
+      const int l = j >> lgbw, k0 = (j >> lgW) & (B0 - 1), w = j & (W - 1);
+      const int flat = k0 * B1;
+      const uint32_t* T = NT + (size_t)l * ng * 16 * W + w;
+      uint32_t e = 0u;
+      if (B1 <= 32) {
+        uint32_t pat = (bm[l * wpl + (flat >> 5)] >> (flat & 31)) & (B1 == 32 ? 0xffffffffu : ((1u << B1) - 1u));
+        for (int g = 0; g < ng; ++g, pat >>= 4) e |= T[((g << 4) + (pat & 15)) * W];
+      } else {
+        uint32_t lo = bm[l * wpl + (flat >> 5)], hi = bm[l * wpl + (flat >> 5) + 1];
+#pragma unroll
+        for (int g = 0; g < 8; ++g, lo >>= 4) e |= T[((g << 4) + (lo & 15)) * W];
+#pragma unroll
+        for (int g = 8; g < 16; ++g, hi >>= 4) e |= T[((g << 4) + (hi & 15)) * W];
+      }
+      E[j] = e;
+    }
+    __syncthreads();
+    // vote rows i0 = tid R + r
+    uint32_t acc[R][8];
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i0 = tid * R + r;
+      uint32_t pl[MODE == 2 ? 8 : 1][MODE == 2 ? 6 : 1];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        acc[r][w] = MODE == 0 ? 0xffffffffu : 0u;
+        if constexpr (MODE == 2) {
+#pragma unroll
+          for (int b = 0; b < 6; ++b) pl[w][b] = 0u;
+        }
+      }
+      if (i0 < N0) {
+#pragma unroll
+        for (int l = 0; l < LP; ++l) {
+          if (l >= L) break;
+          const int k0 = (int)((((uint32_t)sg0[l] * (uint32_t)i0) & n0m) >> lga0);
+          const uint32_t* er = E + ((size_t)l * B0 + k0) * W;
+          uint32_t m[8];
+#pragma unroll
+          for (int w = 0; w < 8; w += 4) {
+            if (w < W) {
+              const uint4 v = *reinterpret_cast<const uint4*>(er + w);
+              m[w] = v.x; m[w + 1] = v.y; m[w + 2] = v.z; m[w + 3] = v.w;
+            } else {
+              m[w] = m[w + 1] = m[w + 2] = m[w + 3] = 0u;
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            if (MODE == 0) acc[r][w] &= m[w];
+            else if (MODE == 1) acc[r][w] |= m[w];
+            else {
+              uint32_t carry = m[w];
+#pragma unroll
+              for (int b = 0; b < 6; ++b) { const uint32_t t = pl[w][b] & carry; pl[w][b] ^= carry; carry = t; }
+            }
+          }
+        }
+        if constexpr (MODE == 2) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+            for (int b = 5; b >= 0; --b) {
+              const uint32_t mb = ((mu >> b) & 1) ? 0xffffffffu : 0u;
+              gt |= eq & pl[w][b] & ~mb;
+              eq &= ~(pl[w][b] ^ mb);
+            }
+            acc[r][w] = gt | eq;
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (w >= W) acc[r][w] = 0u;
+          cnt += __popc(acc[r][w]);
+        }
+        uint32_t* dst = detect + (size_t)frame * fwords + (size_t)i0 * W;
+#pragma unroll
+        for (int w = 0; w < 8; w += 4)
+          if (w < W) *reinterpret_cast<uint4*>(dst + w) = make_uint4(acc[r][w], acc[r][w + 1], acc[r][w + 2], acc[r][w + 3]);
+      } else {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc[r][w] = 0u;
+      }
+    }
+    int total;
+    int pos = block_excl_scan(cnt, wsum, &total);
+    if (slots && total <= list_cap) {
+      uint32_t* sl = slots + (size_t)frame * list_cap;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i0 = tid * R + r;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          uint32_t v = acc[r][w];
+          while (v) {
+            const int bit = __ffs(v) - 1;
+            v &= v - 1;
+            sl[pos++] = (uint32_t)(i0 * N1 + (w << 5) + bit);
+          }
+        }
+      }
+    }
+    if (rcount && tid == 0) rcount[frame] = (unsigned long long)total;
+    __syncthreads();                                 // wsum / bm / E reused by the next frame
   }
 }
 
@@ -2990,9 +3295,84 @@ static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   return check(cudaGetLastError(), "k_vote1d launch");
 }
 
+// D == 3 warp-per-region vote (k_vote3d) on the k_etab expansions: small regions, no abar.
+static bool vote3d_ok(const rsft_plan_s* p, int64_t batch, int64_t d0b, int64_t d0e, uint8_t* counts) {
+  const char* off = getenv("RSFT_NO_VOTE3D");        // read per launch: tests select either kernel
+  if (off && off[0] && off[0] != '0') return false;
+  return p->D == 3 && !counts && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
+         (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= 256 && p->L <= 32;
+}
+
+static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
+                                 uint32_t* det, unsigned long long* rcount, uint32_t* slots, int list_cap,
+                                 cudaStream_t st) {
+  const int64_t ne = batch * p->L * p->b[0] * p->b[1];
+  const int64_t eg = (ne + kThreads - 1) / kThreads;
+  if (cudaError_t le_ = pdl_launch(k_etab, (unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st,
+                                   p->dev, bm, batch); le_ != cudaSuccess)
+    return check(le_, "k_etab launch");
+  p->last_launches += 1;
+  const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
+  const int lp = p->L <= 8 ? 8 : p->L <= 16 ? 16 : 32;
+  void (*kern)(PlanDev, int64_t, int64_t, int64_t, uint32_t*, unsigned long long*, uint32_t*, int) = nullptr;
+#define RSFT_V3(LPV, MV) if (lp == LPV && mode == MV) kern = k_vote3d<LPV, MV>;
+  RSFT_V3(8, 0) RSFT_V3(8, 1) RSFT_V3(8, 2) RSFT_V3(16, 0) RSFT_V3(16, 1) RSFT_V3(16, 2)
+  RSFT_V3(32, 0) RSFT_V3(32, 1) RSFT_V3(32, 2)
+#undef RSFT_V3
+  const int64_t nregions = batch * (d0e - d0b);
+  int64_t grid = (nregions + 7) / 8;
+  if (grid > 16 * (int64_t)p->num_sms) grid = 16 * (int64_t)p->num_sms;
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, 256, 0, st, p->dev, batch, d0b, d0e, det, rcount, slots,
+                                   list_cap); le_ != cudaSuccess)
+    return check(le_, "k_vote3d launch");
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_vote3d launch");
+}
+
+// D == 2 persistent CTA-per-frame vote (k_vote2d): full range, no abar, W = N1/32 in {4, 8},
+// plan-constant nibble tables available, rows per thread <= 8.
+static bool vote2d_ok(const rsft_plan_s* p, int64_t d0b, int64_t d0e, uint8_t* counts) {
+  const char* off = getenv("RSFT_NO_VOTE2D");        // read per launch: tests select either kernel
+  if (off && off[0] && off[0] != '0') return false;
+  const int64_t W = p->D == 2 ? p->n[1] / 32 : 0;
+  return p->D == 2 && !counts && d0b == 0 && d0e == p->n[0] && (W == 4 || W == 8) && p->dev.ntab &&
+         p->b[1] >= 4 && p->n[0] <= 4 * 512 && p->L <= 32;
+}
+
+static rsft_status launch_vote2d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
+                                 unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
+  const int64_t W = p->n[1] / 32, ng = p->b[1] / 4;
+  const size_t smem = ((size_t)p->L * ng * 16 * W + (size_t)p->L * p->b[0] * W + (size_t)p->L * p->dev.wpl + 4) * 4;
+  const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
+  const int lp = p->L <= 8 ? 8 : p->L <= 16 ? 16 : 32;
+  // 4 rows per thread: N0 / 4 threads (a warp at least)
+  const int threads = (int)std::max<int64_t>(32, ((p->n[0] / 4 + 31) / 32) * 32);
+  void (*kern)(PlanDev, const uint32_t*, int64_t, uint32_t*, unsigned long long*, uint32_t*, int) = nullptr;
+#define RSFT_V2(LPV, MV) if (lp == LPV && mode == MV) kern = k_vote2d<LPV, MV, 4>;
+  RSFT_V2(8, 0) RSFT_V2(8, 1) RSFT_V2(8, 2) RSFT_V2(16, 0) RSFT_V2(16, 1) RSFT_V2(16, 2)
+  RSFT_V2(32, 0) RSFT_V2(32, 1) RSFT_V2(32, 2)
+#undef RSFT_V2
+  if (!kern) return RSFT_E_UNSUPPORTED;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  int nb = 0;
+  s = check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem), "occupancy");
+  if (s) return s;
+  if (nb < 1) { set_error("k_vote2d: zero occupancy"); return RSFT_E_UNSUPPORTED; }
+  int64_t grid = (int64_t)nb * p->num_sms;
+  if (grid > batch) grid = batch;
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, (unsigned)threads, smem, st, p->dev, bm, batch, det, rcount, slots,
+                                   list_cap); le_ != cudaSuccess)
+    return check(le_, "k_vote2d launch");
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_vote2d launch");
+}
+
 rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                           uint32_t* det, uint8_t* counts, cudaStream_t st) {
   if (vote1d_ok(p, counts)) return launch_vote1d(p, bm, batch, det, nullptr, nullptr, 0, st);
+  if (vote2d_ok(p, d0b, d0e, counts)) return launch_vote2d(p, bm, batch, det, nullptr, nullptr, 0, st);
+  if (vote3d_ok(p, batch, d0b, d0e, counts)) return launch_vote3d(p, bm, batch, d0b, d0e, det, nullptr, nullptr, 0, st);
   return launch_vote_mode<false, false>(p, bm, batch, d0b, d0e, det, counts, st);
 }
 
@@ -3008,11 +3388,17 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   const int64_t cw = (W % 8 == 0 && mode != 2) ? 8 : W % 4 == 0 ? 4 : W % 2 == 0 ? 2 : 1;
   const int64_t rows = D == 3 ? p->n[1] : D == 2 ? n0 : 1;
   const bool v1 = vote1d_ok(p, nullptr);
-  const bool list = p->dev.region_slots && (v1 || rows * (W / cw) <= (int64_t)kListIpt * kThreads);
+  const bool v3 = !v1 && vote3d_ok(p, batch, 0, n0, nullptr);
+  const bool v2 = !v1 && !v3 && vote2d_ok(p, 0, n0, nullptr);
+  const bool list = p->dev.region_slots && (v1 || v2 || v3 || rows * (W / cw) <= (int64_t)kListIpt * kThreads);
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
   if (nregions > p->dev.region_capacity) return RSFT_E_WORKSPACE;
   rsft_status s = v1 ? launch_vote1d(p, bm, batch, det, p->dev.region_state, list ? p->dev.region_slots : nullptr,
+                                     (int)p->dev.list_cap, st)
+                : v3 ? launch_vote3d(p, bm, batch, 0, n0, det, p->dev.region_state, list ? p->dev.region_slots : nullptr,
+                                     (int)p->dev.list_cap, st)
+                : v2 ? launch_vote2d(p, bm, batch, det, p->dev.region_state, list ? p->dev.region_slots : nullptr,
                                      (int)p->dev.list_cap, st)
                 : list ? launch_vote_mode<true, true>(p, bm, batch, 0, n0, det, nullptr, st)
                        : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);

@@ -61,6 +61,8 @@ CASES = [
     ("3d_split", (64, 32, 32), (8, 4, 8), 8, dict(p_fa=1e-5, random_tau=True), 2, "split"),
     ("3d_split_L12", (32, 16, 64), (4, 4, 8), 12, dict(p_fa=1e-4, mu=9), 1, "split"),
     ("3d_L1", (16, 16, 64), (4, 8, 16), 1, dict(p_fa=1e-3), 1, "split"),
+    ("3d_c3like_mu", (64, 128, 32), (8, 16, 8), 8, dict(p_fa=1e-2, mu=5, random_tau=True), 3, "split"),
+    ("3d_c3like_or", (32, 64, 32), (4, 8, 8), 4, dict(p_fa=1e-3, mu=1), 2, "split"),
     ("2d_B_eq_N_dim0", (64, 128), (64, 8), 3, dict(p_fa=1e-3), 3, "fused"),
     ("2d_B1_dim0", (64, 128), (1, 16), 3, dict(p_fa=1e-3), 2, "fused"),
     ("2d_Blast1", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "fused"),
@@ -111,6 +113,22 @@ def test_parity_1d_streaming_fold_forced(case, monkeypatch):
     the warp-per-frame vote: both paths stay parity-green."""
     monkeypatch.setenv("RSFT_NO_GATHER1D", "1")
     monkeypatch.setenv("RSFT_NO_VOTE1D", "1")
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+V3_CASES = [c for c in CASES if c[0].startswith("3d_")]
+
+
+@pytest.mark.parametrize("case", V3_CASES, ids=[c[0] for c in V3_CASES])
+def test_parity_3d_region_vote_forced(case, monkeypatch):
+    """The 3-D shapes with the CTA-per-region vote (RSFT_NO_VOTE3D=1, read per launch) instead
+    of the warp-per-region vote on the k_etab expansions: both stay parity-green."""
+    monkeypatch.setenv("RSFT_NO_VOTE3D", "1")
     name, n, b, loops, kw, batch, mode = case
     op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
