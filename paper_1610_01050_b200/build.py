@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsft.so")
-SOURCES = ["plan.cpp", "design.cpp", "api.cu", "kernels.cu", "synth.cu", "bartlett.cu"]
+SOURCES = ["plan.cpp", "design.cpp", "api.cu", "kernels.cu", "vote.cu", "synth.cu", "bartlett.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr",
@@ -27,14 +27,19 @@ def build(force=False, verbose=False, extra=(), out=None):
     lib_path = out or LIB
     if out is None and not force and not _stale():
         return LIB
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         obj = lib_path + "." + src + ".o"
-        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmds.append([NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj])
+        objs.append(obj)
+    # translation units compile in parallel (kernels.cu and vote.cu dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    def run(cmd):
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(run, cmds))
     tmp = lib_path + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
