@@ -1725,7 +1725,13 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
                         "smem attr");
   if (s) return s;
   dim3 grid2((unsigned)(nl * blast), (unsigned)batch);
-  if (cudaError_t le_ = pdl_launch(k_split_fft, grid2, kThreadsFft, smem2, st, p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
+  // small outer grids (c3: 512 points) run 4 points per thread so that many CTAs are resident;
+  // large ones (c5: 2048) keep one L2 round trip per thread
+  const char* env_t = getenv("RSFT_FFT_THREADS");
+  int threads = env_t && env_t[0] ? atoi(env_t) : 0;
+  if (threads <= 0) threads = p->dev.bouter >= 2048 ? kThreadsFft : (int)std::max<int64_t>(64, p->dev.bouter / 4);
+  threads = std::min(threads, kThreadsFft);
+  if (cudaError_t le_ = pdl_launch(k_split_fft, grid2, (unsigned)threads, smem2, st, p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
                                                  reinterpret_cast<float2*>(spectra)); le_ != cudaSuccess)
     return check(le_, "k_split_fft launch");
   p->last_launches += 1;
