@@ -45,7 +45,7 @@ typedef enum {
   RSFT_E_ARG = 1,          /* null pointer, bad range, mu/loops/p_fa out of range     */
   RSFT_E_SHAPE = 2,        /* N_d or B_d not a power of two, B_d > N_d, support rule (L2)      */
   RSFT_E_SIGMA = 3,        /* even sigma in rsft_set_schedule (Eq. mod_inv)     */
-  RSFT_E_UNSUPPORTED = 4,  /* D > 3, B_d > 64, L > 32, N_last < 32, or tables beyond smem     */
+  RSFT_E_UNSUPPORTED = 4,  /* D > 3, B_d > 64, L > 63, N_last < 32, or tables beyond smem     */
   RSFT_E_WORKSPACE = 5,    /* workspace missing, too small or misaligned (256 B)              */
   RSFT_E_CUDA = 6,         /* a CUDA runtime call or launch failed (see rsft_last_error)      */
   RSFT_E_STATE = 7         /* plan not bound (rsft_bind) before a device call                 */
@@ -68,7 +68,8 @@ typedef struct {
   int64_t n[3];            /* N_d, powers of two                                       */
   int64_t b[3];            /* B_d, powers of two, 1 <= B_d <= min(N_d, 64) (Def. 2)       */
   int64_t support[3];      /* flat-window support W_d; 0 => N_d; need 2 B_d | W_d <= N_d */
-  int32_t loops;           /* L (the paper's T iterations, Alg. 1 l.4 P:219), 1..32           */
+  int32_t loops;           /* L (the paper's T iterations, Alg. 1 l.4 P:219), 1..63 (> 32: one
+                              pass over x per 32 loops; rsft_bucketize_partial: <= 32)        */
   int32_t prewin;          /* rsft_win of the pre-permutation window               */
   double prewin_param;     /* Chebyshev attenuation dB when prewin == RSFT_WIN_CHEB           */
   double flat_atten_db;    /* Dolph-Chebyshev taper of the flat window, default 60 (L2)       */

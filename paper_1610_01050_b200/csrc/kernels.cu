@@ -1777,6 +1777,7 @@ static rsft_status launch_partial_t(rsft_plan_s* p, const void* d_x, int64_t off
 
 rsft_status launch_partial(rsft_plan_s* p, const void* d_x, int64_t off, int64_t len, void* d_partial,
                            cudaStream_t st) {
+  if (p->L > kMaxLaunchLoops) { set_error("rsft_bucketize_partial: more than 32 loops"); return RSFT_E_UNSUPPORTED; }
   RSFT_DISPATCH_LP(launch_partial_t, loop_pad(p->L), p, d_x, off, len, d_partial, st);
 }
 
@@ -1806,6 +1807,11 @@ static rsft_status launch_segments_fused_t(rsft_plan_s* p, const void* d_x, int6
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                            void* spectra, cudaStream_t st);
 
+static rsft_status launch_fused_lp(rsft_plan_s* p, int lp, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
+                                   void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride) {
+  RSFT_DISPATCH_LP(launch_fused_t, lp, p, d_x, batch, l0, nl, bm, spectra, st, 0, bm_stride, sp_stride);
+}
+
 rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, void* spectra,
                             cudaStream_t st) {
   if (resolve_mode(p, batch) == RSFT_MODE_FUSED && loop_pad(1) == 2) {
@@ -1825,6 +1831,30 @@ rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint
 
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                            void* spectra, cudaStream_t st) {
+  if (nl > kMaxLaunchLoops) {                        // > 32 loops: one pass over x per <= 32 loops
+    const int c = (nl + kMaxLaunchLoops - 1) / kMaxLaunchLoops;
+    const int per = (nl + c - 1) / c;
+    const bool fused = resolve_mode(p, batch) == RSFT_MODE_FUSED;
+    int launches = 0;
+    for (int a = 0; a < nl; a += per) {
+      const int m = std::min(per, nl - a);
+      // loops [a, a + m) of the [batch][nl][...] outputs: frame-strided (fused kernels take
+      // the strides; split mode runs one frame per launch)
+      for (int64_t f = 0; f < (fused ? 1 : batch); ++f) {
+        const char* xf = reinterpret_cast<const char*>(d_x) + (size_t)f * p->ntot * 8;
+        uint32_t* bmf = bm + ((size_t)f * nl + a) * p->dev.wpl;
+        void* spf = spectra ? reinterpret_cast<char*>(spectra) + ((size_t)f * nl + a) * p->btot * 8 : nullptr;
+        p->last_launches = 0;
+        rsft_status s = fused ? launch_fused_lp(p, loop_pad(m), xf, batch, l0 + a, m, bmf, spf, st,
+                                                (int64_t)nl * p->dev.wpl, (int64_t)nl * p->btot)
+                              : launch_execute(p, xf, 1, l0 + a, m, bmf, spf, st);
+        if (s) return s;
+        launches += p->last_launches;
+      }
+    }
+    p->last_launches = launches;
+    return RSFT_OK;
+  }
   int mode = resolve_mode(p, batch);
   int lp = loop_pad(nl);
   if (mode == RSFT_MODE_FUSED) { RSFT_DISPATCH_LP(launch_fused_t, lp, p, d_x, batch, l0, nl, bm, spectra, st); }

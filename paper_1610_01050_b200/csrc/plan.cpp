@@ -306,13 +306,14 @@ int gather1d_taps(const rsft_plan_s* p) {
 
 int resolve_mode(const rsft_plan_s* p, int64_t batch) {
   const int64_t nlast = p->n[p->D - 1];
-  const int lp = loop_pad(p->L);
+  const int Lf = std::min(p->L, kMaxLaunchLoops);   // loops per fold launch
+  const int lp = loop_pad(Lf);
   bool fused_ok = p->D <= 2 && nlast >= 64 && p->btot <= 8 * kThreads &&
-                  (fused_smem_bytes(p, p->L, lp) <= (fused_cfg(p->D).ctas == 1 ? 220 : 110) * 1024 ||
+                  (fused_smem_bytes(p, Lf, lp) <= (fused_cfg(p->D).ctas == 1 ? 220 : 110) * 1024 ||
                    gather1d_taps(p) > 0);
   // split mode chunks dim 0 as far as needed to fit the per-warp tables (launch_split_fold_t)
   const int64_t amin = p->D == 3 ? 1 : std::min<int64_t>(p->a[0], (int64_t)kUSplit * (nlast >= 64 ? 1 : 64 / nlast));
-  bool split_ok = p->D >= 2 && split_smem_bytes(p, p->L, lp, amin) <= 220 * 1024;
+  bool split_ok = p->D >= 2 && split_smem_bytes(p, Lf, lp, amin) <= 220 * 1024;
   int m = p->P.mode;
   if (m == RSFT_MODE_FUSED) return fused_ok ? RSFT_MODE_FUSED : -1;
   if (m == RSFT_MODE_SPLIT) return split_ok ? RSFT_MODE_SPLIT : -1;
@@ -354,7 +355,7 @@ rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out) {
   if (P.ndim < 1) return RSFT_E_ARG;
   if (P.ndim > 3) return RSFT_E_UNSUPPORTED;
   if (P.loops < 1) return RSFT_E_ARG;
-  if (P.loops > kMaxLoops) return RSFT_E_UNSUPPORTED;
+  if (P.loops > kMaxLoops - 1) return RSFT_E_UNSUPPORTED;
   int mu = P.mu == 0 ? P.loops : P.mu;
   if (mu < 1 || mu > P.loops) return RSFT_E_ARG;
   if (!(P.p_fa > 0.0 && P.p_fa < 1.0)) return RSFT_E_ARG;
@@ -470,7 +471,7 @@ rsft_status rsft_get_info(rsft_plan_t p, rsft_info* info) {
   info->bitmap_words = (p->btot + 31) / 32;
   info->detect_words = (p->ntot + 31) / 32;
   info->mode = resolve_mode(p, p->P.max_batch);
-  info->lpad = loop_pad(p->L);
+  info->lpad = loop_pad(std::min(p->L, kMaxLaunchLoops));
   info->workspace_bytes = p->ws.total;
   return RSFT_OK;
 }

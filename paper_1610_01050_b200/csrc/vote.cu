@@ -1278,7 +1278,7 @@ static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t 
 static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
   const char* off = getenv("RSFT_NO_VOTE1D");        // read per launch: tests select either kernel
   if (off && off[0] && off[0] != '0') return false;
-  return p->D == 1 && !counts && p->n[0] >= 32 && p->n[0] <= 32768;
+  return p->D == 1 && !counts && p->n[0] >= 32 && p->n[0] <= 32768 && p->L <= 32;
 }
 
 static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
@@ -1338,8 +1338,10 @@ static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t bat
 // D == 2 persistent CTA-per-frame vote (k_vote2d): full range, no abar, W = N1/32 in {4, 8},
 // plan-constant nibble tables available, rows per thread <= 8.
 static bool vote2d_ok(const rsft_plan_s* p, int64_t d0b, int64_t d0e, uint8_t* counts) {
-  const char* off = getenv("RSFT_NO_VOTE2D");        // read per launch: tests select either kernel
-  if (off && off[0] && off[0] != '0') return false;
+  // opt-in (RSFT_VOTE2D=1, read per launch): at c4 it measured 184-189 us against 129 us for
+  // the CTA-per-region k_vote (shared-memory bank conflicts on the random E rows, 2 CTAs/SM)
+  const char* on = getenv("RSFT_VOTE2D");
+  if (!(on && on[0] && on[0] != '0')) return false;
   const int64_t W = p->D == 2 ? p->n[1] / 32 : 0;
   return p->D == 2 && !counts && d0b == 0 && d0e == p->n[0] && (W == 4 || W == 8) && p->dev.ntab &&
          p->b[1] >= 4 && p->n[0] <= 4 * 512 && p->L <= 32;

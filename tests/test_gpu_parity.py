@@ -63,6 +63,10 @@ CASES = [
     ("3d_L1", (16, 16, 64), (4, 8, 16), 1, dict(p_fa=1e-3), 1, "split"),
     ("3d_c3like_mu", (64, 128, 32), (8, 16, 8), 8, dict(p_fa=1e-2, mu=5, random_tau=True), 3, "split"),
     ("3d_c3like_or", (32, 64, 32), (4, 8, 8), 4, dict(p_fa=1e-3, mu=1), 2, "split"),
+    # more than 32 loops (up to 63, the paper's T = 50 design point P:640): several fold passes
+    ("2d_L40", (128, 64), (16, 8), 40, dict(p_fa=1e-2, mu=30, random_tau=True), 2, "fused"),
+    ("1d_L50_w256", (1024,), (32,), 50, dict(support=(256,), p_fa=1e-2, mu=40), 2, "fused"),
+    ("3d_L36", (16, 32, 32), (4, 8, 8), 36, dict(p_fa=1e-2, mu=20), 2, "split"),
     ("2d_B_eq_N_dim0", (64, 128), (64, 8), 3, dict(p_fa=1e-3), 3, "fused"),
     ("2d_B1_dim0", (64, 128), (1, 16), 3, dict(p_fa=1e-3), 2, "fused"),
     ("2d_Blast1", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "fused"),
@@ -129,6 +133,22 @@ def test_parity_3d_region_vote_forced(case, monkeypatch):
     """The 3-D shapes with the CTA-per-region vote (RSFT_NO_VOTE3D=1, read per launch) instead
     of the warp-per-region vote on the k_etab expansions: both stay parity-green."""
     monkeypatch.setenv("RSFT_NO_VOTE3D", "1")
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+V2_CASES = [c for c in CASES if c[0].startswith("2d_") and c[6] == "fused"]
+
+
+@pytest.mark.parametrize("case", V2_CASES, ids=[c[0] for c in V2_CASES])
+def test_parity_2d_frame_vote_opt_in(case, monkeypatch):
+    """The 2-D shapes with the opt-in persistent CTA-per-frame vote (RSFT_VOTE2D=1, read per
+    launch) instead of the default CTA-per-region vote: both stay parity-green."""
+    monkeypatch.setenv("RSFT_VOTE2D", "1")
     name, n, b, loops, kw, batch, mode = case
     op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
@@ -365,6 +385,7 @@ def test_variant_b_c5_full_cube():
 # ----------------------------------------------------------------------------- segment mode
 @pytest.mark.parametrize("n,b,L,mode", [
     ((128, 64), (16, 8), 5, "fused"),
+    ((1024,), (64,), 50, "fused"),                  # the paper's T = 50
     ((1024,), (32,), 4, "fused"),
     ((32, 16, 64), (4, 4, 8), 3, "split"),
 ])

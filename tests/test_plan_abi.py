@@ -109,7 +109,7 @@ def test_set_schedule_roundtrip_and_errors():
     (dict(n=(1024,), b=(128,), loops=1), 4),                # B > 64 unsupported
     (dict(n=(64,), b=(8,), loops=1, support=(24,)), 2),     # 2B does not divide W
     (dict(n=(64,), b=(8,), loops=0), 1),
-    (dict(n=(64,), b=(8,), loops=40), 4),                   # L > 32
+    (dict(n=(64,), b=(8,), loops=64), 4),                   # L > 63 (6 vote bit planes)
     (dict(n=(64,), b=(8,), loops=4, mu=5), 1),              # mu > L
     (dict(n=(64,), b=(8,), loops=4, p_fa=1.5), 1),
     (dict(n=(16,), b=(8,), loops=1), 4),                    # N_last < 32
