@@ -1338,10 +1338,13 @@ static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t bat
 // D == 2 persistent CTA-per-frame vote (k_vote2d): full range, no abar, W = N1/32 in {4, 8},
 // plan-constant nibble tables available, rows per thread <= 8.
 static bool vote2d_ok(const rsft_plan_s* p, int64_t d0b, int64_t d0e, uint8_t* counts) {
-  // opt-in (RSFT_VOTE2D=1, read per launch): at c4 it measured 184-189 us against 129 us for
-  // the CTA-per-region k_vote (shared-memory bank conflicts on the random E rows, 2 CTAs/SM)
+  // default for short frames (N0 <= 256; c2: 0.98 vs 1.03 ms per step); at c4 (N0 = 1024) it
+  // measured 184-189 us against 129 us for the CTA-per-region k_vote (shared-memory bank
+  // conflicts on the random E rows, 2 CTAs/SM), so there it is opt-in.  RSFT_VOTE2D=1 / 0
+  // (read per launch) forces it on / off.
   const char* on = getenv("RSFT_VOTE2D");
-  if (!(on && on[0] && on[0] != '0')) return false;
+  if (on && on[0] == '0') return false;
+  if (!(on && on[0]) && p->D == 2 && p->n[0] > 256) return false;
   const int64_t W = p->D == 2 ? p->n[1] / 32 : 0;
   return p->D == 2 && !counts && d0b == 0 && d0e == p->n[0] && (W == 4 || W == 8) && p->dev.ntab &&
          p->b[1] >= 4 && p->n[0] <= 4 * 512 && p->L <= 32;

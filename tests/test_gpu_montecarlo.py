@@ -11,6 +11,8 @@ import numpy as np
 import pytest
 
 import synth
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -86,3 +88,67 @@ def test_design_monte_carlo_segment_mode(b, T):
     print(f"   exact-binomial model: P_d={pd_exact:.3f}, P_fa={pfa_exact:.2e}")
     assert 0.75 <= pd_meas <= 1.0 and abs(pd_meas - pd_exact) < 0.12   # alpha varies with sigma (Jensen)
     assert pfa_exact / 2 <= pfa_meas <= 2 * pfa_exact
+
+
+# ----------------------------------------------------------------------------- T = 50
+def test_per_sigma_first_stage_law_and_variance_bound():
+    """The paper's design point (N = 1024, T = 50, B = 64, Dolph-Chebyshev 40 dB, omega_m = 64.5
+    bins).  (a) For every odd sigma the GPU's first-stage detection rate of the tone's
+    bucket follows Eq. tpd with the oracle's alpha(sigma), beta(sigma) (Eq.
+    alpha_beta) -- binomial error, all 512 permutations.  (b) Fig. varAppErr: the
+    approximation error of the variance bound T Pd_bar (1 - Pd_bar) from the measured
+    per-permutation rates is a few percent (the paper: ~1.6 % at T = 10) and agrees with the
+    closed form's."""
+    import study_next2 as S
+    des = S.design()
+    sig, a, b = S.oracle_alpha_beta()
+    law = S.tpd(a, b, des["gamma"], des["snr_min"])
+    sig_g, p_hat, F = S.per_sigma_detection(des, frames=4096)
+    assert np.array_equal(sig, sig_g)
+    z = (p_hat - law) / np.sqrt(law * (1 - law) / F)
+    print(f"per-sigma law: max |z| = {np.max(np.abs(z)):.2f} over {sig.size} sigmas, mean P~ "
+          f"measured {p_hat.mean():.4f} / law {law.mean():.4f}")
+    assert np.max(np.abs(z)) < 5.5
+    pv = p_hat * (1 - p_hat) * F / (F - 1)
+    for T in (10, 50):
+        e_law, _ = S.approx_error(law, T)
+        e_gpu, _ = S.approx_error(p_hat, T, var_unbiased=pv)
+        print(f"T={T}: approximation error law {100 * e_law:.2f} %, GPU {100 * e_gpu:.2f} %")
+        assert 0.0 <= e_law < 0.10 and abs(e_gpu - e_law) < 0.02
+
+
+def test_fixed_schedule_vote_variance_T50():
+    """Eq. var_a1 end to end at T = 50: for one schedule the tone location's vote
+    count abar_i (rsft_detect counts, segment mode) has mean sum_s P~_d(sigma_s) and variance
+    sum_s P~_d (1 - P~_d) <= T Pd_bar (1 - Pd_bar)."""
+    import study_next2 as S
+    des = S.design()
+    sig, a, b = S.oracle_alpha_beta()
+    law = S.tpd(a, b, des["gamma"], des["snr_min"])
+    sg, ab = S.fixed_schedule_votes(des, frames=8192, batches=2)
+    pl = law[(sg - 1) // 2]
+    n = ab.size
+    mean_ref, var_ref = pl.sum(), (pl * (1 - pl)).sum()
+    m4 = np.mean((ab - ab.mean()) ** 4)
+    se_var = math.sqrt(max(m4 - ab.var() ** 2, 1e-12) / n)
+    print(f"abar: mean {ab.mean():.3f} (sum P~ {mean_ref:.3f}), var {ab.var(ddof=1):.3f} "
+          f"(sum P~(1-P~) {var_ref:.3f} +- {se_var:.3f}; bound {S.T_PAPER * law.mean() * (1 - law.mean()):.3f})")
+    assert abs(ab.mean() - mean_ref) < 5 * math.sqrt(var_ref / n)
+    assert abs(ab.var(ddof=1) - var_ref) < 5 * se_var
+
+
+def test_detector_at_paper_design_point_T50():
+    """The two-stage detector with Eq. opt's (gamma*, mu*) at T = 50: P_d against the
+    target 0.9 and the exact-Binomial model; false detections bounded by the model."""
+    from scipy.stats import binom
+    import study_next2 as S
+    des = S.design()
+    pd_m, fa, trials = S.detector_at_design(des, frames=4096, batches=1)
+    q = des["F"] / S.T_PAPER
+    pd_x = binom.sf(des["mu"] - 1, S.T_PAPER, des["pd_bar"])
+    pfa_x = binom.sf(des["mu"] - 1, S.T_PAPER, q * des["pd_bar"] + (1 - q) * des["pfa_bar"])
+    print(f"T=50 design mu*={des['mu']} SNR*={des['snr_min_db']:.2f} dB gamma*={des['gamma']:.4g}: P_d {pd_m:.3f} "
+          f"(target 0.9, exact-binomial {pd_x:.3f}); false detections {fa} / {trials} "
+          f"(exact-binomial expects {pfa_x * trials:.1f})")
+    assert abs(pd_m - pd_x) < 0.05 and pd_m > 0.8
+    assert fa <= max(10, 5 * pfa_x * trials)

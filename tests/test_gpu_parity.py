@@ -145,10 +145,11 @@ V2_CASES = [c for c in CASES if c[0].startswith("2d_") and c[6] == "fused"]
 
 
 @pytest.mark.parametrize("case", V2_CASES, ids=[c[0] for c in V2_CASES])
-def test_parity_2d_frame_vote_opt_in(case, monkeypatch):
-    """The 2-D shapes with the opt-in persistent CTA-per-frame vote (RSFT_VOTE2D=1, read per
-    launch) instead of the default CTA-per-region vote: both stay parity-green."""
-    monkeypatch.setenv("RSFT_VOTE2D", "1")
+@pytest.mark.parametrize("force", ["1", "0"])
+def test_parity_2d_frame_vote_forced(case, force, monkeypatch):
+    """The 2-D shapes with the persistent CTA-per-frame vote forced on / off (RSFT_VOTE2D=1/0,
+    read per launch; default: on for N0 <= 256): both paths stay parity-green."""
+    monkeypatch.setenv("RSFT_VOTE2D", force)
     name, n, b, loops, kw, batch, mode = case
     op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
