@@ -525,7 +525,8 @@ def bench_bartlett(a, wl, rank, world, dev):
     g = plan.bartlett_threshold(T, wl.p_fa)
     power = torch.empty((frames,) + tuple(wl.n), dtype=torch.float32, device=dev)
     det = torch.empty((frames, plan.detect_words), dtype=torch.int32, device=dev)
-    scratch = torch.empty((frames,) + tuple(wl.n), dtype=torch.complex64, device=dev)
+    scratch = (torch.empty((frames, T) + tuple(wl.n), dtype=torch.complex64, device=dev)
+               if int(np.prod(wl.n)) > 8192 else None)
     for _ in range(a.warmup):
         plan.bartlett(xs, gamma=g, power=power, detect=det, scratch=scratch)
     torch.cuda.synchronize()
@@ -538,10 +539,17 @@ def bench_bartlett(a, wl, rank, world, dev):
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / a.steps
+    ntot = int(np.prod(wl.n))
+    algo = frames * (T * ntot * 8 + ntot * 4)                 # segments read once, power written once
+    passes = 1 if ntot <= 8192 else 3                         # two-pass: + scratch write + re-read
+    moved = frames * (passes * T * ntot * 8 + ntot * 4)
+    peak, _ = load_peaks()
     out = {"metric": "Bartlett baseline (Alg. 2) frames/s, T = L segments per frame", "value": frames * 1000.0 / ms,
            "unit": "frames/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
            "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded Eq. sig_model segments)",
            "config": {"workload": wl.name, "n": list(wl.n), "segments": T, "frames": frames, "impl": "bartlett"},
+           "hbm": {"algorithmic_gbs": algo / (ms / 1e3) / 1e9, "design_bytes_gbs": moved / (ms / 1e3) / 1e9,
+                   "design_frac": moved / (ms / 1e3) / 1e9 / peak, "passes_over_input": passes},
            "gpu_launches": launches}
     print(json.dumps(out), flush=True)
     return 0

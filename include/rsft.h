@@ -262,9 +262,13 @@ rsft_status rsft_synthesize(const int64_t* n, int32_t ndim, int64_t batch, int32
 /* Bartlett baseline (Algorithm 2, App. A): for each frame
  * and each of its `segments` segments u = W r_s (the plan's separable pre-window), N-D FFT
  * (hand-written, N_d <= 4096), x += |u_hat|^2; then bit i of d_detect = (x_i / segments > gamma).
- *   d_x      device complex64 [batch][segments][N...];  d_scratch device complex64 [batch][N_tot];
+ * Frames of <= 8192 samples run in one pass (power kept on chip); larger frames (D >= 2, with
+ * N_tot / N_0 <= 8192) in two passes through d_scratch (inner dims, then dim 0 + |.|^2).
+ *   d_x      device complex64 [batch][segments][N...];
+ *   d_scratch device complex64 [batch][segments][N_tot] when N_tot > 8192, else unused (may be NULL);
  *   d_power  device fp32 [batch][N_tot] (x, overwritten);  d_detect NULL or uint32
- *            [batch][detect_words].  Errors: E_ARG, E_STATE, E_UNSUPPORTED (N_d > 4096), E_CUDA. */
+ *            [batch][detect_words].  Errors: E_ARG, E_STATE, E_UNSUPPORTED (N_d > 4096, no
+ *            scratch, inner block > 8192), E_CUDA. */
 rsft_status rsft_bartlett(rsft_plan_t plan, const void* d_x, int64_t batch, int32_t segments, void* d_scratch,
                           float* d_power, double gamma, uint32_t* d_detect, void* stream);
 /* gamma of Eq. bartlettROC for a per-bin false-alarm target: the H'0 statistic is

@@ -2,9 +2,17 @@
 // (P:926-943): for every segment s, u = W r_s (the plan's separable pre-window), u_hat =
 // N-D FFT(u) (forward, unnormalised), x += |u_hat|^2; then l = x / T > gamma (NP test,
 // Eq. bartlettROC).  The dense comparison workload for the RSFT's complexity claim
-// (Tables I-II).  Hand-written FFTs (no cuFFT): one kernel per axis, each CTA
-// transforms C adjacent lines of that axis in shared memory (radix-2 DIT, stage-parallel);
-// the first pass applies the window, the last pass accumulates |.|^2.
+// (Tables I-II).  Hand-written FFTs (no cuFFT), radix-2 DIT in shared memory.
+// Data movement is the design point (the FFT is cheap next to HBM at these sizes):
+//  * frames of <= 8192 samples (c1: 4096): ONE pass -- a CTA keeps the frame's power in shared
+//    memory while it streams the T segments (window on load, N-D FFT, |.|^2), then writes the
+//    power and the detection words once: HBM = T N 8 B read + N 4 B written.
+//  * larger frames (D >= 2, dim-0 rows of <= 8192 samples; c2, c3, c4): TWO passes -- pass 1
+//    transforms the contiguous inner block (all dims but 0) of a tile of dim-0 rows, window
+//    fused into the load, into the scratch (T N 8 B read + T N 8 B written, coalesced); pass 2
+//    transforms dim 0 for a tile of adjacent inner columns and accumulates |.|^2 over the T
+//    segments in registers, writing power and detection bits once (T N 8 B read + N 4 B).
+//    3x the input bytes, the minimum for a 2-D FFT whose frame exceeds one SM's shared memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,51 +24,24 @@
 namespace rsft {
 
 constexpr int kBartTile = 8192;            // complex elements per CTA tile (64 KiB smem)
+constexpr int kBartThreads = 512;
 
-__global__ void __launch_bounds__(256) k_bart_axis(const float2* __restrict__ in, int64_t in_stride,
-                                                   float2* __restrict__ out,
-                                                   float* __restrict__ power, int D, int n0, int n1, int n2,
-                                                   int axis, int window, int last,
-                                                   const float* __restrict__ w0, const float* __restrict__ w1,
-                                                   const float* __restrict__ w2, const float2* __restrict__ tw) {
-  extern __shared__ float2 sv[];
-  const int nn[3] = {n0, n1, n2};
-  const int na = nn[axis];
-  int64_t inner = 1;
-  for (int d = axis + 1; d < 3; ++d) inner *= nn[d];
-  const int lg = __ffs(na) - 1;
-  const int C = (int)(inner < (int64_t)(kBartTile / na) ? inner : (int64_t)(kBartTile / na));
-  const int64_t iblocks = inner / C;
-  const int64_t o = blockIdx.x / iblocks, ib = blockIdx.x - o * iblocks;
-  const int64_t fr = blockIdx.y;                   // frame of the batch
-  const int64_t ntot = (int64_t)n0 * n1 * n2;
-  in += fr * in_stride;
-  out += fr * ntot;
-  power += fr * ntot;
-  const int64_t base = o * na * inner + ib * C;
-  const int tid = threadIdx.x;
-  // load C lines (coalesced along the C adjacent inner indices), window, bit-reversed
-  for (int e = tid; e < na * C; e += blockDim.x) {
-    const int p = e / C, c = e - p * C;
-    const int64_t idx = base + (int64_t)p * inner + c;
-    float2 v = in[idx];
-    if (window) {
-      const int i2 = (int)(idx % n2), i1 = (int)((idx / n2) % n1), i0 = (int)(idx / ((int64_t)n1 * n2));
-      const float w = w0[i0] * w1[i1] * w2[i2];
-      v.x *= w; v.y *= w;
-    }
-    sv[c * na + (int)(__brev((unsigned)p) >> (32 - lg))] = v;
-  }
-  __syncthreads();
-  const int tstep = 4096 / na;                    // tw[k] = e^{-j 2 pi k / 4096}
+// In-place radix-2 DIT along one axis of a shared-memory tile (bit-reversed input, natural
+// output): 2^lg points `ps` apart; line r of nlines starts at (r >> sh) * hs + (r & (2^sh - 1)) * ls.
+// tw[k] = e^{-j 2 pi k / 4096} for k < 2048 (shared copy); one barrier per stage.
+__device__ __forceinline__ void bart_fft_axis(float2* sv, int lg, int ps, int nlines, int sh, int hs, int ls,
+                                              const float2* __restrict__ tw) {
+  if (lg == 0) return;
+  const int nbf = nlines << (lg - 1);
+  const int lm = (1 << sh) - 1;
   for (int s = 1; s <= lg; ++s) {
     const int half = 1 << (s - 1);
-    for (int bf = tid; bf < (na >> 1) * C; bf += blockDim.x) {
-      const int c = bf >> (lg - 1), r = bf & ((na >> 1) - 1);
-      const int j = r & (half - 1), g = r >> (s - 1);
-      float2* e0 = sv + c * na + (g << s) + j;
-      float2* e1 = e0 + half;
-      const float2 t = tw[(j << (lg - s)) * tstep];
+    for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
+      const int r = bf >> (lg - 1), q = bf & ((1 << (lg - 1)) - 1);
+      const int j = q & (half - 1), g = q >> (s - 1);
+      float2* e0 = sv + (r >> sh) * hs + (r & lm) * ls + ((g << s) + j) * ps;
+      float2* e1 = e0 + half * ps;
+      const float2 t = tw[j << (12 - s)];
       const float2 b = *e1;
       const float2 tb = make_float2(t.x * b.x - t.y * b.y, t.x * b.y + t.y * b.x);
       const float2 a = *e0;
@@ -69,25 +50,130 @@ __global__ void __launch_bounds__(256) k_bart_axis(const float2* __restrict__ in
     }
     __syncthreads();
   }
-  for (int e = tid; e < na * C; e += blockDim.x) {
-    const int p = e / C, c = e - p * C;
-    const int64_t idx = base + (int64_t)p * inner + c;
-    const float2 v = sv[c * na + p];
-    if (last) power[idx] += v.x * v.x + v.y * v.y;
-    else out[idx] = v;
+}
+
+__device__ __forceinline__ int bart_brev(int v, int lg) { return lg ? (int)(__brev((unsigned)v) >> (32 - lg)) : 0; }
+
+struct BartGeo {                           // dims right-aligned: (n0, n1, n2), D = 1..3
+  int n0, n1, n2, lg0, lg1, lg2;
+  const float* w0; const float* w1; const float* w2;
+};
+
+// Pass 1 / single pass.  Tile = `rows` consecutive dim-0 rows (all of dims 1, 2), contiguous in
+// memory.  single: the tile is the whole frame; the CTA loops over the T segments keeping the
+// power in shared memory, then writes power + detection.  Otherwise: one (frame, segment, row
+// tile) per CTA iteration, written to the scratch (natural order).
+__global__ void __launch_bounds__(kBartThreads) k_bart_inner(PlanDev pd, BartGeo g, const float2* __restrict__ x,
+                                                             int64_t batch, int T, int rows, int single,
+                                                             float2* __restrict__ scratch, float* __restrict__ power,
+                                                             float scale, float gamma, uint32_t* __restrict__ det) {
+  extern __shared__ __align__(16) float2 bsm[];
+  float2* tw = bsm;                                  // [2048]
+  float2* sv = tw + 2048;                            // [rows * n1 * n2]
+  float* pw = reinterpret_cast<float*>(sv + kBartTile);   // single: [n0 n1 n2]
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) tw[i] = pd.btw[i];
+  const int inner = g.n1 * g.n2, elems = rows * inner;
+  const int lgi = g.lg1 + g.lg2;
+  const int64_t ntot = (int64_t)g.n0 * inner;
+  const int64_t tiles_per_seg = g.n0 / rows;
+  const int64_t units = single ? batch : batch * T * tiles_per_seg;
+  const bool fft0 = single && g.n0 > 1;              // single pass also transforms dim 0
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t frame = single ? u : u / (T * tiles_per_seg);
+    const int seg0 = single ? 0 : (int)((u / tiles_per_seg) % T);
+    const int tile = single ? 0 : (int)(u % tiles_per_seg);
+    if (single)
+      for (int e = threadIdx.x; e < elems; e += blockDim.x) pw[e] = 0.f;
+    for (int s = seg0; s < (single ? T : seg0 + 1); ++s) {
+      __syncthreads();                               // tw ready / previous tile's readers done
+      const float2* src = x + ((size_t)frame * T + s) * ntot + (size_t)tile * elems;
+      for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+        const int i2 = e & (g.n2 - 1), i1 = (e >> g.lg2) & (g.n1 - 1), r = e >> lgi;
+        const float w = g.w0[tile * rows + r] * g.w1[i1] * g.w2[i2];
+        float2 v = src[e];
+        v.x *= w; v.y *= w;
+        const int pr = fft0 ? bart_brev(r, g.lg0) : r;
+        sv[(pr << lgi) + (bart_brev(i1, g.lg1) << g.lg2) + bart_brev(i2, g.lg2)] = v;
+      }
+      __syncthreads();
+      bart_fft_axis(sv, g.lg2, 1, rows * g.n1, 0, g.n2, 0, tw);                 // dim 2 (contiguous)
+      bart_fft_axis(sv, g.lg1, g.n2, rows * g.n2, g.lg2, g.n1 * g.n2, 1, tw);   // dim 1
+      if (fft0) bart_fft_axis(sv, g.lg0, inner, inner, lgi, 0, 1, tw);          // dim 0 (single)
+      if (single) {
+        for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+          const float2 v = sv[e];
+          pw[e] += v.x * v.x + v.y * v.y;
+        }
+      } else {
+        float2* dst = scratch + ((size_t)frame * T + s) * ntot + (size_t)tile * elems;
+        for (int e = threadIdx.x; e < elems; e += blockDim.x) dst[e] = sv[e];
+      }
+    }
+    if (single) {
+      __syncthreads();
+      float* pdst = power + (size_t)frame * ntot;
+      const int64_t words = (ntot + 31) >> 5;
+      for (int e0 = threadIdx.x & ~31; e0 < ((elems + 31) & ~31); e0 += blockDim.x) {
+        const int e = e0 + (threadIdx.x & 31);
+        const float p = e < elems ? pw[e] : 0.f;
+        if (e < elems) pdst[e] = p;
+        const unsigned word = __ballot_sync(0xffffffffu, e < elems && p * scale > gamma);
+        if (det && (threadIdx.x & 31) == 0) det[(size_t)frame * words + (e0 >> 5)] = word;
+      }
+    }
   }
 }
 
-// l = x / T > gamma -> detection bitmap words (one ballot per 32 locations)
-__global__ void k_bart_detect(const float* __restrict__ power, int64_t ntot, int64_t batch, float scale, float gamma,
-                              uint32_t* __restrict__ det) {
-  const int64_t per = (ntot + 31) & ~int64_t(31), words = per >> 5;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < batch * per;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = i / per, k = i - f * per;
-    const bool bit = k < ntot && power[f * ntot + k] * scale > gamma;
-    const unsigned word = __ballot_sync(0xffffffffu, bit);
-    if ((threadIdx.x & 31) == 0) det[f * words + (k >> 5)] = word;
+// Pass 2 (D >= 2): dim-0 FFT of C adjacent inner columns for every segment, |.|^2 summed over
+// the T segments in registers, then power + detection bits (atomicOr: a word spans 32 / C tiles).
+template <int PT>
+__global__ void __launch_bounds__(kBartThreads) k_bart_outer(PlanDev pd, BartGeo g, const float2* __restrict__ scratch,
+                                                             int64_t batch, int T, int C, float* __restrict__ power,
+                                                             float scale, float gamma, uint32_t* __restrict__ det) {
+  extern __shared__ __align__(16) float2 bsm[];
+  float2* tw = bsm;
+  float2* sv = tw + 2048;                            // [n0][C]
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) tw[i] = pd.btw[i];
+  const int inner = g.n1 * g.n2, lgc = __ffs(C) - 1;
+  const int elems = g.n0 * C;
+  const int64_t ntot = (int64_t)g.n0 * inner;
+  const int64_t ctiles = inner / C;
+  const int64_t units = batch * ctiles;
+  const int64_t words = (ntot + 31) >> 5;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t frame = u / ctiles;
+    const int c0 = (int)(u % ctiles) * C;
+    float acc[PT];
+#pragma unroll
+    for (int k = 0; k < PT; ++k) acc[k] = 0.f;
+    for (int s = 0; s < T; ++s) {
+      __syncthreads();
+      const float2* src = scratch + ((size_t)frame * T + s) * ntot + c0;
+      for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+        const int r = e >> lgc, c = e & (C - 1);
+        sv[(bart_brev(r, g.lg0) << lgc) + c] = src[(size_t)r * inner + c];
+      }
+      __syncthreads();
+      bart_fft_axis(sv, g.lg0, C, C, lgc, 0, 1, tw);
+#pragma unroll
+      for (int k = 0; k < PT; ++k) {
+        const int e = threadIdx.x + k * blockDim.x;
+        if (e < elems) { const float2 v = sv[e]; acc[k] += v.x * v.x + v.y * v.y; }
+      }
+    }
+    float* pdst = power + (size_t)frame * ntot + c0;
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < elems) {
+        const int r = e >> lgc, c = e & (C - 1);
+        pdst[(size_t)r * inner + c] = acc[k];
+        if (det && acc[k] * scale > gamma) {
+          const int64_t loc = (int64_t)r * inner + c0 + c;
+          atomicOr(det + (size_t)frame * words + (loc >> 5), 1u << (loc & 31));
+        }
+      }
+    }
   }
 }
 
@@ -99,45 +185,69 @@ extern "C" {
 
 rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t segments, void* d_scratch,
                           float* d_power, double gamma, uint32_t* d_detect, void* stream) {
-  if (!p || !d_x || !d_scratch || !d_power || segments < 1 || batch < 1) return RSFT_E_ARG;
+  if (!p || !d_x || !d_power || segments < 1 || batch < 1) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   for (int d = 0; d < p->D; ++d)
     if (p->n[d] > 4096) return RSFT_E_UNSUPPORTED;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   p->last_launches = 0;
+  BartGeo g{};
   int nn[3] = {1, 1, 1};
   const float* w[3] = {p->dev.bwin[0], p->dev.bwin[1], p->dev.bwin[2]};
   const float* wr[3];
-  for (int d = 0; d < 3; ++d) {                   // right-align the dims in (n0, n1, n2)
+  for (int d = 0; d < 3; ++d) {                     // right-align the dims in (n0, n1, n2)
     const int dd = d - (3 - p->D);
     nn[d] = dd >= 0 ? (int)p->n[dd] : 1;
     wr[d] = dd >= 0 ? w[dd] : p->dev.bone;
   }
-  const int64_t ntot = p->ntot;
-  if (cudaMemsetAsync(d_power, 0, (size_t)batch * ntot * 4, st) != cudaSuccess) return RSFT_E_CUDA;
-  cudaFuncSetAttribute(k_bart_axis, cudaFuncAttributeMaxDynamicSharedMemorySize, kBartTile * 8);
-  for (int s = 0; s < segments; ++s) {
-    const float2* src = reinterpret_cast<const float2*>(d_x) + (size_t)s * ntot;   // frame f: + f T N_tot
-    bool first = true;
-    for (int axis = 2; axis >= 3 - p->D; --axis) { // last dim first (contiguous), then outer dims
-      const bool last = axis == 3 - p->D;
-      int64_t inner = 1;
-      for (int d = axis + 1; d < 3; ++d) inner *= nn[d];
-      const int64_t C = std::min<int64_t>(inner, kBartTile / nn[axis]);
-      const int64_t tiles = ntot / ((int64_t)nn[axis] * C);
-      const size_t smem = (size_t)nn[axis] * C * 8;
-      dim3 grid((unsigned)tiles, (unsigned)batch);
-      k_bart_axis<<<grid, 256, smem, st>>>(first ? src : reinterpret_cast<const float2*>(d_scratch),
-                                           first ? (int64_t)segments * ntot : ntot,
-                                           reinterpret_cast<float2*>(d_scratch), d_power, 0, nn[0], nn[1], nn[2],
-                                           axis, first ? 1 : 0, last ? 1 : 0, wr[0], wr[1], wr[2], p->dev.btw);
-      p->last_launches += 1;
-      first = false;
-    }
-  }
-  if (d_detect) {
-    k_bart_detect<<<1184, 256, 0, st>>>(d_power, ntot, batch, (float)(1.0 / segments), (float)gamma, d_detect);
-    p->last_launches += 1;
+  // D = 1: the single dim is dim 0 (n0); right-aligned it sits in n2 -- move it to n0
+  if (p->D == 1) { nn[0] = nn[2]; nn[2] = 1; wr[0] = wr[2]; wr[2] = p->dev.bone; }
+  if (p->D == 2) { nn[0] = nn[1]; nn[1] = nn[2]; nn[2] = 1; wr[0] = wr[1]; wr[1] = wr[2]; wr[2] = p->dev.bone; }
+  g.n0 = nn[0]; g.n1 = nn[1]; g.n2 = nn[2];
+  g.lg0 = __builtin_ctz(nn[0]); g.lg1 = __builtin_ctz(nn[1]); g.lg2 = __builtin_ctz(nn[2]);
+  g.w0 = wr[0]; g.w1 = wr[1]; g.w2 = wr[2];
+  const int64_t ntot = p->ntot, inner = (int64_t)nn[1] * nn[2];
+  const float scale = (float)(1.0 / segments), gam = (float)gamma;
+  const bool single = ntot <= kBartTile;
+  if (!single && (inner > kBartTile || !d_scratch)) return RSFT_E_UNSUPPORTED;
+  const size_t tw_bytes = 2048 * 8;
+  if (single) {
+    const size_t smem = tw_bytes + (size_t)kBartTile * 8 + (size_t)ntot * 4;
+    if (cudaFuncSetAttribute(k_bart_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return RSFT_E_CUDA;
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_bart_inner, kBartThreads, smem);
+    const int64_t grid = std::min<int64_t>(batch, (int64_t)std::max(nb, 1) * p->num_sms);
+    k_bart_inner<<<(unsigned)grid, kBartThreads, smem, st>>>(p->dev, g, reinterpret_cast<const float2*>(d_x), batch,
+                                                             segments, (int)nn[0], 1, nullptr, d_power, scale, gam,
+                                                             d_detect);
+    p->last_launches = 1;
+  } else {
+    const int rows = (int)std::min<int64_t>(nn[0], kBartTile / inner);
+    const size_t smem1 = tw_bytes + (size_t)kBartTile * 8;
+    if (cudaFuncSetAttribute(k_bart_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess)
+      return RSFT_E_CUDA;
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_bart_inner, kBartThreads, smem1);
+    const int64_t units1 = batch * segments * (nn[0] / rows);
+    const int64_t grid1 = std::min<int64_t>(units1, (int64_t)std::max(nb, 1) * p->num_sms);
+    k_bart_inner<<<(unsigned)grid1, kBartThreads, smem1, st>>>(p->dev, g, reinterpret_cast<const float2*>(d_x), batch,
+                                                               segments, rows, 0, reinterpret_cast<float2*>(d_scratch),
+                                                               nullptr, scale, gam, nullptr);
+    if (d_detect && cudaMemsetAsync(d_detect, 0, (size_t)batch * ((ntot + 31) / 32) * 4, st) != cudaSuccess)
+      return RSFT_E_CUDA;
+    const int C = (int)std::min<int64_t>(inner, kBartTile / nn[0]);
+    const int pt = (nn[0] * C + kBartThreads - 1) / kBartThreads;
+    auto kern = pt <= 4 ? k_bart_outer<4> : pt <= 8 ? k_bart_outer<8> : k_bart_outer<16>;
+    if (pt > 16) return RSFT_E_UNSUPPORTED;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess)
+      return RSFT_E_CUDA;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBartThreads, smem1);
+    const int64_t units2 = batch * (inner / C);
+    const int64_t grid2 = std::min<int64_t>(units2, (int64_t)std::max(nb, 1) * p->num_sms);
+    kern<<<(unsigned)grid2, kBartThreads, smem1, st>>>(p->dev, g, reinterpret_cast<const float2*>(d_scratch), batch,
+                                                       segments, C, d_power, scale, gam, d_detect);
+    p->last_launches = 2;
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_error(std::string("bartlett: ") + cudaGetErrorString(e)); return RSFT_E_CUDA; }

@@ -405,9 +405,10 @@ class Plan:
             power = torch.empty((batch,) + self.n, dtype=torch.float32, device=self.device)
         if detect is None:
             detect = torch.empty((batch, self.detect_words), dtype=torch.int32, device=self.device)
-        if scratch is None:
-            scratch = torch.empty((batch,) + self.n, dtype=torch.complex64, device=self.device)
-        _check(lib().rsft_bartlett(self._h, c_void_p(xb.data_ptr()), batch, T, c_void_p(scratch.data_ptr()),
+        if scratch is None and self.ntot > 8192:       # two-pass frames: [batch][T][N_tot]
+            scratch = torch.empty((batch, T) + self.n, dtype=torch.complex64, device=self.device)
+        _check(lib().rsft_bartlett(self._h, c_void_p(xb.data_ptr()), batch, T,
+                                   c_void_p(scratch.data_ptr()) if scratch is not None else None,
                                    c_void_p(power.data_ptr()), float(gamma), c_void_p(detect.data_ptr()),
                                    _stream_handle(stream)))
         if single:
