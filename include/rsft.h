@@ -120,6 +120,9 @@ typedef struct {
   size_t workspace_bytes;
 } rsft_info;
 rsft_status rsft_get_info(rsft_plan_t plan, rsft_info* info);
+/* Workspace size.  The plan is host-only (no CUDA call), so the split-mode folded-spectra
+ * buffer is sized for a 148-SM device (B200); on a device with more SMs the launcher keeps
+ * fewer dim-0 chunks per class (memory-safe, slightly less parallel). */
 size_t rsft_workspace_bytes(rsft_plan_t plan);
 
 /* Upload the plan tables into the caller-owned device workspace (>= rsft_workspace_bytes,
@@ -192,19 +195,23 @@ rsft_status rsft_detect(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t bat
 rsft_status rsft_compact(rsft_plan_t plan, const uint32_t* d_detect, int64_t batch,
                          int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);
 
-/* Fused second stage + compaction (full dim-0 range): the same detection bitmap as
- * rsft_detect and the same index list / count as rsft_compact, computed in one kernel when
- * a vote region fits (regions taken in ticket order, decoupled look-back), else as the two
- * passes.  Errors: E_ARG, E_STATE, E_WORKSPACE, E_CUDA. */
+/* Second stage + compaction (full dim-0 range): the same detection bitmap as rsft_detect and
+ * the same index list / count as rsft_compact.  Runs the vote kernel for the frame shape
+ * (D = 1: a warp per frame; D = 2 with N_0 <= 256: a CTA per frame; D = 3 with small planes: a
+ * warp per dim-0 plane; else a CTA per vote region), which also writes per-region detection
+ * counts and region-local sorted index lists into the workspace; then a two-pass parallel scan
+ * of the region counts (offsets, total -> *d_count) and a writer that copies each region's
+ * list to its offset (re-reading the region's detection words if its list overflowed).
+ * Errors: E_ARG, E_STATE, E_WORKSPACE, E_CUDA. */
 rsft_status rsft_detect_compact(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t batch,
                                 uint32_t* d_detect, int64_t* d_idx, int64_t capacity,
                                 int64_t* d_count, void* stream);
 
-/* Whole hot path on device buffers: rsft_execute (all loops) + rsft_detect_compact, with the
- * same outputs (d_bitmaps [batch][L][bitmap_words], d_detect [batch][detect_words], sorted
- * indices, *d_count).  In fused mode the second stage runs inside the fold kernel's
- * per-frame epilogue (the frame's bitmaps stay on the SM).  Errors: as rsft_execute and
- * rsft_detect_compact. */
+/* Whole hot path on device buffers: rsft_execute (all loops) + rsft_detect_compact, issued
+ * back to back on `stream` (programmatic dependent launches), with the same outputs (d_bitmaps
+ * [batch][L][bitmap_words], d_detect [batch][detect_words], sorted indices, *d_count).
+ * (Voting inside the fold kernel's per-frame epilogue was measured slower and is not done.)
+ * Errors: as rsft_execute and rsft_detect_compact. */
 rsft_status rsft_run(rsft_plan_t plan, const void* d_x, int64_t batch, uint32_t* d_bitmaps, uint32_t* d_detect,
                      int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);
 

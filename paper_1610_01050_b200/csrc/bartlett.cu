@@ -124,54 +124,223 @@ __global__ void __launch_bounds__(kBartThreads) k_bart_inner(PlanDev pd, BartGeo
   }
 }
 
-// Pass 2 (D >= 2): dim-0 FFT of C adjacent inner columns for every segment, |.|^2 summed over
-// the T segments in registers, then power + detection bits (atomicOr: a word spans 32 / C tiles).
-template <int PT>
-__global__ void __launch_bounds__(kBartThreads) k_bart_outer(PlanDev pd, BartGeo g, const float2* __restrict__ scratch,
-                                                             int64_t batch, int T, int C, float* __restrict__ power,
-                                                             float scale, float gamma, uint32_t* __restrict__ det) {
-  extern __shared__ __align__(16) float2 bsm[];
-  float2* tw = bsm;
-  float2* sv = tw + 2048;                            // [n0][C]
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) tw[i] = pd.btw[i];
-  const int inner = g.n1 * g.n2, lgc = __ffs(C) - 1;
-  const int elems = g.n0 * C;
-  const int64_t ntot = (int64_t)g.n0 * inner;
-  const int64_t ctiles = inner / C;
-  const int64_t units = batch * ctiles;
-  const int64_t words = (ntot + 31) >> 5;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t frame = u / ctiles;
-    const int c0 = (int)(u % ctiles) * C;
-    float acc[PT];
+// ---------------------------------------------------------------------------------------
+// Warp-level FFT of n = 32 M points held in registers (no barrier): lane l holds
+// v[k] = x[l + 32 k]; an in-lane M-point DIF over k, the twiddles W_n^{l q1}, then a 32-point
+// DIF across the lanes (xor shuffles).  On return lane p holds v[r] = X[brev_M(r) + M brev5(p)].
+// t = half-circle table e^{-j 2 pi k / 4096}, k < 2048, in shared memory.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 bart_twn(const float2* t, int j, int lgn) {
+  const int i = (j << (12 - lgn)) & 4095;
+  const float2 w = t[i & 2047];
+  return i < 2048 ? w : make_float2(-w.x, -w.y);
+}
+__device__ __forceinline__ float2 bart_cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+constexpr int bart_lg(int m) { return m <= 1 ? 0 : 1 + bart_lg(m / 2); }
+__device__ __forceinline__ int bart_brev_c(int v, int lg) { return lg ? (int)(__brev((unsigned)v) >> (32 - lg)) : 0; }
+
+template <int M>
+__device__ __forceinline__ void bart_warp_fft(float2 (&v)[M], int lane, int lgn, const float2* __restrict__ t,
+                                              const float2 (&stw)[5]) {
+  constexpr int LM = bart_lg(M);
 #pragma unroll
-    for (int k = 0; k < PT; ++k) acc[k] = 0.f;
+  for (int s = 0; s < LM; ++s) {                      // in-lane DIF over k (span M / 2^{s+1})
+#pragma unroll
+    for (int e = 0; e < M / 2; ++e) {
+      const int span = M >> (s + 1);
+      const int j = e & (span - 1), blk = (e / span) * 2 * span;
+      const float2 a = v[blk + j], b = v[blk + j + span];
+      v[blk + j] = make_float2(a.x + b.x, a.y + b.y);
+      const float2 d = make_float2(a.x - b.x, a.y - b.y);
+      v[blk + j + span] = j == 0 ? d : bart_cmul(d, bart_twn(t, j * (16 * M / span), lgn));
+    }
+  }
+  if (M > 1) {                                        // W_n^{lane q1}, q1 = brev(r), by recurrence
+    const float2 w1 = bart_twn(t, lane, lgn);
+    float2 cur = w1;
+#pragma unroll
+    for (int q1 = 1; q1 < M; ++q1) {
+      const int r = bart_brev_c(q1, LM);
+      v[r] = bart_cmul(v[r], cur);
+      cur = bart_cmul(cur, w1);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < M; ++r) {                       // 32-point DIF across lanes
+    float2 x = v[r];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int h = 16 >> q;
+      const float2 p = make_float2(__shfl_xor_sync(0xffffffffu, x.x, h), __shfl_xor_sync(0xffffffffu, x.y, h));
+      x = (lane & h) ? bart_cmul(make_float2(p.x - x.x, p.y - x.y), stw[q]) : make_float2(x.x + p.x, x.y + p.y);
+    }
+    v[r] = x;
+  }
+}
+
+__device__ __forceinline__ void bart_stw(float2 (&stw)[5], int lane, const float2* t) {
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {                       // W_{2h}^{lane mod h}, h = 16 >> q
+    const int h = 16 >> q;
+    stw[q] = bart_twn(t, (lane & (h - 1)) * (16 / h), 5);
+  }
+}
+
+// natural-order position of v[r] held by lane p after bart_warp_fft
+template <int M>
+__device__ __forceinline__ int bart_pos(int r, int lane) {
+  return bart_brev_c(r, bart_lg(M)) + M * (int)(__brev((unsigned)lane) >> 27);
+}
+
+// Pass 1, D == 2: one warp per (frame, segment, row): window on load, row FFT (n1 = 32 M),
+// natural order through the warp's shared line buffer, coalesced store to the scratch.
+template <int M>
+__global__ void __launch_bounds__(256) k_bart_rows(PlanDev pd, const float2* __restrict__ x, int64_t nrows, int n0,
+                                                   int lgn1, const float* __restrict__ w0, const float* __restrict__ w1,
+                                                   float2* __restrict__ scratch) {
+  extern __shared__ __align__(16) float2 br[];
+  float2* t = br;                                      // [2048]
+  float2 (*line)[32 * M] = reinterpret_cast<float2 (*)[32 * M]>(br + 2048);   // [8][n1]
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2 stw[5];
+  bart_stw(stw, lane, t);
+  constexpr int n1 = 32 * M;
+  float wc[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) wc[k] = w1[lane + 32 * k];
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < nrows; row += (int64_t)gridDim.x * 8) {
+    const float2* src = x + (size_t)row * n1;
+    const float wr = w0[(int)(row % n0)];
+    float2 v[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const float2 a = src[lane + 32 * k];
+      const float w = wr * wc[k];
+      v[k] = make_float2(a.x * w, a.y * w);
+    }
+    bart_warp_fft<M>(v, lane, lgn1, t, stw);
+#pragma unroll
+    for (int r = 0; r < M; ++r) line[warp][bart_pos<M>(r, lane)] = v[r];
+    __syncwarp();
+    float2* dst = scratch + (size_t)row * n1;
+#pragma unroll
+    for (int k = 0; k < M; ++k) dst[lane + 32 * k] = line[warp][lane + 32 * k];
+    __syncwarp();
+  }
+}
+
+// Pass 1, D == 3: one CTA per (frame, segment, dim-0 plane of n1 x n2 <= 8192): window on
+// load into shared memory, dim-2 lines (warp per line), dim-1 lines (warp per column, padded
+// rows), coalesced store of the plane to the scratch.
+template <int M2, int M1>
+__global__ void __launch_bounds__(256) k_bart_planes(PlanDev pd, const float2* __restrict__ x, int64_t nplanes,
+                                                     int n0, int lgn1, int lgn2, const float* __restrict__ w0,
+                                                     const float* __restrict__ w1, const float* __restrict__ w2,
+                                                     float2* __restrict__ scratch) {
+  extern __shared__ __align__(16) float2 bp[];
+  float2* t = bp;                                      // [2048]
+  float2* pl = t + 2048;                               // [n1][n2 + 1]
+  constexpr int n1 = 32 * M1, n2 = 32 * M2, st = n2 + 1;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float2 stw[5];
+  bart_stw(stw, lane, t);
+  for (int64_t pi = blockIdx.x; pi < nplanes; pi += gridDim.x) {
+    const float2* src = x + (size_t)pi * n1 * n2;
+    const float wr = w0[(int)(pi % n0)];
+    __syncthreads();                                   // previous plane's readers done
+    for (int e = threadIdx.x; e < n1 * n2; e += blockDim.x) {
+      const int i1 = e / n2, i2 = e - i1 * n2;
+      const float2 a = src[e];
+      const float w = wr * w1[i1] * w2[i2];
+      pl[i1 * st + i2] = make_float2(a.x * w, a.y * w);
+    }
+    __syncthreads();
+    for (int i1 = warp; i1 < n1; i1 += nw) {           // dim 2
+      float2 v[M2];
+#pragma unroll
+      for (int k = 0; k < M2; ++k) v[k] = pl[i1 * st + lane + 32 * k];
+      bart_warp_fft<M2>(v, lane, lgn2, t, stw);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < M2; ++r) pl[i1 * st + bart_pos<M2>(r, lane)] = v[r];
+    }
+    __syncthreads();
+    for (int i2 = warp; i2 < n2; i2 += nw) {           // dim 1
+      float2 v[M1];
+#pragma unroll
+      for (int k = 0; k < M1; ++k) v[k] = pl[(lane + 32 * k) * st + i2];
+      bart_warp_fft<M1>(v, lane, lgn1, t, stw);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < M1; ++r) pl[bart_pos<M1>(r, lane) * st + i2] = v[r];
+    }
+    __syncthreads();
+    float2* dst = scratch + (size_t)pi * n1 * n2;
+    for (int e = threadIdx.x; e < n1 * n2; e += blockDim.x) {
+      const int i1 = e / n2, i2 = e - i1 * n2;
+      dst[e] = pl[i1 * st + i2];
+    }
+  }
+}
+
+// Pass 2 (D >= 2): one CTA per (frame, tile of 8 adjacent inner columns); per segment the
+// [n0][8] tile is staged in shared memory (padded rows), warp w transforms column w along dim 0
+// and accumulates |.|^2 in registers over the T segments; power (natural order) and the
+// detection bits are written once.
+template <int M0>
+__global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __restrict__ scratch, int64_t batch, int T,
+                                                   int64_t inner, int lgn0, float* __restrict__ power, float scale,
+                                                   float gamma, uint32_t* __restrict__ det) {
+  extern __shared__ __align__(16) float2 bc[];
+  float2* t = bc;                                      // [2048]
+  float2* tile = t + 2048;                             // [n0][9]
+  constexpr int n0 = 32 * M0, C = 8, st = C + 1;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2 stw[5];
+  bart_stw(stw, lane, t);
+  const int64_t ctiles = inner / C, ntot = (int64_t)n0 * inner, words = (ntot + 31) >> 5;
+  float* ptile = reinterpret_cast<float*>(tile);       // reused for the power transpose: [n0][C]
+  for (int64_t u = blockIdx.x; u < batch * ctiles; u += gridDim.x) {
+    const int64_t frame = u / ctiles;
+    const int64_t c0 = (u - frame * ctiles) * C;
+    float acc[M0];
+#pragma unroll
+    for (int r = 0; r < M0; ++r) acc[r] = 0.f;
     for (int s = 0; s < T; ++s) {
       __syncthreads();
       const float2* src = scratch + ((size_t)frame * T + s) * ntot + c0;
-      for (int e = threadIdx.x; e < elems; e += blockDim.x) {
-        const int r = e >> lgc, c = e & (C - 1);
-        sv[(bart_brev(r, g.lg0) << lgc) + c] = src[(size_t)r * inner + c];
+      for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) {
+        const int r = e >> 3, c = e & 7;
+        tile[r * st + c] = src[(size_t)r * inner + c];
       }
       __syncthreads();
-      bart_fft_axis(sv, g.lg0, C, C, lgc, 0, 1, tw);
+      float2 v[M0];
 #pragma unroll
-      for (int k = 0; k < PT; ++k) {
-        const int e = threadIdx.x + k * blockDim.x;
-        if (e < elems) { const float2 v = sv[e]; acc[k] += v.x * v.x + v.y * v.y; }
-      }
+      for (int k = 0; k < M0; ++k) v[k] = tile[(lane + 32 * k) * st + warp];
+      bart_warp_fft<M0>(v, lane, lgn0, t, stw);
+#pragma unroll
+      for (int r = 0; r < M0; ++r) acc[r] += v[r].x * v[r].x + v[r].y * v[r].y;
     }
-    float* pdst = power + (size_t)frame * ntot + c0;
+    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < PT; ++k) {
-      const int e = threadIdx.x + k * blockDim.x;
-      if (e < elems) {
-        const int r = e >> lgc, c = e & (C - 1);
-        pdst[(size_t)r * inner + c] = acc[k];
-        if (det && acc[k] * scale > gamma) {
-          const int64_t loc = (int64_t)r * inner + c0 + c;
-          atomicOr(det + (size_t)frame * words + (loc >> 5), 1u << (loc & 31));
-        }
+    for (int r = 0; r < M0; ++r) ptile[bart_pos<M0>(r, lane) * C + warp] = acc[r];
+    __syncthreads();
+    float* pdst = power + (size_t)frame * ntot + c0;
+    for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) {
+      const int r = e >> 3, c = e & 7;
+      const float p = ptile[e];
+      pdst[(size_t)r * inner + c] = p;
+      if (det && p * scale > gamma) {
+        const int64_t loc = (int64_t)r * inner + c0 + c;
+        atomicOr(det + (size_t)frame * words + (loc >> 5), 1u << (loc & 31));
       }
     }
   }
@@ -223,30 +392,52 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
                                                              d_detect);
     p->last_launches = 1;
   } else {
-    const int rows = (int)std::min<int64_t>(nn[0], kBartTile / inner);
-    const size_t smem1 = tw_bytes + (size_t)kBartTile * 8;
-    if (cudaFuncSetAttribute(k_bart_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess)
-      return RSFT_E_CUDA;
-    int nb = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_bart_inner, kBartThreads, smem1);
-    const int64_t units1 = batch * segments * (nn[0] / rows);
-    const int64_t grid1 = std::min<int64_t>(units1, (int64_t)std::max(nb, 1) * p->num_sms);
-    k_bart_inner<<<(unsigned)grid1, kBartThreads, smem1, st>>>(p->dev, g, reinterpret_cast<const float2*>(d_x), batch,
-                                                               segments, rows, 0, reinterpret_cast<float2*>(d_scratch),
-                                                               nullptr, scale, gam, nullptr);
+    // pass 1: inner dims (D = 2: rows, warp per row; D = 3: planes, CTA per plane)
+    const int64_t nlines = batch * segments * nn[0];
+    const float2* xin = reinterpret_cast<const float2*>(d_x);
+    float2* scr = reinterpret_cast<float2*>(d_scratch);
+    auto mof = [](int n) { return n / 32; };
+    if (p->D == 2) {
+      const int m = mof(nn[1]);
+      void (*k1)(PlanDev, const float2*, int64_t, int, int, const float*, const float*, float2*) =
+          m == 1 ? k_bart_rows<1> : m == 2 ? k_bart_rows<2> : m == 4 ? k_bart_rows<4> : m == 8 ? k_bart_rows<8>
+        : m == 16 ? k_bart_rows<16> : m == 32 ? k_bart_rows<32> : nullptr;
+      if (!k1) return RSFT_E_UNSUPPORTED;
+      const size_t smem = (2048 + 8 * (size_t)nn[1]) * 8;
+      if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return RSFT_E_CUDA;
+      const int64_t grid = std::min<int64_t>((nlines + 7) / 8, 8 * (int64_t)p->num_sms);
+      k1<<<(unsigned)grid, 256, smem, st>>>(p->dev, xin, nlines, nn[0], g.lg1, wr[0], wr[1], scr);
+    } else {
+      const int m2 = mof(nn[2]), m1 = mof(nn[1]);
+      void (*k1)(PlanDev, const float2*, int64_t, int, int, int, const float*, const float*, const float*, float2*) = nullptr;
+#define RSFT_BP(A, B_) if (m2 == A && m1 == B_) k1 = k_bart_planes<A, B_>;
+      RSFT_BP(1, 1) RSFT_BP(1, 2) RSFT_BP(1, 4) RSFT_BP(1, 8) RSFT_BP(2, 1) RSFT_BP(2, 2) RSFT_BP(2, 4)
+      RSFT_BP(4, 1) RSFT_BP(4, 2) RSFT_BP(8, 1)
+#undef RSFT_BP
+      if (!k1) return RSFT_E_UNSUPPORTED;
+      const size_t smem = (2048 + (size_t)nn[1] * (nn[2] + 1)) * 8;
+      if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return RSFT_E_CUDA;
+      const int64_t grid = std::min<int64_t>(nlines, 4 * (int64_t)p->num_sms);
+      k1<<<(unsigned)grid, 256, smem, st>>>(p->dev, xin, nlines, nn[0], g.lg1, g.lg2, wr[0], wr[1], wr[2], scr);
+    }
     if (d_detect && cudaMemsetAsync(d_detect, 0, (size_t)batch * ((ntot + 31) / 32) * 4, st) != cudaSuccess)
       return RSFT_E_CUDA;
-    const int C = (int)std::min<int64_t>(inner, kBartTile / nn[0]);
-    const int pt = (nn[0] * C + kBartThreads - 1) / kBartThreads;
-    auto kern = pt <= 4 ? k_bart_outer<4> : pt <= 8 ? k_bart_outer<8> : k_bart_outer<16>;
-    if (pt > 16) return RSFT_E_UNSUPPORTED;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess)
+    // pass 2: dim 0 + |.|^2 over the segments + detection
+    const int m0 = mof(nn[0]);
+    void (*k2)(PlanDev, const float2*, int64_t, int, int64_t, int, float*, float, float, uint32_t*) =
+        m0 == 1 ? k_bart_cols<1> : m0 == 2 ? k_bart_cols<2> : m0 == 4 ? k_bart_cols<4> : m0 == 8 ? k_bart_cols<8>
+      : m0 == 16 ? k_bart_cols<16> : m0 == 32 ? k_bart_cols<32> : nullptr;
+    if (!k2 || inner % 8) return RSFT_E_UNSUPPORTED;
+    const size_t smem2 = (2048 + (size_t)nn[0] * 9) * 8;
+    if (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess)
       return RSFT_E_CUDA;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBartThreads, smem1);
-    const int64_t units2 = batch * (inner / C);
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2, 256, smem2);
+    const int64_t units2 = batch * (inner / 8);
     const int64_t grid2 = std::min<int64_t>(units2, (int64_t)std::max(nb, 1) * p->num_sms);
-    kern<<<(unsigned)grid2, kBartThreads, smem1, st>>>(p->dev, g, reinterpret_cast<const float2*>(d_scratch), batch,
-                                                       segments, C, d_power, scale, gam, d_detect);
+    k2<<<(unsigned)grid2, 256, smem2, st>>>(p->dev, scr, batch, segments, inner, g.lg0, d_power, scale, gam, d_detect);
     p->last_launches = 2;
   }
   const cudaError_t e = cudaGetLastError();

@@ -194,7 +194,7 @@ void layout_workspace(rsft_plan_s* p) {
   w.fbuf_off = off;
   w.fbuf_bytes = 0;
   if (p->D >= 2) {
-    const int64_t warps = (int64_t)148 * (kThreadsSplit / 32) * kCtasSplit;
+    const int64_t warps = (int64_t)kSizingSms * (kThreadsSplit / 32) * kCtasSplit;   // rsft.h: 148-SM sizing
     int64_t best = p->P.max_batch;
     for (int64_t b = 1; b <= std::min<int64_t>(p->P.max_batch, 64); b *= 2)
       best = std::max(best, b << split_lg_chunks(p, b, p->L, p->a[0], warps));

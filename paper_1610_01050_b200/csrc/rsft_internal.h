@@ -15,6 +15,7 @@ namespace rsft {
 constexpr int kMaxDim = 3;
 constexpr int kMaxLoops = 64;         // L <= 63: 6 bit planes of vote counts
 constexpr int kMaxLaunchLoops = 32;   // loops per fold launch (more loops: several passes)
+constexpr int kSizingSms = 148;     // host-only plan: workspace sized for a B200 (rsft.h)
 constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
 constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detection bitmap
 constexpr int kThreads = 256;          // CTA size of most kernels
