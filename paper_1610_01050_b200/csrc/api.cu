@@ -22,6 +22,7 @@ rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int
 rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
                            int64_t capacity, int64_t* d_count, cudaStream_t st);
 rsft_status upload_twiddles(cudaStream_t st);
+rsft_status upload_bartlett_twiddles(cudaStream_t st);   // bartlett.cu
 rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                   int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st);
 
@@ -101,6 +102,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
     if ((s = cuda_check(cudaMemcpyAsync(base + p->ws.xmask_off, p->xmask.data(), p->ws.xmask_bytes,
                                         cudaMemcpyHostToDevice, st), "upload vote masks"))) return s;
   if ((s = upload_twiddles(st))) return s;
+  if ((s = upload_bartlett_twiddles(st))) return s;
   if ((s = cuda_check(cudaStreamSynchronize(st), "bind sync"))) return s;   // tables are host temporaries
 
   PlanDev& pd = p->dev;

@@ -130,6 +130,14 @@ __global__ void __launch_bounds__(kBartThreads) k_bart_inner(PlanDev pd, BartGeo
 // DIF across the lanes (xor shuffles).  On return lane p holds v[r] = X[brev_M(r) + M brev5(p)].
 // t = half-circle table e^{-j 2 pi k / 4096}, k < 2048, in shared memory.
 // ---------------------------------------------------------------------------------------
+__constant__ float2 c_btw[2048];                       // e^{-j 2 pi k / 4096}, k < 2048 (set at bind)
+
+// compile-time twiddle indices: the constant bank (folds into the FFMA operands)
+__device__ __forceinline__ float2 bart_twc(int j, int lgn) {
+  const int i = (j << (12 - lgn)) & 4095;
+  const float2 w = c_btw[i & 2047];
+  return i < 2048 ? w : make_float2(-w.x, -w.y);
+}
 __device__ __forceinline__ float2 bart_twn(const float2* t, int j, int lgn) {
   const int i = (j << (12 - lgn)) & 4095;
   const float2 w = t[i & 2047];
@@ -154,7 +162,7 @@ __device__ __forceinline__ void bart_warp_fft(float2 (&v)[M], int lane, int lgn,
       const float2 a = v[blk + j], b = v[blk + j + span];
       v[blk + j] = make_float2(a.x + b.x, a.y + b.y);
       const float2 d = make_float2(a.x - b.x, a.y - b.y);
-      v[blk + j + span] = j == 0 ? d : bart_cmul(d, bart_twn(t, j * (16 * M / span), lgn));
+      v[blk + j + span] = j == 0 ? d : bart_cmul(d, bart_twc(j * (16 * M / span), lgn));
     }
   }
   if (M > 1) {                                        // W_n^{lane q1}, q1 = brev(r), by recurrence
@@ -317,10 +325,22 @@ __global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __r
     for (int s = 0; s < T; ++s) {
       __syncthreads();
       const float2* src = scratch + ((size_t)frame * T + s) * ntot + c0;
-      for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) {
-        const int r = e >> 3, c = e & 7;
-        tile[r * st + c] = src[(size_t)r * inner + c];
+      // 16-B loads (two adjacent columns of one row), all of a thread's loads in flight at once
+      constexpr int NQ = n0 * C / 2 / 256;             // 16-B chunks per thread (blockDim 256)
+      float4 q[NQ > 0 ? NQ : 1];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int qi = threadIdx.x + 256 * j, r = qi >> 2, c2 = (qi & 3) * 2;
+        q[j] = __ldcs(reinterpret_cast<const float4*>(src + (size_t)r * inner + c2));
       }
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int qi = threadIdx.x + 256 * j, r = qi >> 2, c2 = (qi & 3) * 2;
+        tile[r * st + c2] = make_float2(q[j].x, q[j].y);
+        tile[r * st + c2 + 1] = make_float2(q[j].z, q[j].w);
+      }
+      if (NQ == 0)
+        for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) tile[(e >> 3) * st + (e & 7)] = src[(size_t)(e >> 3) * inner + (e & 7)];
       __syncthreads();
       float2 v[M0];
 #pragma unroll
@@ -344,6 +364,14 @@ __global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __r
       }
     }
   }
+}
+
+rsft_status upload_bartlett_twiddles(cudaStream_t st) {
+  float2 tw[2048];
+  for (int k = 0; k < 2048; ++k)
+    tw[k] = make_float2((float)std::cos(-2.0 * M_PI * k / 4096.0), (float)std::sin(-2.0 * M_PI * k / 4096.0));
+  return cudaMemcpyToSymbolAsync(c_btw, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st) == cudaSuccess ? RSFT_OK
+                                                                                                   : RSFT_E_CUDA;
 }
 
 }  // namespace rsft

@@ -704,7 +704,10 @@ template <int LP, int U, int RPW>
 __global__ void __launch_bounds__(kThreadsSplit, LP >= 24 ? 1 : kCtasSplit)
 k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch,
              int a0_base, int a0_count, int lg_chunk, float2* __restrict__ R, uint32_t* __restrict__ zero_bm,
-             int64_t zero_words) {
+             int64_t zero_words, int seg_L) {
+  // seg_L > 0 (segment mode): `batch` counts (frame, segment) pseudo-frames f L + s, each
+  // folded for the single loop l0 + s (nl == 1); the tables then hold all seg_L loops
+  const int LT = seg_L > 0 ? seg_L : LP;             // loops in the column-weight / DFT tables
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int S = kStagesSplit;
@@ -751,32 +754,34 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   // column weights h_last[l0 + l][col] for the whole launch in shared memory (if small):
   // rows l >= nl are zero (padded loops)
   const float* hl_smem = nullptr;
-  if ((size_t)LP * nlast * 4 <= kSplitHlastBytes) {
+  const int LH = seg_L > 0 ? seg_L + LP : LP;        // rows (segment mode: + LP zero rows)
+  const int nlh = seg_L > 0 ? seg_L : nl;
+  if ((size_t)LH * nlast * 4 <= kSplitHlastBytes) {
     float* t = reinterpret_cast<float*>(smem + (size_t)nwarps * wl.total);
-    for (int i = threadIdx.x; i < LP * nlast; i += blockDim.x) {
+    for (int i = threadIdx.x; i < LH * nlast; i += blockDim.x) {
       const int l = i / nlast, c = i - l * nlast;
-      t[i] = l < nl ? pd.h[D - 1][(size_t)(l0 + l) * nlast + c] : 0.f;
+      t[i] = l < nlh ? pd.h[D - 1][(size_t)(l0 + l) * nlast + c] : 0.f;
     }
     __syncthreads();
     hl_smem = t;
   }
   float2* tws = reinterpret_cast<float2*>(smem + (size_t)nwarps * wl.total +
-                                         ((size_t)LP * nlast * 4 <= kSplitHlastBytes ? (size_t)LP * nlast * 4 : 0));
+                                         ((size_t)LH * nlast * 4 <= kSplitHlastBytes ? (size_t)LH * nlast * 4 : 0));
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tws[i] = c_tw128[i];
   __syncthreads();
   // last-dim DFT factors e^{-j pi b_l(r) (2k + 1) / B} [or e^{-j 2 pi b_l(r) k / B}],
   // b_l(r) = sigma^{-1}(r - tau) mod B_last, as (T, jT) float4 [r][l][k] (I3, L1)
   const int dl = D - 1, lgbl = pd.lgb[dl], shl = pd.shift[dl];
   const float4* dtab = nullptr;
-  if ((size_t)LP * blast * blast * 16 <= kSplitDftBytes) {
+  if ((size_t)LT * blast * blast * 16 <= kSplitDftBytes) {
     float4* t = reinterpret_cast<float4*>(tws + 128);
     const int m2 = shl ? 2 * blast - 1 : blast - 1;
     const int tsh = shl ? 6 - lgbl : 7 - lgbl;
-    for (int i = threadIdx.x; i < LP * blast * blast; i += blockDim.x) {
-      const int r = i / (LP * blast), rem = i - r * (LP * blast);
+    for (int i = threadIdx.x; i < LT * blast * blast; i += blockDim.x) {
+      const int r = i / (LT * blast), rem = i - r * (LT * blast);
       const int l = rem >> lgbl, k = rem & (blast - 1);
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (l < nl) {
+      if (l < nlh) {
         const LoopDev& lp = pd.loops[l0 + l];
         const int b = (lp.sinv[dl] * (r - lp.tau[dl])) & (blast - 1);
         const float2 w = tws[((b * (shl ? 2 * k + 1 : k)) & m2) << tsh];
@@ -810,9 +815,11 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
   };
   // stage h0[l0 + l][(a0_base + chunk A0c + a) B0 + r0] (a < A0c) [and h1[l0 + l][r1 + B1 a1]]
   // from the class-major tables into hs with an LP row stride (cp.async, waited per unit)
-  const bool stage16 = ((nl | l0 | pd.L) & 3) == 0;
+  const bool stage16 = seg_L == 0 && ((nl | l0 | pd.L) & 3) == 0;
+  auto uloop = [&](const Unit& t) { return seg_L > 0 ? l0 + t.frame % seg_L : l0; };   // unit's first loop
   auto stage = [&](const Unit& t, float* h) {
-    const float* s0 = pd.ht[0] + ((size_t)t.r0 * A0 + a0_base + t.chunk * A0c) * pd.L + l0;
+    const int lu = uloop(t);
+    const float* s0 = pd.ht[0] + ((size_t)t.r0 * A0 + a0_base + t.chunk * A0c) * pd.L + lu;
     if (stage16) {                                   // 16-B copies: rows of nl loops, 16-B aligned
       const int nl4 = nl >> 2;
       for (int i = lane; i < A0c * nl4; i += 32) {
@@ -820,7 +827,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
         cp_async16(h + a * LP + l, s0 + (size_t)a * pd.L + l);
       }
       if (D == 3) {
-        const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + l0;
+        const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + lu;
         float* h1 = h + A0c * LP;
         for (int i = lane; i < A1 * nl4; i += 32) {
           const int a = i / nl4, l = (i - a * nl4) << 2;
@@ -834,7 +841,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
       cp_async4(h + a * LP + l, s0 + (size_t)a * pd.L + l);
     }
     if (D == 3) {
-      const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + l0;
+      const float* s1 = pd.ht[1] + (size_t)t.r1 * A1 * pd.L + lu;
       float* h1 = h + A0c * LP;
       for (int i = lane; i < A1 * nl; i += 32) {
         const int a = i / nl, l = i - a * nl;
@@ -1010,8 +1017,9 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
         }
       }
       // column weights of this segment + cross-lane residue fold -> slot[l][r] (segments add)
-      if (hl_smem) colweight_plain<LP>(acc, hl_smem, nlast, seg * 64 + 2 * lane_c4);
-      else colweight<LP>(acc, hlast, l0, nl, nlast, seg * 64 + 2 * lane_c4);
+      const int lofs = uloop(t) - l0;                // segment mode: the unit's loop
+      if (hl_smem) colweight_plain<LP>(acc, hl_smem + (size_t)lofs * nlast, nlast, seg * 64 + 2 * lane_c4);
+      else colweight<LP>(acc, hlast, l0 + lofs, nl, nlast, seg * 64 + 2 * lane_c4);
       if (LP <= kUSplit && blast >= 2 && blast <= 32) {
         fold_smem<LP>(acc, ring + (size_t)((c_st + S - 1) % S) * U * 32, slot, lane, blast, lgbl - 1, nl, seg == 0);
         continue;
@@ -1038,12 +1046,12 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
       for (int i = lane; i < nl * blast; i += 32) {
         const int l = i >> lgbl, k = i & (blast - 1);
         const float2* row = slot + l * blast;
-        const float4* tk = dtab + l * blast + k;
+        const float4* tk = dtab + (l + uloop(t) - l0) * blast + k;
         float2 v = make_float2(0.f, 0.f);
 #pragma unroll 8
         for (int r = 0; r < blast; ++r) {
           const float2 x = row[r];
-          const float4 w = tk[r * LP * blast];
+          const float4 w = tk[r * LT * blast];
           v = __ffma2_rn(make_float2(x.x, x.x), make_float2(w.x, w.y), v);
           v = __ffma2_rn(make_float2(x.y, x.y), make_float2(w.z, w.w), v);
         }
@@ -1055,7 +1063,7 @@ k_split_fold(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int n
       const int tsh = shl ? 6 - lgbl : 7 - lgbl;
       for (int i = lane; i < nl * blast; i += 32) {
         const int l = i >> lgbl, k = i & (blast - 1);
-        const LoopDev& lp = pd.loops[l0 + l];
+        const LoopDev& lp = pd.loops[uloop(t) + l];
         const float2* row = slot + l * blast;
         // twiddle index b(r) (2k + 1) mod 2B [or b(r) k mod B], b(r) = sigma^{-1} (r - tau) mod B
         const int f = shl ? 2 * k + 1 : k;
@@ -1446,7 +1454,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
 __global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const float2* __restrict__ F, int rl0,
                                                            int rnl, int nchunk, int l0, int nl,
                                                            uint32_t* __restrict__ bitmaps,
-                                                           float2* __restrict__ spectra) {
+                                                           float2* __restrict__ spectra, int seg_L) {
   pdl_enter();
   extern __shared__ float4 smem_f4[];
   float2* tw = reinterpret_cast<float2*>(smem_f4);
@@ -1460,7 +1468,8 @@ __global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const flo
   const int vstride = b1 + 1;                        // padded rows [B0][B1+1]
   const int lgb0 = pd.lgb[0], lgb1 = D == 3 ? pd.lgb[1] : 0;
   const int bouter = pd.bouter;
-  const LoopDev& lp = pd.loops[l0 + l];
+  // segment mode: pseudo-frame f L + s runs loop l0 + s (nl == rnl == 1)
+  const LoopDev& lp = pd.loops[seg_L > 0 ? l0 + (int)(frame % seg_L) : l0 + l];
   const float2* src = F + ((((size_t)frame * rnl + (l0 + l - rl0)) * blast + kl) * nchunk) * bouter;
   load_twiddles(tw);
   __syncthreads();
@@ -1662,8 +1671,8 @@ static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t bat
 template <int LP>
 static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl,
                                        int64_t a0_base, int64_t a0_count, int* lg_out, uint32_t* zero_bm,
-                                       int64_t zero_words, cudaStream_t st) {
-  if (LP <= kMmaLP && mma_fold_ok(p, batch, l0, nl, a0_count)) {
+                                       int64_t zero_words, cudaStream_t st, int seg_L = 0) {
+  if (seg_L == 0 && LP <= kMmaLP && mma_fold_ok(p, batch, l0, nl, a0_count)) {
     *lg_out = 0;
     return launch_split_mma(p, d_x, batch, l0, nl, a0_base, a0_count, zero_bm, zero_words, st);
   }
@@ -1674,10 +1683,10 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
   if (batch * per > p->dev.fbuf_capacity) { set_error("split fold: batch exceeds the workspace"); return RSFT_E_ARG; }
   // more chunks if the per-warp weight tables do not fit (smaller dim-0 chunk per unit)
   const int64_t amin = p->D == 3 ? 1 : (int64_t)kUSplit * (p->n[p->D - 1] >= 64 ? 1 : 64 / p->n[p->D - 1]);
-  while (split_smem_bytes(p, nl, LP, a0_count >> lg) > 227 * 1024 && (a0_count >> (lg + 1)) >= amin &&
+  while (split_smem_bytes(p, nl, LP, a0_count >> lg, seg_L) > 227 * 1024 && (a0_count >> (lg + 1)) >= amin &&
          (batch << (lg + 1)) * per <= p->dev.fbuf_capacity)
     ++lg;
-  const size_t smem = split_smem_bytes(p, nl, LP, a0_count >> lg);
+  const size_t smem = split_smem_bytes(p, nl, LP, a0_count >> lg, seg_L);
   if (smem > 227 * 1024) { set_error("k_split_fold: tables beyond shared memory"); return RSFT_E_UNSUPPORTED; }
   CUtensorMap tmap;
   const int rpw = p->n[p->D - 1] >= 64 ? 1 : (int)(64 / p->n[p->D - 1]);
@@ -1707,7 +1716,7 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
   const int64_t need = (wunits + kThreadsSplit / 32 - 1) / (kThreadsSplit / 32);
   if (grid > need) grid = need;
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreadsSplit, smem, st, p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count, lg,
-                                                    p->dev.fbuf, zero_bm, zero_words); le_ != cudaSuccess)
+                                                    p->dev.fbuf, zero_bm, zero_words, seg_L); le_ != cudaSuccess)
     return check(le_, "kern launch");
   p->last_launches += 1;
   *lg_out = lg;
@@ -1716,7 +1725,7 @@ static rsft_status launch_split_fold_t(rsft_plan_s* p, const void* d_x, int64_t 
 
 // Folded spectra F (loops [rl0, rl0 + rnl), nchunk chunks) -> bitmaps / spectra of loops [l0, l0 + nl).
 static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, int rnl, int nchunk, int64_t batch,
-                                    int l0, int nl, uint32_t* bm, void* spectra, cudaStream_t st) {
+                                    int l0, int nl, uint32_t* bm, void* spectra, cudaStream_t st, int seg_L = 0) {
   const int D = p->D;
   const int64_t blast = p->b[D - 1];
   const int64_t b1 = D == 3 ? p->b[1] : 1;
@@ -1732,7 +1741,7 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
   if (threads <= 0) threads = p->dev.bouter >= 2048 ? kThreadsFft : (int)std::max<int64_t>(64, p->dev.bouter / 4);
   threads = std::min(threads, kThreadsFft);
   if (cudaError_t le_ = pdl_launch(k_split_fft, grid2, (unsigned)threads, smem2, st, p->dev, F, rl0, rnl, nchunk, l0, nl, bm,
-                                                 reinterpret_cast<float2*>(spectra)); le_ != cudaSuccess)
+                                                 reinterpret_cast<float2*>(spectra), seg_L); le_ != cudaSuccess)
     return check(le_, "k_split_fft launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_fft launch");
@@ -1817,9 +1826,16 @@ rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint
   if (resolve_mode(p, batch) == RSFT_MODE_FUSED && loop_pad(1) == 2) {
     return launch_segments_fused_t<2>(p, d_x, batch, bm, spectra, st);
   }
-  // split mode: one launch per (frame, segment) on the contiguous segment
+  // split mode: the batch x L segments are batch L contiguous pseudo-frames f L + s, each
+  // folded for loop s (one fold + one outer-FFT launch for the whole step)
   const int64_t L = p->L, wpl = p->dev.wpl;
-  for (int64_t f = 0; f < batch; ++f)
+  if (L <= kMaxLaunchLoops && batch * L * p->btot <= p->dev.fbuf_capacity) {
+    int lg = 0;
+    rsft_status s = launch_split_fold_t<2>(p, d_x, batch * L, 0, 1, 0, p->a[0], &lg, bm, batch * L * wpl, st, (int)L);
+    if (s) return s;
+    return launch_split_fft(p, p->dev.fbuf, 0, 1, 1 << lg, batch * L, 0, 1, bm, spectra, st, (int)L);
+  }
+  for (int64_t f = 0; f < batch; ++f)               // fallback: one launch per (frame, segment)
     for (int64_t l = 0; l < L; ++l) {
       const char* x = reinterpret_cast<const char*>(d_x) + (size_t)(f * L + l) * p->ntot * 8;
       void* sp = spectra ? reinterpret_cast<char*>(spectra) + (size_t)(f * L + l) * p->btot * 8 : nullptr;

@@ -256,14 +256,14 @@ size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
   return ring + fbytes + (size_t)(n0 + 1) * lpad * 4;
 }
 
-size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c) {
+size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c, int seg_L) {
   const int D = p->D;
   const int64_t nlast = p->n[D - 1];
   const int nseg = nlast >= 64 ? (int)(nlast / 64) : 1;
   SplitWarpLayout w = split_warp_layout(D, lpad, nl, (int)a0c, D == 3 ? (int)p->a[1] : 1, (int)p->b[D - 1], nseg,
                                         nlast >= 64 ? 1 : (int)(64 / nlast));
-  const size_t hl = (size_t)lpad * nlast * 4;
-  const size_t dft = (size_t)lpad * p->b[D - 1] * p->b[D - 1] * 16;
+  const size_t hl = (size_t)(seg_L > 0 ? seg_L + lpad : lpad) * nlast * 4;     // segment mode: all loops
+  const size_t dft = (size_t)(seg_L > 0 ? seg_L : lpad) * p->b[D - 1] * p->b[D - 1] * 16;
   return (size_t)(kThreadsSplit / 32) * w.total + (hl <= (size_t)kSplitHlastBytes ? hl : 0) + 128 * 8 +
          (dft <= (size_t)kSplitDftBytes ? dft : 0);
 }

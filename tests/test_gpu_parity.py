@@ -389,6 +389,8 @@ def test_variant_b_c5_full_cube():
     ((1024,), (64,), 50, "fused"),                  # the paper's T = 50
     ((1024,), (32,), 4, "fused"),
     ((32, 16, 64), (4, 4, 8), 3, "split"),
+    ((64, 128, 32), (8, 16, 8), 4, "split"),          # c3-like: multi-a0 boxes, batched segments
+    ((128, 64), (16, 16), 3, "split"),                # D = 2 split, batched segments
 ])
 def test_segment_mode_parity(n, b, L, mode):
     """Segment mode (P:204): loop l folds segment l of each frame (rsft_execute_segments);
