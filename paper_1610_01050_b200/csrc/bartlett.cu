@@ -149,6 +149,49 @@ __device__ __forceinline__ float2 bart_cmul(float2 a, float2 b) {
 constexpr int bart_lg(int m) { return m <= 1 ? 0 : 1 + bart_lg(m / 2); }
 __device__ __forceinline__ int bart_brev_c(int v, int lg) { return lg ? (int)(__brev((unsigned)v) >> (32 - lg)) : 0; }
 
+// in-lane M-point DIF (natural in, bit-reversed out); twiddles W_{2 span}^j from the constant
+// bank, indexed as W_n^{j n / (2 span)} with n = 32 M (lgn = log2 n)
+template <int M>
+__device__ __forceinline__ void bart_lane_dif(float2 (&v)[M], int lgn) {
+  constexpr int LM = bart_lg(M);
+#pragma unroll
+  for (int s = 0; s < LM; ++s) {
+#pragma unroll
+    for (int e = 0; e < M / 2; ++e) {
+      const int span = M >> (s + 1);
+      const int j = e & (span - 1), blk = (e / span) * 2 * span;
+      const float2 a = v[blk + j], b = v[blk + j + span];
+      v[blk + j] = make_float2(a.x + b.x, a.y + b.y);
+      const float2 d = make_float2(a.x - b.x, a.y - b.y);
+      v[blk + j + span] = j == 0 ? d : bart_cmul(d, bart_twc(j * (16 * M / span), lgn));
+    }
+  }
+}
+
+// 1024-point FFT of a warp's line with a shared-memory transpose instead of cross-lane shuffles:
+// in-lane 32-point DIF over k, twiddles W_1024^{l q1}, transpose through the warp's 32 x 33
+// scratch xs (lane q1 then holds Y_l[q1] for all l), in-lane 32-point DIF over l.
+// On return lane q1 holds v[r] = X[q1 + 32 brev5(r)].
+__device__ __forceinline__ void bart_warp_fft1024(float2 (&v)[32], int lane, const float2* __restrict__ t,
+                                                  float2* __restrict__ xs) {
+  bart_lane_dif<32>(v, 10);
+  const float2 w1 = bart_twn(t, lane, 10);
+  float2 cur = w1;
+#pragma unroll
+  for (int q1 = 1; q1 < 32; ++q1) {
+    const int r = bart_brev_c(q1, 5);
+    v[r] = bart_cmul(v[r], cur);
+    cur = bart_cmul(cur, w1);
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) xs[bart_brev_c(r, 5) * 33 + lane] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; ++l) v[l] = xs[lane * 33 + l];
+  __syncwarp();
+  bart_lane_dif<32>(v, 10);
+}
+
 template <int M>
 __device__ __forceinline__ void bart_warp_fft(float2 (&v)[M], int lane, int lgn, const float2* __restrict__ t,
                                               const float2 (&stw)[5]) {
@@ -309,6 +352,7 @@ __global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __r
   float2* t = bc;                                      // [2048]
   float2* tile = t + 2048;                             // [n0][9]
   constexpr int n0 = 32 * M0, C = 8, st = C + 1;
+  float2* xs = tile + n0 * st + (threadIdx.x >> 5) * (32 * 33);   // M0 == 32: transpose scratch
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -345,13 +389,15 @@ __global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __r
       float2 v[M0];
 #pragma unroll
       for (int k = 0; k < M0; ++k) v[k] = tile[(lane + 32 * k) * st + warp];
-      bart_warp_fft<M0>(v, lane, lgn0, t, stw);
+      if constexpr (M0 == 32) bart_warp_fft1024(reinterpret_cast<float2 (&)[32]>(v), lane, t, xs);
+      else bart_warp_fft<M0>(v, lane, lgn0, t, stw);
 #pragma unroll
       for (int r = 0; r < M0; ++r) acc[r] += v[r].x * v[r].x + v[r].y * v[r].y;
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < M0; ++r) ptile[bart_pos<M0>(r, lane) * C + warp] = acc[r];
+    for (int r = 0; r < M0; ++r)
+      ptile[(M0 == 32 ? lane + 32 * bart_brev_c(r, 5) : bart_pos<M0>(r, lane)) * C + warp] = acc[r];
     __syncthreads();
     float* pdst = power + (size_t)frame * ntot + c0;
     for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) {
@@ -458,7 +504,7 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
         m0 == 1 ? k_bart_cols<1> : m0 == 2 ? k_bart_cols<2> : m0 == 4 ? k_bart_cols<4> : m0 == 8 ? k_bart_cols<8>
       : m0 == 16 ? k_bart_cols<16> : m0 == 32 ? k_bart_cols<32> : nullptr;
     if (!k2 || inner % 8) return RSFT_E_UNSUPPORTED;
-    const size_t smem2 = (2048 + (size_t)nn[0] * 9) * 8;
+    const size_t smem2 = (2048 + (size_t)nn[0] * 9 + (m0 == 32 ? 8 * 32 * 33 : 0)) * 8;
     if (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess)
       return RSFT_E_CUDA;
     int nb = 1;
