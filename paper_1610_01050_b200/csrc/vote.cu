@@ -1206,6 +1206,9 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* __restrict
 
 // ------------------------------------------------------------------------------------
 // Host launchers
+rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
+                           int64_t capacity, int64_t* d_count, cudaStream_t st);
+
 static int64_t vote_regions_per_frame(const rsft_plan_s* p, int64_t d0b, int64_t d0e) {
   return p->D == 3 ? d0e - d0b : 1;
 }
@@ -1401,6 +1404,16 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   const bool v1 = vote1d_ok(p, nullptr);
   const bool v3 = !v1 && vote3d_ok(p, batch, 0, n0, nullptr);
   const bool v2 = !v1 && !v3 && vote2d_ok(p, 0, n0, nullptr);
+  {
+    // RSFT_COMPACT=1 (read per launch): plain vote, then the single-pass look-back compaction
+    // of the detection words (k_compact) instead of per-region counts / lists + scan + writer
+    const char* cm = getenv("RSFT_COMPACT");
+    if (cm && cm[0] == '1') {
+      rsft_status s = launch_detect(p, bm, batch, 0, n0, det, nullptr, st);
+      if (s) return s;
+      return launch_compact(p, det, batch, idx, capacity, d_count, st);
+    }
+  }
   const bool list = p->dev.region_slots && (v1 || v2 || v3 || rows * (W / cw) <= (int64_t)kListIpt * kThreads);
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
