@@ -412,6 +412,72 @@ __global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __r
   }
 }
 
+// Single pass for 1-D frames of N = R C samples, 1024 <= N <= 4096 (c1): the four-step FFT with
+// warp-register FFTs.  n = C r + c; R-point DFTs down the columns (warp per column), twiddles
+// W_N^{c k1}, C-point DFTs along the rows (warp per row): X[k1 + R k2].  One CTA per frame streams
+// the T segments (window on load) and keeps |X|^2 in shared memory; power and detection words
+// are written once (T N 8 B read, N 4 B written).  Padded rows keep the column accesses
+// conflict-free.
+template <int MR, int MC>
+__global__ void __launch_bounds__(256) k_bart_1d(PlanDev pd, const float2* __restrict__ x, int64_t batch, int T,
+                                                 const float* __restrict__ w0, float* __restrict__ power, float scale,
+                                                 float gamma, uint32_t* __restrict__ det) {
+  extern __shared__ __align__(16) float2 b1[];
+  constexpr int R = 32 * MR, C = 32 * MC, N = R * C, st = C + 1;
+  constexpr int lgR = bart_lg(R), lgC = bart_lg(C), lgN = lgR + lgC;
+  float2* t = b1;                                      // [2048]
+  float2* tile = t + 2048;                             // [R][C + 1]
+  float* pw = reinterpret_cast<float*>(tile + R * st); // [R][C + 1]
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float2 stw[5];
+  bart_stw(stw, lane, t);
+  for (int64_t frame = blockIdx.x; frame < batch; frame += gridDim.x) {
+    for (int e = threadIdx.x; e < R * st; e += blockDim.x) pw[e] = 0.f;
+    for (int s = 0; s < T; ++s) {
+      __syncthreads();
+      const float2* src = x + ((size_t)frame * T + s) * N;
+      for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        const float2 a = src[n];
+        const float w = w0[n];
+        tile[(n >> lgC) * st + (n & (C - 1))] = make_float2(a.x * w, a.y * w);
+      }
+      __syncthreads();
+      for (int c = warp; c < C; c += nw) {             // R-point DFTs down the columns
+        float2 v[MR];
+#pragma unroll
+        for (int j = 0; j < MR; ++j) v[j] = tile[(lane + 32 * j) * st + c];
+        bart_warp_fft<MR>(v, lane, lgR, t, stw);
+#pragma unroll
+        for (int r = 0; r < MR; ++r) {
+          const int k1 = bart_pos<MR>(r, lane);
+          tile[k1 * st + c] = bart_cmul(v[r], bart_twn(t, (c * k1) & (N - 1), lgN));
+        }
+      }
+      __syncthreads();
+      for (int k1 = warp; k1 < R; k1 += nw) {          // C-point DFTs along the rows
+        float2 v[MC];
+#pragma unroll
+        for (int j = 0; j < MC; ++j) v[j] = tile[k1 * st + lane + 32 * j];
+        bart_warp_fft<MC>(v, lane, lgC, t, stw);
+#pragma unroll
+        for (int r = 0; r < MC; ++r) pw[k1 * st + bart_pos<MC>(r, lane)] += v[r].x * v[r].x + v[r].y * v[r].y;
+      }
+    }
+    __syncthreads();
+    float* pdst = power + (size_t)frame * N;
+    uint32_t* ddst = det ? det + (size_t)frame * (N >> 5) : nullptr;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {        // X[k1 + R k2] -> natural order
+      const float p = pw[(k & (R - 1)) * st + (k >> lgR)];
+      pdst[k] = p;
+      const unsigned word = __ballot_sync(0xffffffffu, p * scale > gamma);
+      if (ddst && lane == 0) ddst[k >> 5] = word;
+    }
+    __syncthreads();
+  }
+}
+
 rsft_status upload_bartlett_twiddles(cudaStream_t st) {
   float2 tw[2048];
   for (int k = 0; k < 2048; ++k)
@@ -454,7 +520,24 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
   const bool single = ntot <= kBartTile;
   if (!single && (inner > kBartTile || !d_scratch)) return RSFT_E_UNSUPPORTED;
   const size_t tw_bytes = 2048 * 8;
-  if (single) {
+  if (p->D == 1 && ntot >= 1024 && ntot <= 4096) {   // four-step warp FFTs, one pass
+    const int lg = __builtin_ctzll(ntot), lr = lg / 2, lc = lg - lr;
+    void (*k)(PlanDev, const float2*, int64_t, int, const float*, float*, float, float, uint32_t*) = nullptr;
+    if (lr == 5 && lc == 5) k = k_bart_1d<1, 1>;
+    if (lr == 5 && lc == 6) k = k_bart_1d<1, 2>;
+    if (lr == 6 && lc == 6) k = k_bart_1d<2, 2>;
+    if (!k) return RSFT_E_UNSUPPORTED;
+    const int R = 1 << lr, C = 1 << lc;
+    const size_t smem = 2048 * 8 + (size_t)R * (C + 1) * 12;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return RSFT_E_CUDA;
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, smem);
+    const int64_t grid = std::min<int64_t>(batch, (int64_t)std::max(nb, 1) * p->num_sms);
+    k<<<(unsigned)grid, 256, smem, st>>>(p->dev, reinterpret_cast<const float2*>(d_x), batch, segments, wr[0], d_power,
+                                          scale, gam, d_detect);
+    p->last_launches = 1;
+  } else if (single) {
     const size_t smem = tw_bytes + (size_t)kBartTile * 8 + (size_t)ntot * 4;
     if (cudaFuncSetAttribute(k_bart_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return RSFT_E_CUDA;
