@@ -62,7 +62,7 @@ def test_roc_monotone():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,batch", [((1024,), 3), ((256, 128), 2), ((64, 32, 32), 2), ((4096,), 3), ((128, 64), 3),
-                                     ((2048,), 2), ((512,), 2), ((8192,), 2),
+                                     ((2048,), 2), ((512,), 2),
                                      ((1024, 256), 2), ((512, 128, 32), 1)])
 def test_bartlett_gpu_parity(n, batch):
     """Single-pass (<= 8192 samples) and two-pass frames, several frames per call, against the
