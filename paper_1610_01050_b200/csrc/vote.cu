@@ -1308,8 +1308,10 @@ static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t bat
 static bool vote3d_ok(const rsft_plan_s* p, int64_t batch, int64_t d0b, int64_t d0e, uint8_t* counts) {
   const char* off = getenv("RSFT_NO_VOTE3D");        // read per launch: tests select either kernel
   if (off && off[0] && off[0] != '0') return false;
+  const char* on = getenv("RSFT_VOTE3D");            // force for larger planes (measurement)
+  const int64_t lim = on && on[0] == '1' ? (int64_t)1 << 20 : 256;
   return p->D == 3 && !counts && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
-         (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= 256 && p->L <= 32;
+         (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= lim && p->L <= 32;
 }
 
 static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
