@@ -593,13 +593,15 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
       cmask |= 1u << bl;
       ncand += best;
     }
+    // filter loop lf (mu = L): its mask and sigma in plain registers (no per-test loop select)
     int lf = -1;
+    uint32_t flo = 0xffffffffu, fhi = 0xffffffffu, fsg = 0u;
     if (mu == L && L > 1) {
       int best = 1 << 30;
 #pragma unroll
       for (int l = 0; l < LP; ++l) {
         const int pc = __popc(mlo[l]) + __popc(mhi[l]);
-        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; lf = l; }
+        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; lf = l; flo = mlo[l]; fhi = mhi[l]; fsg = (uint32_t)sg[l]; }
       }
     }
     if (2 * ncand * A <= N) {                         // ---- candidate mode
@@ -634,9 +636,10 @@ __global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const 
         const uint32_t i = ((uint32_t)sinv_s[e >> 8] * u) & nm;          // Def. 4
         // mu = L: a location needs the filter loop's vote too (cheap pre-test, then queue)
         bool pass = valid;
-#pragma unroll
-        for (int l = 0; l < LP; ++l)
-          if (l == lf) pass = pass && vote(l, i);
+        if (lf >= 0) {
+          const uint32_t k = ((fsg * i) & nm) >> lga;
+          pass = pass && (((k < 32 ? flo : fhi) >> (k & 31)) & 1u);
+        }
         const uint32_t bal = __ballot_sync(0xffffffffu, pass);
         if (pass) q[qn + __popc(bal & lt)] = i;
         qn += __popc(bal);
