@@ -382,7 +382,7 @@ def main_gpu(a):
         "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(wl.name),
-                     "kernel": "k_fused (pre-window+permute+flat window+fold+FFT+threshold)",
+                     "kernel": fold_kernel_label(plan, wl),
                      "algorithmic_bytes_per_launch": algo_bytes,
                      "avg_launch_ms": k1_avg, "share_of_step": k1_avg / step_ms, "peak_source": peak_src},
         "gpu_launches": launches,
@@ -397,6 +397,17 @@ def main_gpu(a):
     if pg:
         dist.destroy_process_group()
     return 0
+
+
+def fold_kernel_label(plan, wl):
+    """The first-stage kernel(s) rsft_execute launches for this plan (librsft's dispatch rules)."""
+    if plan.mode == 2:
+        mma = (len(wl.n) == 3 and wl.n[2] == 64 and not os.environ.get("RSFT_NO_MMA"))
+        return ("k_split_mma (3xTF32 tcgen05)" if mma else "k_split_fold") + " + k_split_fft (fold + outer FFT + threshold)"
+    w = (wl.support[0] if wl.support else 0) or wl.n[0]
+    if len(wl.n) == 1 and w % 32 == 0 and w <= 1024 and not os.environ.get("RSFT_NO_GATHER1D"):
+        return "k_gather1d (gather-form fold + FFT + threshold)"
+    return "k_fused (pre-window+permute+flat window+fold+FFT+threshold)"
 
 
 def cpu_baseline(wl, budget):
