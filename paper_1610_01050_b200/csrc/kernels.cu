@@ -1609,7 +1609,17 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
                              sp_stride ? sp_stride : (int64_t)nl * p->btot);
   }
   auto kern = p->D == 2 ? k_fused<LP, F2.u, F2.stages, F2.threads, F2.ctas> : k_fused<LP, F1.u, F1.stages, F1.threads, F1.ctas>;
-  const size_t smem = fused_smem_bytes(p, nl, LP);
+  size_t smem = fused_smem_bytes(p, nl, LP);
+  {
+    // D = 2 frames whose tables leave room: a third ring stage per warp keeps a box in flight
+    // through the per-frame epilogue (RSFT_F2_STAGES=2 keeps two)
+    const char* es = getenv("RSFT_F2_STAGES");
+    const size_t s3 = fused_smem_bytes(p, nl, LP, F2.stages + 1);
+    if (p->D == 2 && s3 <= 227 * 1024 && !(es && es[0] == '2')) {
+      kern = k_fused<LP, F2.u, F2.stages + 1, F2.threads, F2.ctas>;
+      smem = s3;
+    }
+  }
   if (bm_stride == 0) bm_stride = (int64_t)nl * p->dev.wpl;
   if (sp_stride == 0) sp_stride = (int64_t)nl * p->btot;
   CUtensorMap tmap;

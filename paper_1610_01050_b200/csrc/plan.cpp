@@ -243,8 +243,9 @@ void layout_workspace(rsft_plan_s* p) {
 }
 
 // Shared-memory footprints (must match the carve-up at the top of k_fused / k_split_fold).
-size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad) {
-  const FusedCfg fc = fused_cfg(p->D);
+size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int stages) {
+  FusedCfg fc = fused_cfg(p->D);
+  if (stages > 0) fc.stages = stages;
   const int nwarps = fc.threads / 32;
   int64_t blast = p->b[p->D - 1], nlast = p->n[p->D - 1];
   int64_t bouter = p->btot / blast;

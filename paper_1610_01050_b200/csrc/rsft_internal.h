@@ -190,7 +190,7 @@ void layout_workspace(rsft_plan_s* p);
 int resolve_mode(const rsft_plan_s* p, int64_t batch);
 int gather1d_taps(const rsft_plan_s* p);
 int loop_pad(int nl);
-size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad);
+size_t fused_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int stages = 0);
 inline FusedCfg fused_cfg(int D) { return D == 2 ? kFused2D : kFused1D; }
 size_t split_smem_bytes(const rsft_plan_s* p, int nl, int lpad, int64_t a0c, int seg_L = 0);
 int split_lg_chunks(const rsft_plan_s* p, int64_t batch, int nl, int64_t a0_count, int64_t warps_total);
