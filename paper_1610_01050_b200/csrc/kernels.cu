@@ -1137,7 +1137,7 @@ RSFT_HD inline MmaLayout mma_layout(int a0c, int a1, int nlast, int blast) {
   L.e = off; off += kMmaLP * kMmaEStride * 4;
   L.slot = off; off += kMmaLP * blast * 8;
   off = (off + 15) / 16 * 16;
-  L.bar = off; off += (2 * kMmaSX + kMmaSP + 4) * 8;
+  L.bar = off; off += (2 * kMmaSX + 2 * kMmaSP + 4) * 8;
   L.taddr = off; off += 16;
   L.total = off;
   return L;
@@ -1184,7 +1184,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 __global__ void __launch_bounds__(kMmaThreads, 1)
 k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl, int64_t batch, int a0_base,
-            int a0_count, float2* __restrict__ R, uint32_t* __restrict__ zero_bm, int64_t zero_words) {
+            int a0_count, float2* __restrict__ R, uint32_t* __restrict__ zero_bm, int64_t zero_words, int mbar_issue) {
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int LP = kMmaLP;
@@ -1200,6 +1200,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
   uint64_t* opempty = xempty + kMmaSX;
   uint64_t* accfull = opempty + kMmaSP;
   uint64_t* accempty = accfull + 2;
+  uint64_t* opfull = accempty + 2;                     // [kMmaSP]: the 4 group warps' operands written
   uint32_t* taddr_s = reinterpret_cast<uint32_t*>(smem + ly.taddr);
   float* hl = reinterpret_cast<float*>(smem + ly.hl);
   float2* tws = reinterpret_cast<float2*>(smem + ly.tws);
@@ -1220,6 +1221,7 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
     for (int i = 0; i < kMmaNB; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 4 * (kMmaQB / 2)); }  // consuming warps
     for (int i = 0; i < kMmaSP; ++i) mbar_init(&opempty[i], 1);                              // MMA commit
     for (int i = 0; i < 2; ++i) { mbar_init(&accfull[i], 2); mbar_init(&accempty[i], 4); }  // 2 groups / 4 epi warps
+    for (int i = 0; i < kMmaSP; ++i) mbar_init(&opfull[i], 4);                               // group warps
     fence_mbar_init();
   }
   if (warp == kMmaTmem) {
@@ -1338,8 +1340,14 @@ k_split_mma(PlanDev pd, const __grid_constant__ CUtensorMap tmap, int l0, int nl
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");    // W tiles -> tensor core
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        named_bar(2 + grp, 128);                       // the group's operands are complete
+        if (mbar_issue) {                              // only the issuing warp waits for the group
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&opfull[op]);
+        } else {
+          named_bar(2 + grp, 128);                     // the group's operands are complete
+        }
         if (kq == grp) {                               // issuing warp: SMSP 0 (group 0) / 1 (group 1)
+          if (mbar_issue) mbar_wait(&opfull[op], oph);
           if (pl == pl0) mbar_wait(&accempty[buf], (((uint32_t)(ci >> 1)) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #if RSFT_MMA_DEBUG != 3
@@ -1671,8 +1679,10 @@ static rsft_status launch_split_mma(rsft_plan_s* p, const void* d_x, int64_t bat
   if (s) return s;
   const int64_t units = batch * p->dev.bouter;
   const int64_t grid = units < p->num_sms ? units : p->num_sms;
+  const char* mb = getenv("RSFT_MMA_MBAR");             // issue behind an mbarrier (1) or a group barrier (0)
+  const int mbar_issue = mb && mb[0] == '1' ? 1 : 0;
   if (cudaError_t le_ = pdl_launch(k_split_mma, (unsigned)grid, kMmaThreads, smem, st, p->dev, tmap, l0, nl, batch, (int)a0_base, (int)a0_count,
-                                                         p->dev.fbuf, zero_bm, zero_words); le_ != cudaSuccess)
+                                                         p->dev.fbuf, zero_bm, zero_words, mbar_issue); le_ != cudaSuccess)
     return check(le_, "k_split_mma launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_split_mma launch");
