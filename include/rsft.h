@@ -93,6 +93,13 @@ void rsft_default_params(rsft_params* p);
 rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out);
 void rsft_plan_destroy(rsft_plan_t plan);
 
+/* SURVEY §8(b) spelling of the same two calls: rsft_plan(params, device, out) creates the plan
+ * (host only, like rsft_plan_create) and records `device` (>= 0) as the CUDA device rsft_bind
+ * must be called on (rsft_bind returns E_STATE on another current device; -1 = any);
+ * rsft_destroy == rsft_plan_destroy. */
+rsft_status rsft_plan(const rsft_params* params, int32_t device, rsft_plan_t* out);
+void rsft_destroy(rsft_plan_t plan);
+
 /* Replace the seeded schedule.  sigma: [L][D] odd values in [N_d] (Def. 1: sigma invertible
  * mod N_d); tau: [L][D] in [N_d] or NULL (=> 0).  Recomputes tables, beta, gamma and
  * marks the plan unbound.  Errors: E_SIGMA (even sigma), E_ARG. */

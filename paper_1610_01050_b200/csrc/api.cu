@@ -46,6 +46,10 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
   rsft_status s;
   int dev = 0;
   if ((s = cuda_check(cudaGetDevice(&dev), "cudaGetDevice"))) return s;
+  if (p->want_device >= 0 && dev != p->want_device) {
+    set_error("rsft_bind: the plan was created for another device (rsft_plan)");
+    return RSFT_E_STATE;
+  }
   int sms = 0;
   if ((s = cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count"))) return s;
   p->device = dev;

@@ -415,6 +415,15 @@ rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out) {
 
 void rsft_plan_destroy(rsft_plan_t plan) { delete plan; }
 
+rsft_status rsft_plan(const rsft_params* params, int32_t device, rsft_plan_t* out) {
+  if (device < -1) return RSFT_E_ARG;
+  rsft_status s = rsft_plan_create(params, out);
+  if (s == RSFT_OK) (*out)->want_device = device;
+  return s;
+}
+
+void rsft_destroy(rsft_plan_t plan) { rsft_plan_destroy(plan); }
+
 rsft_status rsft_set_schedule(rsft_plan_t p, const int64_t* sigma, const int64_t* tau) {
   if (!p || !sigma) return RSFT_E_ARG;
   for (int l = 0; l < p->L; ++l)

@@ -177,6 +177,7 @@ struct rsft_plan_s {
   // binding
   bool bound = false;
   int device = -1;
+  int want_device = -1;                           // rsft_plan(device): bind only there
   int num_sms = 148;
   void* d_ws = nullptr;
   rsft::PlanDev dev{};

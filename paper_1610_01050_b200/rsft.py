@@ -69,6 +69,8 @@ def lib():
         "rsft_default_params": (None, [P(RsftParams)]),
         "rsft_plan_create": (c_int32, [P(RsftParams), P(c_void_p)]),
         "rsft_plan_destroy": (None, [c_void_p]),
+        "rsft_plan": (c_int32, [P(RsftParams), c_int32, P(c_void_p)]),
+        "rsft_destroy": (None, [c_void_p]),
         "rsft_set_schedule": (c_int32, [c_void_p, P(c_int64), P(c_int64)]),
         "rsft_get_schedule": (c_int32, [c_void_p, P(c_int64), P(c_int64), P(c_int64)]),
         "rsft_get_thresholds": (c_int32, [c_void_p, P(c_double), P(c_double)]),
@@ -108,7 +110,8 @@ def lib():
     return L
 
 
-EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsft_set_schedule",
+EXPORTED = ["rsft_default_params", "rsft_plan_create", "rsft_plan_destroy", "rsft_plan", "rsft_destroy",
+            "rsft_set_schedule",
             "rsft_get_schedule", "rsft_get_thresholds", "rsft_get_window", "rsft_get_info",
             "rsft_workspace_bytes", "rsft_bind", "rsft_execute", "rsft_execute_segments", "rsft_bucketize_partial",
             "rsft_finalize",

@@ -160,3 +160,20 @@ def test_new_entry_points_validate_before_any_launch():
         p.design_thresholds(K=2, p_d=1.5)
     r = p.design_thresholds(K=2, loops=20, omega=(3.5, 1.0, 7.25))
     assert 1 <= r["mu"] <= 20 and r["pfa_bar"] < r["pd_bar"] and r["gamma"] > 0
+
+
+def test_survey_spelling_plan_and_destroy():
+    """rsft_plan(params, device, out) / rsft_destroy (SURVEY §8(b) names) behave like
+    rsft_plan_create / rsft_plan_destroy; bad device ids are argument errors."""
+    import ctypes
+    L = B.lib()
+    p = B.RsftParams()
+    L.rsft_default_params(ctypes.byref(p))
+    p.ndim, p.n[0], p.b[0], p.loops = 1, 1024, 32, 4
+    h = ctypes.c_void_p()
+    assert L.rsft_plan(ctypes.byref(p), 0, ctypes.byref(h)) == 0 and h.value
+    info = B.RsftInfo()
+    assert L.rsft_get_info(h, ctypes.byref(info)) == 0 and info.ntot == 1024 and info.btot == 32
+    L.rsft_destroy(h)
+    h2 = ctypes.c_void_p()
+    assert L.rsft_plan(ctypes.byref(p), -2, ctypes.byref(h2)) == 1
