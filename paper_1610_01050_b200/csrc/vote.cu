@@ -716,8 +716,11 @@ __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64
                                                  uint32_t* __restrict__ slots, int list_cap) {
   pdl_enter();
   __shared__ int s0[LP], s1[LP];
+  extern __shared__ __align__(16) uint32_t v3s[];    // per warp: the region's E rows [L][B1][W]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int L = pd.L, B0 = pd.b[0], B1 = pd.b[1], W = pd.n[2] >> 5, N1 = pd.n[1];
+  const int rw = B1 * W, lgrw = __ffs(rw) - 1;       // words per (loop, k0) E block
+  uint32_t* es = v3s + (size_t)warp * L * rw;
   const uint32_t n0m = (uint32_t)(pd.n[0] - 1), n1m = (uint32_t)(N1 - 1);
   const int lga0 = pd.lga[0], lga1 = pd.lga[1];
   for (int l = threadIdx.x; l < LP; l += blockDim.x) {
@@ -737,12 +740,18 @@ __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64
   const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, TW = (int64_t)gridDim.x * nwarps;
   for (int64_t r = gw; r < nregions; r += TW) {
     const int64_t frame = r / slab, i0 = d0b + (r - frame * slab);
-    const uint32_t* et[LP];                          // E rows of this region's dim-0 buckets
-#pragma unroll
-    for (int l = 0; l < LP; ++l) {
-      const int k0 = (int)((((uint32_t)s0[l < L ? l : 0] * (uint32_t)i0) & n0m) >> lga0);
-      et[l] = pd.etab + (((size_t)frame * L + (l < L ? l : 0)) * B0 + k0) * (size_t)B1 * W;
+    // this region's E blocks (one dim-0 bucket per loop) into the warp's shared copy: coalesced
+    // rw-word runs, then every detection word reads its L words from shared memory
+    __syncwarp();
+    for (int j = lane; j < L * rw; j += 32) {
+      const int l = j >> lgrw, q = j & (rw - 1);
+      const int k0 = (int)((((uint32_t)s0[l] * (uint32_t)i0) & n0m) >> lga0);
+      es[j] = __ldg(pd.etab + (((size_t)frame * L + l) * B0 + k0) * (size_t)rw + q);
     }
+    __syncwarp();
+    const uint32_t* et[LP];
+#pragma unroll
+    for (int l = 0; l < LP; ++l) et[l] = es + (l < L ? l : 0) * rw;
     uint32_t* det = detect + (size_t)frame * slab_words + (size_t)(i0 - d0b) * items;
     uint32_t* sl = slots ? slots + (size_t)r * list_cap : nullptr;
     int run = 0;
@@ -754,7 +763,7 @@ __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64
         uint32_t e[LP];
 #pragma unroll
         for (int l = 0; l < LP; ++l)
-          e[l] = l < L ? __ldg(et[l] + ((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w) : 0u;
+          e[l] = l < L ? et[l][((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w] : 0u;
         if (MODE == 0) {
           word = 0xffffffffu;
 #pragma unroll
@@ -1314,7 +1323,8 @@ static bool vote3d_ok(const rsft_plan_s* p, int64_t batch, int64_t d0b, int64_t 
   const char* on = getenv("RSFT_VOTE3D");            // force for larger planes (measurement)
   const int64_t lim = on && on[0] == '1' ? (int64_t)1 << 20 : 256;
   return p->D == 3 && !counts && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
-         (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= lim && p->L <= 32;
+         (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= lim && p->L <= 32 &&
+         8 * p->L * p->b[1] * (p->n[2] / 32) * 4 <= 96 * 1024;
 }
 
 static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
@@ -1336,7 +1346,10 @@ static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   const int64_t nregions = batch * (d0e - d0b);
   int64_t grid = (nregions + 7) / 8;
   if (grid > 16 * (int64_t)p->num_sms) grid = 16 * (int64_t)p->num_sms;
-  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, 256, 0, st, p->dev, batch, d0b, d0e, det, rcount, slots,
+  const size_t smem = (size_t)8 * p->L * p->b[1] * (p->n[2] / 32) * 4;
+  rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  if (s) return s;
+  if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, 256, smem, st, p->dev, batch, d0b, d0e, det, rcount, slots,
                                    list_cap); le_ != cudaSuccess)
     return check(le_, "k_vote3d launch");
   p->last_launches += 1;
