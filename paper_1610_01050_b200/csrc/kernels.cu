@@ -1508,6 +1508,100 @@ __global__ void __launch_bounds__(kThreadsFft) k_split_fft(PlanDev pd, const flo
   }
 }
 
+// Split mode, kernel 2, warp form for B_0 = 32 outer grids (D == 3, c3: 32 x 16): one WARP per
+// (frame, loop, k_last) line, no barrier.  Lane b0 loads its relabelled dim-0 row
+// r0 = sigma0 b0 + tau0 (mod B0) of the summed folded spectra, does the dim-1 DFT as a direct
+// B1 x B1 product with a per-loop factor table T[l][r1][k1] = e^{-j pi b1(r1) / B1} W^{b1(r1) k1},
+// b1(r1) = sigma1^{-1}(r1 - tau1) (the relabelling and half twiddle folded in, I3 / L1), applies its
+// dim-0 half twiddle and runs the 32-point dim-0 DFT across the lanes (xor shuffles); lane p then
+// holds k0 = brev5(p), k1 = 0..B1-1: |.|^2 > gamma_l -> atomicOr into the bitmap words.
+template <int B1>
+__global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2* __restrict__ F, int rl0, int rnl,
+                                                        int nchunk, int l0, int nl, int64_t batch,
+                                                        uint32_t* __restrict__ bitmaps, float2* __restrict__ spectra,
+                                                        int seg_L) {
+  pdl_enter();
+  extern __shared__ __align__(16) float2 fw[];
+  const int LT = seg_L > 0 ? seg_L : nl;             // loops in the factor table
+  float2* T = fw;                                      // [LT][B1][B1]
+  float2* tw = fw + (size_t)LT * B1 * B1;             // [128]
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
+  __syncthreads();
+  const int lgb1 = pd.lgb[1], sh1 = pd.shift[1];
+  for (int i = threadIdx.x; i < LT * B1 * B1; i += blockDim.x) {
+    const int l = i / (B1 * B1), r1 = (i / B1) % B1, k1 = i % B1;
+    const LoopDev& lp = pd.loops[l0 + l];
+    const int b1 = (lp.sinv[1] * (r1 - lp.tau[1])) & (B1 - 1);
+    // e^{-j pi b1 / B1} e^{-j 2 pi b1 k1 / B1} = e^{-j 2 pi b1 (2 k1 + 1) / (2 B1)} (shift) or W^{b1 k1}
+    const int idx = sh1 ? ((b1 * (2 * k1 + 1)) & (2 * B1 - 1)) << (6 - lgb1) : ((b1 * k1) & (B1 - 1)) << (7 - lgb1);
+    T[i] = tw[idx];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int blast = pd.blast, bouter = pd.bouter, sh0 = pd.shift[0];
+  float2 stw[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int h = 16 >> q;
+    stw[q] = tw[((lane & (h - 1)) * 64) / h];          // W_{2h}^{lane mod h}
+  }
+  const int64_t lines = batch * nl * blast;
+  for (int64_t li = (int64_t)blockIdx.x * nw + warp; li < lines; li += (int64_t)gridDim.x * nw) {
+    const int64_t frame = li / (nl * blast);
+    const int rem = (int)(li - frame * nl * blast), l = rem / blast, kl = rem - l * blast;
+    const int lg = seg_L > 0 ? (int)(frame % seg_L) : l;            // loop index into the tables
+    const LoopDev& lp = pd.loops[l0 + lg];
+    const float2* src = F + ((((size_t)frame * rnl + (l0 + l - rl0)) * blast + kl) * nchunk) * bouter;
+    const int r0 = (lp.sig[0] * lane + lp.tau[0]) & 31;             // b0 = lane
+    float2 y[B1];
+#pragma unroll
+    for (int q = 0; q < B1; q += 2) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(src + r0 * B1 + q));
+      for (int c = 1; c < nchunk; ++c) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(src + (size_t)c * bouter + r0 * B1 + q));
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      y[q] = make_float2(a.x, a.y);
+      y[q + 1] = make_float2(a.z, a.w);
+    }
+    const float2* Tl = T + (size_t)lg * B1 * B1;
+    const float2 t0 = sh0 ? tw[lane << 1] : make_float2(1.f, 0.f);  // e^{-j pi b0 / 32}
+    float2 X[B1];
+#pragma unroll
+    for (int k1 = 0; k1 < B1; ++k1) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r1 = 0; r1 < B1; ++r1) {
+        const float2 t = Tl[r1 * B1 + k1];
+        acc = __ffma2_rn(make_float2(y[r1].x, y[r1].x), t, acc);
+        acc = __ffma2_rn(make_float2(-y[r1].y, y[r1].y), make_float2(t.y, t.x), acc);
+      }
+      X[k1] = cmul(acc, t0);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < B1; ++k1) {                  // dim-0 DFT across the lanes (DIF)
+      float2 x = X[k1];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int h = 16 >> q;
+        const float2 p = make_float2(__shfl_xor_sync(0xffffffffu, x.x, h), __shfl_xor_sync(0xffffffffu, x.y, h));
+        x = (lane & h) ? cmul(csub(p, x), stw[q]) : cadd(x, p);
+      }
+      X[k1] = x;
+    }
+    const int k0 = brev(lane, 5);
+    const float gamma = lp.gamma;
+    uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
+    float2* sp = spectra ? spectra + ((size_t)frame * nl + l) * pd.btot : nullptr;
+#pragma unroll
+    for (int k1 = 0; k1 < B1; ++k1) {
+      const int64_t k = (int64_t)(k0 * B1 + k1) * blast + kl;
+      if (X[k1].x * X[k1].x + X[k1].y * X[k1].y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
+      if (sp) sp[k] = X[k1];
+    }
+  }
+}
+
 // Variant B helper: sum the dim-0 chunks of the folded spectra F [L][B_last][nchunk][B_outer]
 // into the canonical partial [L][B_last][B_outer] (in chunk order).
 __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bouter, int64_t n, float2* __restrict__ out) {
@@ -1749,6 +1843,24 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
   const int D = p->D;
   const int64_t blast = p->b[D - 1];
   const int64_t b1 = D == 3 ? p->b[1] : 1;
+  {
+    // warp form for 32 x B1 outer grids (c3); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
+    const char* ew = getenv("RSFT_FFT_WARP");
+    const int LT = seg_L > 0 ? seg_L : nl;
+    const size_t smw = ((size_t)LT * b1 * b1 + 128) * 8;
+    if (D == 3 && p->b[0] == 32 && (b1 == 8 || b1 == 16) && smw <= 64 * 1024 && !(ew && ew[0] == '0')) {
+      auto kw = b1 == 8 ? k_split_fft_w32<8> : k_split_fft_w32<16>;
+      rsft_status s = check(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw), "smem attr");
+      if (s) return s;
+      const int64_t lines = batch * nl * blast;
+      const int64_t grid = std::min<int64_t>((lines + 7) / 8, 8 * (int64_t)p->num_sms);
+      if (cudaError_t le_ = pdl_launch(kw, (unsigned)grid, 256, smw, st, p->dev, F, rl0, rnl, nchunk, l0, nl, batch, bm,
+                                       reinterpret_cast<float2*>(spectra), seg_L); le_ != cudaSuccess)
+        return check(le_, "k_split_fft_w32 launch");
+      p->last_launches += 1;
+      return check(cudaGetLastError(), "k_split_fft_w32 launch");
+    }
+  }
   size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;
   rsft_status s = check(cudaFuncSetAttribute(k_split_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2),
                         "smem attr");

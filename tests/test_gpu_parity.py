@@ -63,6 +63,9 @@ CASES = [
     ("3d_L1", (16, 16, 64), (4, 8, 16), 1, dict(p_fa=1e-3), 1, "split"),
     ("3d_c3like_mu", (64, 128, 32), (8, 16, 8), 8, dict(p_fa=1e-2, mu=5, random_tau=True), 3, "split"),
     ("3d_c3like_or", (32, 64, 32), (4, 8, 8), 4, dict(p_fa=1e-3, mu=1), 2, "split"),
+    # warp-form outer FFT (B_0 = 32, B_1 in {8, 16})
+    ("3d_w32_b16", (64, 32, 32), (32, 16, 8), 6, dict(p_fa=1e-3, random_tau=True), 2, "split"),
+    ("3d_w32_b8_mu", (128, 64, 32), (32, 8, 4), 5, dict(p_fa=1e-2, mu=3), 2, "split"),
     # more than 32 loops (up to 63, the paper's T = 50 design point P:640): several fold passes
     ("2d_L40", (128, 64), (16, 8), 40, dict(p_fa=1e-2, mu=30, random_tau=True), 2, "fused"),
     ("1d_L50_w256", (1024,), (32,), 50, dict(support=(256,), p_fa=1e-2, mu=40), 2, "fused"),
@@ -155,6 +158,25 @@ def test_parity_2d_frame_vote_forced(case, force, monkeypatch):
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
     x = frames(wl, batch)
     plan, res, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+
+
+W32_CASES = [c for c in CASES if c[0].startswith("3d_w32")]
+
+
+@pytest.mark.parametrize("case", W32_CASES, ids=[c[0] for c in W32_CASES])
+def test_outer_fft_warp_vs_cta_forms(case, monkeypatch):
+    """The warp-form outer FFT (k_split_fft_w32) and the CTA form (RSFT_FFT_WARP=0, read per
+    launch) on the same input: both within the oracle tolerance, bits equal outside the band."""
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = frames(wl, batch)
+    monkeypatch.setenv("RSFT_FFT_WARP", "0")
+    _, res_cta, reps = run_case(op, x, mode=mode)
+    assert max(r["max_ratio"] for r in reps) < 1e-4
+    monkeypatch.delenv("RSFT_FFT_WARP")
+    _, res_w, reps = run_case(op, x, mode=mode)
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
@@ -391,6 +413,7 @@ def test_variant_b_c5_full_cube():
     ((32, 16, 64), (4, 4, 8), 3, "split"),
     ((64, 128, 32), (8, 16, 8), 4, "split"),          # c3-like: multi-a0 boxes, batched segments
     ((128, 64), (16, 16), 3, "split"),                # D = 2 split, batched segments
+    ((64, 32, 32), (32, 16, 8), 4, "split"),          # B_0 = 32: warp-form outer FFT, segments
 ])
 def test_segment_mode_parity(n, b, L, mode):
     """Segment mode (P:204): loop l folds segment l of each frame (rsft_execute_segments);
