@@ -527,8 +527,8 @@ __global__ void __launch_bounds__(kThreads) k_region_write(const uint32_t* __res
 // ------------------------------------------------------------------------------------
 constexpr int kVote1dWarps = 8;
 
-template <int LP>
-__global__ void __launch_bounds__(32 * kVote1dWarps) k_vote1d(PlanDev pd, const uint32_t* __restrict__ bitmaps,
+template <int LP, int MINB = 1>
+__global__ void __launch_bounds__(32 * kVote1dWarps, MINB) k_vote1d(PlanDev pd, const uint32_t* __restrict__ bitmaps,
                                                                int64_t batch, uint32_t* __restrict__ detect,
                                                                unsigned long long* __restrict__ rcount,
                                                                uint32_t* __restrict__ slots, int list_cap) {
@@ -1299,7 +1299,10 @@ static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
 static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                  unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
   const size_t smem = (size_t)kVote1dWarps * (p->n[0] / 32) * 4;
-  auto kern = p->L <= 8 ? k_vote1d<8> : p->L <= 16 ? k_vote1d<16> : k_vote1d<32>;
+  // RSFT_VOTE1D_OCC=6 (read per launch): the register-capped build (6 CTAs of 8 warps per SM)
+  const char* oc = getenv("RSFT_VOTE1D_OCC");
+  const bool cap = oc && oc[0] == '6' && p->L <= 8;
+  auto kern = cap ? k_vote1d<8, 6> : p->L <= 8 ? k_vote1d<8> : p->L <= 16 ? k_vote1d<16> : k_vote1d<32>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   int nb = 0;
