@@ -1299,9 +1299,10 @@ static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
 static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                  unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
   const size_t smem = (size_t)kVote1dWarps * (p->n[0] / 32) * 4;
-  // RSFT_VOTE1D_OCC=6 (read per launch): the register-capped build (6 CTAs of 8 warps per SM)
+  // L <= 8: the register-capped build (40 registers, 6 CTAs of 8 warps per SM): c1 step 0.978 vs
+  // 1.001 ms with the uncapped one (89 registers, 2 CTAs/SM); RSFT_VOTE1D_OCC=1 selects the latter
   const char* oc = getenv("RSFT_VOTE1D_OCC");
-  const bool cap = oc && oc[0] == '6' && p->L <= 8;
+  const bool cap = !(oc && oc[0] == '1') && p->L <= 8;
   auto kern = cap ? k_vote1d<8, 6> : p->L <= 8 ? k_vote1d<8> : p->L <= 16 ? k_vote1d<16> : k_vote1d<32>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
