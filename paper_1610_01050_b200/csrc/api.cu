@@ -5,6 +5,15 @@
 #include <string>
 
 #include "rsft_internal.h"
+#include <nvtx3/nvToolsExt.h>
+
+namespace {
+// NVTX range per ABI call (SURVEY §5 tracing): visible in nsys / ncu timelines, no cost without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace rsft {
 rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
@@ -40,6 +49,7 @@ using namespace rsft;
 extern "C" {
 
 rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
+  NvtxRange nvtx_("rsft_bind");
   if (!p) return RSFT_E_ARG;
   if (!d_ws || bytes < p->ws.total || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return RSFT_E_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -158,6 +168,7 @@ rsft_status rsft_bind(rsft_plan_t p, void* d_ws, size_t bytes, void* stream) {
 
 rsft_status rsft_execute(rsft_plan_t p, const void* d_x, int64_t batch, int32_t loop_begin, int32_t loop_end,
                          uint32_t* d_bitmaps, void* d_spectra, void* stream) {
+  NvtxRange nvtx_("rsft_execute");
   if (!p || !d_x || !d_bitmaps) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -171,6 +182,7 @@ rsft_status rsft_execute(rsft_plan_t p, const void* d_x, int64_t batch, int32_t 
 
 rsft_status rsft_execute_segments(rsft_plan_t p, const void* d_x, int64_t batch, uint32_t* d_bitmaps,
                                   void* d_spectra, void* stream) {
+  NvtxRange nvtx_("rsft_execute_segments");
   if (!p || !d_x || !d_bitmaps) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -182,6 +194,7 @@ rsft_status rsft_execute_segments(rsft_plan_t p, const void* d_x, int64_t batch,
 
 rsft_status rsft_bucketize_partial(rsft_plan_t p, const void* d_x_slab, int64_t off, int64_t len, void* d_partial,
                                    void* stream) {
+  NvtxRange nvtx_("rsft_bucketize_partial");
   if (!p || !d_x_slab || !d_partial) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (p->D < 2 || resolve_mode(p, 1) != RSFT_MODE_SPLIT) return RSFT_E_UNSUPPORTED;
@@ -193,6 +206,7 @@ rsft_status rsft_bucketize_partial(rsft_plan_t p, const void* d_x_slab, int64_t 
 
 rsft_status rsft_finalize(rsft_plan_t p, const void* d_folded, int32_t loop_begin, int32_t loop_end,
                           uint32_t* d_bitmaps, void* d_spectra, void* stream) {
+  NvtxRange nvtx_("rsft_finalize");
   if (!p || !d_folded || !d_bitmaps) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (p->D < 2 || resolve_mode(p, 1) != RSFT_MODE_SPLIT) return RSFT_E_UNSUPPORTED;
@@ -204,6 +218,7 @@ rsft_status rsft_finalize(rsft_plan_t p, const void* d_folded, int32_t loop_begi
 
 rsft_status rsft_detect(rsft_plan_t p, const uint32_t* d_bitmaps, int64_t batch, int64_t d0b, int64_t d0e,
                         uint32_t* d_detect, uint8_t* d_counts, void* stream) {
+  NvtxRange nvtx_("rsft_detect");
   if (!p || !d_bitmaps || !d_detect) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 0 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -217,6 +232,7 @@ rsft_status rsft_detect(rsft_plan_t p, const uint32_t* d_bitmaps, int64_t batch,
 
 rsft_status rsft_compact(rsft_plan_t p, const uint32_t* d_detect, int64_t batch, int64_t* d_idx,
                          int64_t capacity, int64_t* d_count, void* stream) {
+  NvtxRange nvtx_("rsft_compact");
   if (!p || !d_detect || !d_count || (capacity > 0 && !d_idx) || capacity < 0) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -226,6 +242,7 @@ rsft_status rsft_compact(rsft_plan_t p, const uint32_t* d_detect, int64_t batch,
 
 rsft_status rsft_detect_compact(rsft_plan_t p, const uint32_t* d_bitmaps, int64_t batch, uint32_t* d_detect,
                                 int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream) {
+  NvtxRange nvtx_("rsft_detect_compact");
   if (!p || !d_bitmaps || !d_detect || !d_count || (capacity > 0 && !d_idx) || capacity < 0) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -236,6 +253,7 @@ rsft_status rsft_detect_compact(rsft_plan_t p, const uint32_t* d_bitmaps, int64_
 
 rsft_status rsft_run(rsft_plan_t p, const void* d_x, int64_t batch, uint32_t* d_bitmaps, uint32_t* d_detect,
                      int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream) {
+  NvtxRange nvtx_("rsft_run");
   if (!p || !d_x || !d_bitmaps || !d_detect || !d_count || (capacity > 0 && !d_idx) || capacity < 0) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
@@ -255,6 +273,7 @@ size_t rsft_host_scratch_bytes(rsft_plan_t p, int64_t batch, int64_t capacity) {
 
 rsft_status rsft_run_host(rsft_plan_t p, const void* h_x, int64_t batch, int64_t* h_idx, int64_t capacity,
                           int64_t* h_count, void* d_scratch, size_t scratch_bytes, void* stream) {
+  NvtxRange nvtx_("rsft_run_host");
   if (!p || !h_x || !h_count || (capacity > 0 && !h_idx) || capacity < 0) return RSFT_E_ARG;
   if (!p->bound) return RSFT_E_STATE;
   if (batch < 1 || batch > p->P.max_batch) return RSFT_E_ARG;
