@@ -254,6 +254,7 @@ __device__ int vote_region(const PlanDev& pd, const uint32_t* bm, int lw, uint32
       if (total <= pd.list_cap) {
 #pragma unroll
         for (int k = 0; k < kListIpt; ++k) {
+          if (__ballot_sync(0xffffffffu, ck[k] != 0) == 0u) continue;   // most rows hold no detection
           const int64_t it = tid + (int64_t)k * blockDim.x;
           int q = pos[k];
 #pragma unroll
