@@ -309,6 +309,15 @@ def main_gpu(a):
     cnt = torch.empty(1, dtype=torch.int64, device=dev)
 
     def step(events=None):
+        if a.run:
+            # one rsft_run call (D = 1 gather plans: fold + vote in one kernel); the "dominant
+            # kernel" events then bracket the whole call (conservative)
+            if events is not None:
+                events[0].record(stream)
+            plan.run(x, cap, bitmaps=bm, detect=det, idx=idx, count=cnt)
+            if events is not None:
+                events[1].record(stream)
+            return plan.last_launch_count()
         # == rsft_run (execute + detect_compact), as two ABI calls so that the fused
         # fold/FFT/threshold kernel can be timed alone on the launching stream
         if events is not None:
@@ -374,6 +383,8 @@ def main_gpu(a):
         cpu = cpu_baseline(wl, a.cpu_budget)
     cfg = workload_config(wl, frames)
     cfg["mode"] = {1: "fused", 2: "split"}.get(plan.mode, plan.mode)
+    if a.run:
+        cfg["step_call"] = "rsft_run (one call; roofline times the whole call)"
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "step_ms": step_stats(per_step),
@@ -382,7 +393,7 @@ def main_gpu(a):
         "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(wl.name),
-                     "kernel": fold_kernel_label(plan, wl),
+                     "kernel": fold_kernel_label(plan, wl) + (" [whole rsft_run call]" if a.run else ""),
                      "algorithmic_bytes_per_launch": algo_bytes,
                      "avg_launch_ms": k1_avg, "share_of_step": k1_avg / step_ms, "peak_source": peak_src},
         "gpu_launches": launches,
@@ -630,6 +641,9 @@ def main():
     ap.add_argument("--bartlett", action="store_true", help="time the Bartlett baseline (Alg. 2) instead")
     ap.add_argument("--segments", action="store_true", help="time the RSFT in segment mode (P:204)")
     ap.add_argument("--c5-variant", default="B", choices=["A", "B"], help="c5 multi-GPU scheme (DESIGN.md §8)")
+    ap.add_argument("--run", action="store_true",
+                    help="issue each step as ONE rsft_run call (D = 1: fold and vote fused in one kernel); the "
+                         "roofline then times the whole call")
     ap.add_argument("--force-collectives", action="store_true",
                     help="initialise an NCCL process group even with one rank, so the multi-GPU code path "
                          "(barriers, max-over-ranks timing, c5 reduce-scatter + all-gather) runs on a 1-GPU lease")

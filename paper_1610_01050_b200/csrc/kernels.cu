@@ -25,6 +25,7 @@
 #include "rsft_internal.h"
 #include "kcommon.cuh"
 #include "hcommon.h"
+#include "vote1d.cuh"
 
 namespace rsft {
 
@@ -544,28 +545,80 @@ __device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const fl
   return x;
 }
 
-template <int TAPS, int LPW>
-__global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
+// Fused c1 path (VL > 0; rsft_run): `nv` vote warps per CTA vote the frames the loop warps just
+// finished -- each loop warp also drops its bitmap words into a BS-slot shared ring (mbarriers
+// bfull / bempty), a vote warp takes frame fi = v, v + nv, ... and runs the per-frame D = 1 vote
+// (vote1d.cuh) while the loop warps fold the next frames: the second stage hides under the HBM
+// stream.  Outputs as k_vote1d: detection words, per-frame counts, local index lists.
+constexpr int kG1BS = 8;                              // bitmap ring slots (>= vote warps)
+template <int TAPS, int LPW, int VL = 0>
+__global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
                                                       int l0, int nl, int W, int S, int chunk, uint32_t* __restrict__ bitmaps,
                                                       float2* __restrict__ spectra, int64_t bm_stride,
-                                                      int64_t sp_stride) {
+                                                      int64_t sp_stride, int nv, uint32_t* __restrict__ vdet,
+                                                      unsigned long long* __restrict__ rcount, uint32_t* __restrict__ slots,
+                                                      int list_cap) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = pd.n[0], B = pd.b[0], lgb = pd.lgb[0];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ncw = (blockDim.x >> 5) - 1;            // loop warps; the last warp produces
+  const int ncw = (blockDim.x >> 5) - 1 - (VL ? nv : 0);   // loop warps; then the producer, then vote warps
   const uint32_t fbytes = (uint32_t)N * 8u;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + S;
   float2* tw = reinterpret_cast<float2*>(smem + 16 * S + 128 - ((16 * S) & 127));  // 128-B aligned
   unsigned char* ring = reinterpret_cast<unsigned char*>(tw + 128);
+  // fused vote state after the ring: bfull / bempty [BS] | bitmap slots [BS][L wpl] | sinv [VL] |
+  // per vote warp: detection words [N/32], ent [32], queue [64]
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(ring + (size_t)S * fbytes);
+  uint64_t* bempty = bfull + kG1BS;
+  const int bsw = pd.L * pd.wpl;
+  uint32_t* bslot = reinterpret_cast<uint32_t*>(bempty + kG1BS);
+  int* vsinv = reinterpret_cast<int*>(bslot + kG1BS * bsw);
+  uint32_t* vbase = reinterpret_cast<uint32_t*>(vsinv + (VL ? VL : 1));
   if (tid < 128) tw[tid] = c_tw128[tid];
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], ncw); }
+    if (VL) for (int s = 0; s < kG1BS; ++s) { mbar_init(&bfull[s], ncw); mbar_init(&bempty[s], 1); }
     fence_mbar_init();
   }
   pdl_enter();
+  if (VL)
+    for (int l = tid; l < VL; l += blockDim.x) vsinv[l] = l < pd.L ? pd.loops[l].sinv[0] : 0;
   __syncthreads();
   const int64_t nfr = batch > (int64_t)blockIdx.x ? (batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if constexpr (VL > 0) {
+    if (warp > ncw) {                               // ---- vote warps
+      const int vw = warp - ncw - 1;
+      const int nw = N >> 5;
+      uint32_t* dw = vbase + (size_t)vw * (nw + 96);
+      int* ent = reinterpret_cast<int*>(dw + nw);
+      uint32_t* q = dw + nw + 32;
+      for (int w = lane; w < nw; w += 32) dw[w] = 0u;
+      int sg[VL];
+#pragma unroll
+      for (int l = 0; l < VL; ++l) sg[l] = l < pd.L ? pd.loops[l].sig[0] : 0;
+      __syncwarp();
+      const int L = pd.L, wpl = pd.wpl;
+      for (int64_t fi = vw; fi < nfr; fi += nv) {
+        const int slot = (int)(fi & (kG1BS - 1));
+        mbar_wait(&bfull[slot], (uint32_t)((fi / kG1BS) & 1));
+        const uint32_t* b = bslot + slot * bsw;
+        uint32_t mlo[VL], mhi[VL];
+#pragma unroll
+        for (int l = 0; l < VL; ++l) {
+          mlo[l] = l < L ? b[l * wpl] : 0u;
+          mhi[l] = (l < L && wpl > 1) ? b[l * wpl + 1] : 0u;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bempty[slot]);
+        vote1d_frame<VL>(pd, mlo, mhi, sg, vsinv, ent, q, dw, (int64_t)blockIdx.x + fi * gridDim.x, vdet, rcount,
+                         slots, list_cap);
+        __syncwarp();
+      }
+      return;
+    }
+  }
 
   if (warp == ncw) {                                // ---- producer: whole frames, S-deep ring
     if (lane == 0) {
@@ -622,6 +675,8 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
   uint32_t ph = 0;
   for (int64_t fi = 0; fi < nfr; ++fi) {
     const int64_t frame = blockIdx.x + fi * gridDim.x;
+    const int bsl = (int)(fi & (kG1BS - 1));
+    if (VL && fi >= kG1BS) mbar_wait(&bempty[bsl], (uint32_t)(((fi / kG1BS) - 1) & 1));   // slot voted
     mbar_wait(&full[s], ph);
     const unsigned char* xs = ring + (size_t)s * fbytes;
     // even taps k -> bucket lane, odd taps -> bucket lane + 32 (B = 64); for B <= 32 both
@@ -660,6 +715,7 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
         const uint32_t w0 = __ballot_sync(0xffffffffu, (va >> (lane & 1)) & 1);
         const uint32_t w1 = __ballot_sync(0xffffffffu, (vb >> (lane & 1)) & 1);
         if (lane == 0) *reinterpret_cast<uint2*>(bmw) = make_uint2(w0, w1);
+        if (VL && lane == 0) { bslot[bsl * bsw + l * wpl] = w0; bslot[bsl * bsw + l * wpl + 1] = w1; }
       } else {
         float2 a = cadd(acc[q][0], acc[q][1]);
 #pragma unroll
@@ -673,7 +729,12 @@ __global__ void __launch_bounds__(544, 1) k_gather1d(PlanDev pd, const float2* _
         const int vq = __shfl_sync(0xffffffffu, val, brev(lane & (B - 1), lgb));
         const uint32_t w0 = __ballot_sync(0xffffffffu, lane < B && vq);
         if (lane == 0) bmw[0] = w0;
+        if (VL && lane == 0) bslot[bsl * bsw + l * wpl] = w0;
       }
+    }
+    if (VL) {                                       // this warp's loops of frame fi are in the slot
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfull[bsl]);
     }
   }
 }
@@ -1651,20 +1712,27 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
 }
 
 
-template <int TAPS, int LPW>
+template <int TAPS, int LPW, int VL = 0>
 static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
-                                     void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride) {
-  auto kern = k_gather1d<TAPS, LPW>;
+                                     void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride,
+                                     uint32_t* vdet = nullptr, unsigned long long* rcount = nullptr,
+                                     uint32_t* slots = nullptr, int list_cap = 0) {
+  auto kern = k_gather1d<TAPS, LPW, VL>;
   const int ncw = (nl + LPW - 1) / LPW;
-  const int threads = 32 * (ncw + 1);
+  const char* env_v = getenv("RSFT_G1_VOTE_WARPS");
+  const int nv = VL ? (env_v && env_v[0] ? std::max(1, std::min(atoi(env_v), kG1BS)) : 4) : 0;
+  const int threads = 32 * (ncw + 1 + nv);
   const int W = (int)(p->b[0] < p->n[0] ? p->W[0] : p->n[0]);
   const size_t fbytes = (size_t)p->n[0] * 8;
   const char* env_s = getenv("RSFT_G1_STAGES");
   const char* env_c = getenv("RSFT_G1_CTAS");
-  int ctas = env_c && env_c[0] ? atoi(env_c) : 2;
+  int ctas = env_c && env_c[0] ? atoi(env_c) : (VL ? 1 : 2);
+  const size_t vbytes = VL ? (size_t)16 * kG1BS + (size_t)kG1BS * p->L * p->dev.wpl * 4 + (size_t)VL * 4 +
+                                 (size_t)nv * (p->n[0] / 32 + 96) * 4
+                           : 0;
   int S = env_s && env_s[0] ? atoi(env_s) : 0;
-  if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048) / fbytes));
-  const size_t smem = 16 * S + 128 + 1024 + S * fbytes;
+  if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048 - vbytes) / fbytes));
+  const size_t smem = 16 * S + 128 + 1024 + S * fbytes + vbytes;
   const char* env_k = getenv("RSFT_G1_CHUNK");        // bytes per bulk copy (divides the frame)
   int chunk = env_k && env_k[0] ? atoi(env_k) : (int)std::min<size_t>(fbytes, 8192);
   if (chunk <= 0 || chunk % 16 || fbytes % chunk) chunk = (int)fbytes;
@@ -1678,7 +1746,8 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   if (grid > batch) grid = batch;
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, (unsigned)threads, smem, st, p->dev,
                                    reinterpret_cast<const float2*>(d_x), batch, l0, nl, W, S, chunk, bm,
-                                   reinterpret_cast<float2*>(spectra), bm_stride, sp_stride); le_ != cudaSuccess)
+                                   reinterpret_cast<float2*>(spectra), bm_stride, sp_stride, nv, vdet, rcount, slots,
+                                   list_cap); le_ != cudaSuccess)
     return check(le_, "k_gather1d launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_gather1d launch");
@@ -1693,6 +1762,21 @@ static rsft_status launch_gather1d(rsft_plan_s* p, const void* d_x, int64_t batc
                                  : launch_gather1d_t<T, 2>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride);
   RSFT_G1(4) RSFT_G1(8) RSFT_G1(16) RSFT_G1(32)
 #undef RSFT_G1
+  return RSFT_E_UNSUPPORTED;
+}
+
+// rsft_run for D = 1 gather plans: the fold kernel with vote warps (first and second stage in one
+// launch), all L <= 16 loops; returns E_UNSUPPORTED when the shape does not qualify.
+static rsft_status launch_gather1d_voted(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det,
+                                         unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
+  const int taps = gather1d_taps(p);
+  if (p->L > 16 || !taps) return RSFT_E_UNSUPPORTED;
+  const int64_t bs = (int64_t)p->L * p->dev.wpl;
+#define RSFT_G1V(T) \
+  if (taps == T) return p->L <= 8 ? launch_gather1d_t<T, 1, 8>(p, d_x, batch, 0, p->L, bm, nullptr, st, bs, 0, det, rcount, slots, list_cap) \
+                                  : launch_gather1d_t<T, 1, 16>(p, d_x, batch, 0, p->L, bm, nullptr, st, bs, 0, det, rcount, slots, list_cap);
+  RSFT_G1V(4) RSFT_G1V(8) RSFT_G1V(16) RSFT_G1V(32)
+#undef RSFT_G1V
   return RSFT_E_UNSUPPORTED;
 }
 
@@ -2012,12 +2096,26 @@ rsft_status launch_execute(rsft_plan_s* p, const void* d_x, int64_t batch, int l
 
 rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                   int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st);   // vote.cu
+bool vote1d_usable(const rsft_plan_s* p);                                                              // vote.cu
+rsft_status launch_scan_write(rsft_plan_s* p, int64_t batch, uint32_t* det, int64_t* idx, int64_t capacity,
+                              int64_t* d_count, bool list, cudaStream_t st);                          // vote.cu
 
 // Whole pipeline on one batch: execute (all loops) + detect_compact.  (Running the vote in
 // the fold kernel's per-frame epilogue was measured slower at c4: the CTA's TMA stream
 // stalls while it votes.)
 rsft_status launch_run(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det, int64_t* idx,
                        int64_t capacity, int64_t* d_count, cudaStream_t st) {
+  {
+    // D = 1 gather plans: fold + vote in one kernel (RSFT_FUSED_RUN=0, read per launch, splits them)
+    const char* fr = getenv("RSFT_FUSED_RUN");
+    if (!(fr && fr[0] == '0') && p->D == 1 && gather1d_taps(p) && vote1d_usable(p) && batch <= p->dev.region_capacity) {
+      const bool list = p->dev.region_slots != nullptr;
+      rsft_status s = launch_gather1d_voted(p, d_x, batch, bm, det, p->dev.region_state,
+                                            list ? p->dev.region_slots : nullptr, (int)p->dev.list_cap, st);
+      if (s == RSFT_OK) return launch_scan_write(p, batch, det, idx, capacity, d_count, list, st);
+      if (s != RSFT_E_UNSUPPORTED) return s;
+    }
+  }
   rsft_status s = launch_execute(p, d_x, batch, 0, p->L, bm, nullptr, st);
   if (s) return s;
   return launch_detect_compact(p, bm, batch, det, idx, capacity, d_count, st);

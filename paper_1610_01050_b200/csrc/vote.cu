@@ -10,6 +10,7 @@
 
 #include "kcommon.cuh"
 #include "hcommon.h"
+#include "vote1d.cuh"
 
 namespace rsft {
 
@@ -539,9 +540,8 @@ __global__ void __launch_bounds__(32 * kVote1dWarps, MINB) k_vote1d(PlanDev pd, 
   __shared__ int ent_s[kVote1dWarps][32];
   __shared__ uint32_t q_s[kVote1dWarps][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int N = pd.n[0], L = pd.L, mu = pd.mu, wpl = pd.wpl, lga = pd.lga[0];
-  const int A = 1 << lga, nw = N >> 5;
-  const uint32_t nm = (uint32_t)(N - 1), lt = (1u << lane) - 1u;
+  const int N = pd.n[0], L = pd.L, wpl = pd.wpl;
+  const int nw = N >> 5;
   for (int l = threadIdx.x; l < LP; l += blockDim.x) {
     sig_s[l] = l < L ? pd.loops[l].sig[0] : 0;
     sinv_s[l] = l < L ? pd.loops[l].sinv[0] : 0;
@@ -552,7 +552,6 @@ __global__ void __launch_bounds__(32 * kVote1dWarps, MINB) k_vote1d(PlanDev pd, 
   int sg[LP];
 #pragma unroll
   for (int l = 0; l < LP; ++l) sg[l] = sig_s[l];
-  const int ncl = L - mu + 1;                        // candidate loops needed
   const bool vec = ((L * wpl) & 3) == 0;
   uint32_t* q = q_s[warp];
 
@@ -575,126 +574,7 @@ __global__ void __launch_bounds__(32 * kVote1dWarps, MINB) k_vote1d(PlanDev pd, 
         mhi[l] = (l < L && wpl > 1) ? __ldg(src + l * wpl + 1) : 0u;
       }
     }
-    // one vote: bit M_l(i) of loop l (Def. 3)
-    auto vote = [&](int l, uint32_t i) -> uint32_t {
-      const uint32_t k = (((uint32_t)sg[l] * i) & nm) >> lga;
-      return ((k < 32 ? mlo[l] : mhi[l]) >> (k & 31)) & 1u;
-    };
-    // candidate loops: the ncl loops with the fewest set buckets (bit l of cmask); for
-    // mu = L also a filter loop lf (fewest set buckets among the others)
-    uint32_t cmask = 0u;
-    int ncand = 0;
-    for (int t = 0; t < ncl; ++t) {
-      int best = 1 << 30, bl = 0;
-#pragma unroll
-      for (int l = 0; l < LP; ++l) {
-        const int pc = __popc(mlo[l]) + __popc(mhi[l]);
-        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; bl = l; }
-      }
-      cmask |= 1u << bl;
-      ncand += best;
-    }
-    // filter loop lf (mu = L): its mask and sigma in plain registers (no per-test loop select)
-    int lf = -1;
-    uint32_t flo = 0xffffffffu, fhi = 0xffffffffu, fsg = 0u;
-    if (mu == L && L > 1) {
-      int best = 1 << 30;
-#pragma unroll
-      for (int l = 0; l < LP; ++l) {
-        const int pc = __popc(mlo[l]) + __popc(mhi[l]);
-        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; lf = l; flo = mlo[l]; fhi = mhi[l]; fsg = (uint32_t)sg[l]; }
-      }
-    }
-    if (2 * ncand * A <= N) {                         // ---- candidate mode
-      int base = 0;                                   // entries (loop, bucket), ascending loops
-#pragma unroll
-      for (int l = 0; l < LP; ++l) {
-        if (!((cmask >> l) & 1u)) continue;
-        const bool b0 = (mlo[l] >> lane) & 1u, b1 = (mhi[l] >> lane) & 1u;
-        const uint32_t bl0 = __ballot_sync(0xffffffffu, b0), bl1 = __ballot_sync(0xffffffffu, b1);
-        if (b0) ent_s[warp][base + __popc(bl0 & lt)] = (l << 8) | lane;
-        base += __popc(bl0);
-        if (b1) ent_s[warp][base + __popc(bl1 & lt)] = (l << 8) | (lane + 32);
-        base += __popc(bl1);
-      }
-      __syncwarp();
-      // full test of up to 32 queued locations (lane per location), all loops
-      auto drain = [&](int n) {
-        const uint32_t i = lane < n ? q[lane] : 0u;
-        int cnt = 0;
-#pragma unroll
-        for (int l = 0; l < LP; ++l)
-          if (l < L) cnt += (int)vote(l, i);
-        if (lane < n && cnt >= mu) atomicOr(&dw[i >> 5], 1u << (i & 31));
-      };
-      int qn = 0;
-      const int T = ncand * A;
-      for (int c0 = 0; c0 < T; c0 += 32) {
-        const int c = c0 + lane;
-        const bool valid = c < T;
-        const int e = ent_s[warp][valid ? (c >> lga) : 0];
-        const uint32_t u = ((uint32_t)(e & 255) << lga) | (uint32_t)(c & (A - 1));
-        const uint32_t i = ((uint32_t)sinv_s[e >> 8] * u) & nm;          // Def. 4
-        // mu = L: a location needs the filter loop's vote too (cheap pre-test, then queue)
-        bool pass = valid;
-        if (lf >= 0) {
-          const uint32_t k = ((fsg * i) & nm) >> lga;
-          pass = pass && (((k < 32 ? flo : fhi) >> (k & 31)) & 1u);
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-        if (pass) q[qn + __popc(bal & lt)] = i;
-        qn += __popc(bal);
-        __syncwarp();
-        if (qn >= 32) {
-          drain(32);
-          __syncwarp();
-          const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
-          __syncwarp();
-          if (lane + 32 < qn) q[lane] = rest;
-          qn -= 32;
-          __syncwarp();
-        }
-      }
-      if (qn > 0) drain(qn);
-    } else {                                          // ---- dense mode
-      for (int w = 0; w < nw; ++w) {
-        const uint32_t i = (uint32_t)(w << 5) | (uint32_t)lane;
-        int cnt = 0;
-#pragma unroll
-        for (int l = 0; l < LP; ++l)
-          if (l < L) cnt += (int)vote(l, i);
-        const uint32_t word = __ballot_sync(0xffffffffu, cnt >= mu);
-        if (lane == 0) dw[w] = word;
-      }
-    }
-    __syncwarp();
-    // read-out: detection words (coalesced), count, ascending local index list
-    uint32_t* det = detect + (size_t)frame * nw;
-    uint32_t* sl = slots ? slots + (size_t)frame * list_cap : nullptr;
-    int run = 0;
-    for (int w0 = 0; w0 < nw; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t v = 0u;
-      if (w < nw) { v = dw[w]; dw[w] = 0u; det[w] = v; }
-      const int c = __popc(v);
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (sl) {
-        int qq = run + incl - c;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          if (qq < list_cap) sl[qq] = (uint32_t)((w << 5) + bit);
-          ++qq;
-        }
-      }
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (rcount && lane == 0) rcount[frame] = (unsigned long long)run;
+    vote1d_frame<LP>(pd, mlo, mhi, sg, sinv_s, ent_s[warp], q, dw, frame, detect, rcount, slots, list_cap);
     __syncwarp();
   }
 }
@@ -1291,6 +1171,12 @@ static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t 
 }
 
 // D == 1 warp-per-frame vote (k_vote1d): full range, no abar output, frame words in smem.
+bool vote1d_usable(const rsft_plan_s* p) {
+  const char* off = getenv("RSFT_NO_VOTE1D");
+  if (off && off[0] && off[0] != '0') return false;
+  return p->D == 1 && p->n[0] >= 32 && p->n[0] <= 32768 && p->L <= 32;
+}
+
 static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
   const char* off = getenv("RSFT_NO_VOTE1D");        // read per launch: tests select either kernel
   if (off && off[0] && off[0] != '0') return false;
@@ -1414,6 +1300,9 @@ rsft_status launch_detect(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int
 }
 
 // vote (+ per-region counts) -> offset scan -> per-region sorted index writes
+rsft_status launch_scan_write(rsft_plan_s* p, int64_t batch, uint32_t* det, int64_t* idx, int64_t capacity,
+                              int64_t* d_count, bool list, cudaStream_t st);
+
 rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,
                                   int64_t* idx, int64_t capacity, int64_t* d_count, cudaStream_t st) {
   const int64_t n0 = p->n[0];
@@ -1450,6 +1339,36 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
                 : list ? launch_vote_mode<true, true>(p, bm, batch, 0, n0, det, nullptr, st)
                        : launch_vote_mode<true, false>(p, bm, batch, 0, n0, det, nullptr, st);
   if (s) return s;
+  return launch_scan_write(p, batch, det, idx, capacity, d_count, list, st);
+}
+
+
+rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
+                           int64_t capacity, int64_t* d_count, cudaStream_t st) {
+  const int64_t nwords = batch * ((p->ntot + 31) / 32);
+  const int64_t nchunks = (nwords + kChunkWords - 1) / kChunkWords;
+  if (nchunks > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;
+  unsigned long long* state = reinterpret_cast<unsigned long long*>(p->dev.chunk_counts);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(state + nchunks);
+  rsft_status s = check(cudaMemsetAsync(state, 0, (size_t)(nchunks + 1) * 8, st), "compaction state reset");
+  if (s) return s;
+  if (cudaError_t le_ = pdl_launch(k_compact, (unsigned)nchunks, kThreads, 0, st, det, nwords, nchunks, state, ticket,
+                                                   reinterpret_cast<long long*>(idx), capacity,
+                                                   reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
+    return check(le_, "k_compact launch");
+  p->last_launches += 1;
+  return check(cudaGetLastError(), "k_compact launch");
+}
+
+
+
+// Offsets of the per-region detection counts (two-pass parallel scan) + the sorted index list
+// writer (region lists, or the detection words when a list overflowed / is absent).
+rsft_status launch_scan_write(rsft_plan_s* p, int64_t batch, uint32_t* det, int64_t* idx, int64_t capacity,
+                              int64_t* d_count, bool list, cudaStream_t st) {
+  const int64_t n0 = p->n[0];
+  const int64_t np = vote_regions_per_frame(p, 0, n0);
+  const int64_t nregions = np * batch;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
   {
     const int64_t ntiles = (nregions + kScanTile - 1) / kScanTile;
@@ -1477,23 +1396,5 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
   p->last_launches += 2;
   return check(cudaGetLastError(), "region scan/write launch");
 }
-
-rsft_status launch_compact(rsft_plan_s* p, const uint32_t* det, int64_t batch, int64_t* idx,
-                           int64_t capacity, int64_t* d_count, cudaStream_t st) {
-  const int64_t nwords = batch * ((p->ntot + 31) / 32);
-  const int64_t nchunks = (nwords + kChunkWords - 1) / kChunkWords;
-  if (nchunks > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;
-  unsigned long long* state = reinterpret_cast<unsigned long long*>(p->dev.chunk_counts);
-  unsigned int* ticket = reinterpret_cast<unsigned int*>(state + nchunks);
-  rsft_status s = check(cudaMemsetAsync(state, 0, (size_t)(nchunks + 1) * 8, st), "compaction state reset");
-  if (s) return s;
-  if (cudaError_t le_ = pdl_launch(k_compact, (unsigned)nchunks, kThreads, 0, st, det, nwords, nchunks, state, ticket,
-                                                   reinterpret_cast<long long*>(idx), capacity,
-                                                   reinterpret_cast<long long*>(d_count)); le_ != cudaSuccess)
-    return check(le_, "k_compact launch");
-  p->last_launches += 1;
-  return check(cudaGetLastError(), "k_compact launch");
-}
-
 
 }  // namespace rsft
