@@ -550,7 +550,7 @@ __device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const fl
 // bfull / bempty), a vote warp takes frame fi = v, v + nv, ... and runs the per-frame D = 1 vote
 // (vote1d.cuh) while the loop warps fold the next frames: the second stage hides under the HBM
 // stream.  Outputs as k_vote1d: detection words, per-frame counts, local index lists.
-constexpr int kG1BS = 8;                              // bitmap ring slots (>= vote warps)
+constexpr int kG1BS = 16;                             // bitmap ring slots (>= vote warps)
 template <int TAPS, int LPW, int VL = 0>
 __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
                                                       int l0, int nl, int W, int S, int chunk, uint32_t* __restrict__ bitmaps,
@@ -1720,7 +1720,7 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   auto kern = k_gather1d<TAPS, LPW, VL>;
   const int ncw = (nl + LPW - 1) / LPW;
   const char* env_v = getenv("RSFT_G1_VOTE_WARPS");
-  const int nv = VL ? (env_v && env_v[0] ? std::max(1, std::min(atoi(env_v), kG1BS)) : 4) : 0;
+  const int nv = VL ? (env_v && env_v[0] ? std::max(1, std::min(atoi(env_v), kG1BS)) : 8) : 0;   // 6-12 measured alike, 4 slower
   const int threads = 32 * (ncw + 1 + nv);
   const int W = (int)(p->b[0] < p->n[0] ? p->W[0] : p->n[0]);
   const size_t fbytes = (size_t)p->n[0] * 8;

@@ -32,25 +32,36 @@ __device__ __forceinline__ void vote1d_frame(const PlanDev& pd, const uint32_t (
   // mu = L also a filter loop lf (fewest set buckets among the others)
   uint32_t cmask = 0u;
   int ncand = 0;
-  for (int t = 0; t < ncl; ++t) {
-    int best = 1 << 30, bl = 0;
-#pragma unroll
-    for (int l = 0; l < LP; ++l) {
-      const int pc = __popc(mlo[l]) + __popc(mhi[l]);
-      if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; bl = l; }
-    }
-    cmask |= 1u << bl;
-    ncand += best;
-  }
-  // filter loop lf (mu = L): its mask and sigma in plain registers (no per-test loop select)
   int lf = -1;
   uint32_t flo = 0xffffffffu, fhi = 0xffffffffu, fsg = 0u;
-  if (mu == L && L > 1) {
-    int best = 1 << 30;
+  if (mu == L) {
+    // one pass: the loop with the fewest set buckets gives the candidates, the runner-up filters
+    // (best / runner-up kept in plain registers: compile-time indices only)
+    int b1 = 1 << 30, b2 = 1 << 30, l1 = 0;
+    uint32_t blo = 0u, bhi = 0u, bsg = 0u;
 #pragma unroll
     for (int l = 0; l < LP; ++l) {
-      const int pc = __popc(mlo[l]) + __popc(mhi[l]);
-      if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; lf = l; flo = mlo[l]; fhi = mhi[l]; fsg = (uint32_t)sg[l]; }
+      const int pc = l < L ? __popc(mlo[l]) + __popc(mhi[l]) : (1 << 30);
+      if (pc < b1) {
+        if (b1 < (1 << 30)) { b2 = b1; lf = l1; flo = blo; fhi = bhi; fsg = bsg; }
+        b1 = pc; l1 = l; blo = mlo[l]; bhi = mhi[l]; bsg = (uint32_t)sg[l];
+      } else if (pc < b2) {
+        b2 = pc; lf = l; flo = mlo[l]; fhi = mhi[l]; fsg = (uint32_t)sg[l];
+      }
+    }
+    cmask = 1u << l1;
+    ncand = b1;
+    if (b2 >= (1 << 30)) lf = -1;
+  } else {
+    for (int t = 0; t < ncl; ++t) {
+      int best = 1 << 30, bl = 0;
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        const int pc = __popc(mlo[l]) + __popc(mhi[l]);
+        if (l < L && !((cmask >> l) & 1u) && pc < best) { best = pc; bl = l; }
+      }
+      cmask |= 1u << bl;
+      ncand += best;
     }
   }
   if (2 * ncand * A <= N) {                         // ---- candidate mode
@@ -124,6 +135,7 @@ __device__ __forceinline__ void vote1d_frame(const PlanDev& pd, const uint32_t (
     const int w = w0 + lane;
     uint32_t v = 0u;
     if (w < nw) { v = dw[w]; dw[w] = 0u; det[w] = v; }
+    if (__ballot_sync(0xffffffffu, v != 0u) == 0u) continue;   // most words of a frame are empty
     const int c = __popc(v);
     int incl = c;
 #pragma unroll
