@@ -671,6 +671,7 @@ __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64
         }
         det[it] = word;
       }
+      if (__ballot_sync(0xffffffffu, word != 0u) == 0u) continue;   // no detection in these 32 words
       const int c = __popc(word);
       int incl = c;
 #pragma unroll
