@@ -75,6 +75,13 @@ CASES = [
     ("2d_Blast1", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "fused"),
     ("2d_Blast1_split", (64, 64), (16, 1), 3, dict(p_fa=1e-3), 2, "split"),
     ("2d_rect_cheb40", (128, 128), (16, 16), 4, dict(prewin="cheb", prewin_param=40.0, p_fa=1e-4), 2, "fused"),
+    # D = 2 votes at N_1 = 128 / 256: c4's shape, dense spectra, every vote mode, B_0 = 64,
+    # B_1 = 64 (two-word bucket rows)
+    ("2d_v_c4like", (1024, 256), (32, 16), 6, dict(p_fa=1e-3), 2, "fused"),
+    ("2d_v_dense_mu", (256, 256), (16, 16), 10, dict(p_fa=0.2, mu=3), 2, "fused"),
+    ("2d_v_mu1_dense", (512, 128), (16, 8), 4, dict(p_fa=0.05, mu=1), 2, "fused"),
+    ("2d_v_L12_B64", (256, 256), (64, 8), 12, dict(p_fa=1e-2, mu=9, random_tau=True), 2, "fused"),
+    ("2d_v_B1_64", (128, 256), (8, 64), 5, dict(p_fa=1e-2), 2, "fused"),
     ("3d_B_eq_N_last", (16, 32, 32), (4, 8, 32), 3, dict(p_fa=1e-3), 1, "split"),
     # tensor-core split fold (k_split_mma: N_last = 64, A_1 % 16 == 0, L <= 16, L % 4 == 0)
     ("3d_mma_A16", (16, 128, 64), (4, 8, 8), 8, dict(p_fa=1e-3, random_tau=True), 2, "split"),
