@@ -30,6 +30,7 @@
 namespace rsft {
 
 __constant__ float2 c_tw128[128];   // e^{-j 2 pi k / 128}, k < 128 (fp64-rounded at bind)
+__constant__ float2 c_tw512[512];   // e^{-j 2 pi k / 512}, k < 512 (k_gather1d with B_0 > 64)
 
 // Multi-axis view of a shared-memory array: element (i_0, ..., i_{k-1}) lives at
 // sum_a i_a * st[a].  Axis 0 (loops) may have any size; axes >= 1 are powers of two.
@@ -551,13 +552,21 @@ __device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const fl
 // (vote1d.cuh) while the loop warps fold the next frames: the second stage hides under the HBM
 // stream.  Outputs as k_vote1d: detection words, per-frame counts, local index lists.
 constexpr int kG1BS = 16;                             // bitmap ring slots (>= vote warps)
-template <int TAPS, int LPW, int VL = 0>
+// MB = buckets per lane: 2 for B <= 64 (B = 64: lane j owns buckets j and j + 32; B <= 32: the
+// lanes' sums are folded by shuffles), B / 32 for B = 128 and 256 (lane j owns buckets j + 32 m;
+// the B-point FFT is an in-lane MB-point DIF, the twiddles W_B^{j k1} and a 32-point DIF across
+// the lanes: lane p slot r then holds X[brev_MB(r) + MB brev5(p)]).
+// seg != 0: segment mode (x [batch][L][N]): loop l0 + l runs on segment l0 + l of each
+// frame; the producer streams the nl segments of every frame, each gathered by its loop's warp.
+template <int TAPS, int LPW, int VL = 0, int MB = 2>
 __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, const float2* __restrict__ x, int64_t batch,
                                                       int l0, int nl, int W, int S, int chunk, uint32_t* __restrict__ bitmaps,
                                                       float2* __restrict__ spectra, int64_t bm_stride,
                                                       int64_t sp_stride, int nv, uint32_t* __restrict__ vdet,
                                                       unsigned long long* __restrict__ rcount, uint32_t* __restrict__ slots,
-                                                      int list_cap) {
+                                                      int list_cap, int seg) {
+  constexpr int TWN = MB > 2 ? 512 : 128;            // twiddle table W_TWN^k in shared memory
+  constexpr int LM = MB == 8 ? 3 : MB == 4 ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = pd.n[0], B = pd.b[0], lgb = pd.lgb[0];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -566,7 +575,7 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + S;
   float2* tw = reinterpret_cast<float2*>(smem + 16 * S + 128 - ((16 * S) & 127));  // 128-B aligned
-  unsigned char* ring = reinterpret_cast<unsigned char*>(tw + 128);
+  unsigned char* ring = reinterpret_cast<unsigned char*>(tw + TWN);
   // fused vote state after the ring: bfull / bempty [BS] | bitmap slots [BS][L wpl] | sinv [VL] |
   // per vote warp: detection words [N/32], ent [32], queue [64]
   uint64_t* bfull = reinterpret_cast<uint64_t*>(ring + (size_t)S * fbytes);
@@ -575,7 +584,7 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
   uint32_t* bslot = reinterpret_cast<uint32_t*>(bempty + kG1BS);
   int* vsinv = reinterpret_cast<int*>(bslot + kG1BS * bsw);
   uint32_t* vbase = reinterpret_cast<uint32_t*>(vsinv + (VL ? VL : 1));
-  if (tid < 128) tw[tid] = c_tw128[tid];
+  for (int i = tid; i < TWN; i += blockDim.x) tw[i] = MB > 2 ? c_tw512[i] : c_tw128[i];
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], ncw); }
     if (VL) for (int s = 0; s < kG1BS; ++s) { mbar_init(&bfull[s], ncw); mbar_init(&bempty[s], 1); }
@@ -620,17 +629,20 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
     }
   }
 
-  if (warp == ncw) {                                // ---- producer: whole frames, S-deep ring
+  if (warp == ncw) {                                // ---- producer: whole frames (segments), S-deep ring
     if (lane == 0) {
       int s = 0;
-      uint32_t ph = 0;                              // empty-barrier parity of slot s's previous use
-      for (int64_t fi = 0; fi < nfr; ++fi) {
-        if (fi >= S) mbar_wait(&empty[s], ph);
+      const int64_t nit = seg ? nfr * nl : nfr;
+      for (int64_t g = 0; g < nit; ++g) {
+        if (g >= S) mbar_wait(&empty[s], (uint32_t)(((g / S) - 1) & 1));   // use u + 1 waits for parity u & 1
         mbar_expect_tx(&full[s], fbytes);
-        const char* src = reinterpret_cast<const char*>(x + (size_t)(blockIdx.x + fi * gridDim.x) * N);
+        const int64_t fi = seg ? g / nl : g;
+        const int64_t frame = blockIdx.x + fi * gridDim.x;
+        const int64_t row = seg ? frame * pd.L + l0 + (g - fi * nl) : frame;
+        const char* src = reinterpret_cast<const char*>(x + (size_t)row * N);
         for (uint32_t o = 0; o < fbytes; o += (uint32_t)chunk)
           tma_load_1d(ring + (size_t)s * fbytes + o, src + o, (uint32_t)chunk, &full[s]);
-        if (++s == S) { s = 0; if (fi >= 2 * S - 1) ph ^= 1u; }   // use u + 1 waits for parity u & 1
+        if (++s == S) s = 0;
       }
     }
     return;
@@ -663,11 +675,11 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
     const int hh = 16 >> q;
-    stw[q] = tw[((lane & (hh - 1)) * 64) / hh];
+    stw[q] = tw[((lane & (hh - 1)) * (TWN / 2)) / hh];
   }
   // half-bucket twiddles e^{-j pi b / B} of the lane's buckets (L1), stage-1 twiddle (B = 64)
-  const float2 sh0 = shift ? tw[(lane & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
-  const float2 sh1 = shift ? tw[((lane + 32) & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
+  const float2 sh0 = MB > 2 ? make_float2(1.f, 0.f) : shift ? tw[(lane & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
+  const float2 sh1 = MB > 2 ? make_float2(1.f, 0.f) : shift ? tw[((lane + 32) & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
   const float2 w64 = tw[2 * lane];
   const int wpl = pd.wpl;
 
@@ -677,23 +689,49 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
     const int64_t frame = blockIdx.x + fi * gridDim.x;
     const int bsl = (int)(fi & (kG1BS - 1));
     if (VL && fi >= kG1BS) mbar_wait(&bempty[bsl], (uint32_t)(((fi / kG1BS) - 1) & 1));   // slot voted
-    mbar_wait(&full[s], ph);
-    const unsigned char* xs = ring + (size_t)s * fbytes;
-    // even taps k -> bucket lane, odd taps -> bucket lane + 32 (B = 64); for B <= 32 both
-    // parities land in bucket lane mod B and are added below (compile-time register indices)
-    float2 acc[LPW][2];
+    // tap k -> bucket lane + 32 (k mod MB) (B = 32 MB; B = 64: even / odd taps); for B <= 32
+    // both parities land in bucket lane mod B and are added below (compile-time register indices)
+    float2 acc[LPW][MB];
+    if (seg) {
+      // one ring slot per (frame, loop j): every loop warp passes every slot in order (so no
+      // warp runs two phases ahead of a slot's barrier); the owner of loop j gathers from it
 #pragma unroll
-    for (int q = 0; q < LPW; ++q) {
-      acc[q][0] = acc[q][1] = make_float2(0.f, 0.f);
+      for (int q = 0; q < LPW; ++q)
 #pragma unroll
-      for (int k = 0; k < TAPS; ++k) {
-        const float2 v = *reinterpret_cast<const float2*>(xs + off[q][k]);
-        acc[q][k & 1] = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, acc[q][k & 1]);
+        for (int m = 0; m < MB; ++m) acc[q][m] = make_float2(0.f, 0.f);
+      for (int j = 0; j < nl; ++j) {
+        mbar_wait(&full[s], ph);
+        const unsigned char* xs = ring + (size_t)s * fbytes;
+#pragma unroll
+        for (int q = 0; q < LPW; ++q) {
+          if (lid[q] != j) continue;                // warp-uniform
+#pragma unroll
+          for (int k = 0; k < TAPS; ++k) {
+            const float2 v = *reinterpret_cast<const float2*>(xs + off[q][k]);
+            acc[q][k % MB] = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, acc[q][k % MB]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) { s = 0; ph ^= 1u; }
       }
+    } else {
+      mbar_wait(&full[s], ph);
+      const unsigned char* xs = ring + (size_t)s * fbytes;
+#pragma unroll
+      for (int q = 0; q < LPW; ++q) {
+#pragma unroll
+        for (int m = 0; m < MB; ++m) acc[q][m] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < TAPS; ++k) {
+          const float2 v = *reinterpret_cast<const float2*>(xs + off[q][k]);
+          acc[q][k % MB] = __ffma2_rn(make_float2(wt[q][k], wt[q][k]), v, acc[q][k % MB]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);        // slot free: the rest is in registers
+      if (++s == S) { s = 0; ph ^= 1u; }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);          // slot free: the rest is in registers
-    if (++s == S) { s = 0; ph ^= 1u; }
 
 #pragma unroll
     for (int q = 0; q < LPW; ++q) {
@@ -702,7 +740,47 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
       const float gamma = gam[q];
       uint32_t* bmw = bitmaps + (size_t)frame * bm_stride + (size_t)l * wpl;
       float2* sp = spectra ? spectra + (size_t)frame * sp_stride + (size_t)l * pd.btot : nullptr;
-      if (B == 64) {
+      if constexpr (MB > 2) {                       // B = 32 MB (128, 256)
+        float2 v[MB];
+#pragma unroll
+        for (int m = 0; m < MB; ++m)                // half-bucket twiddles e^{-j pi b / B} (L1)
+          v[m] = shift ? cmul(acc[q][m], tw[(lane + 32 * m) << (8 - lgb)]) : acc[q][m];
+#pragma unroll
+        for (int st = 0; st < LM; ++st) {           // in-lane MB-point DIF over m (bit-reversed out)
+#pragma unroll
+          for (int e = 0; e < MB / 2; ++e) {
+            const int span = MB >> (st + 1);
+            const int j = e & (span - 1), blk = (e / span) * 2 * span;
+            const float2 a = v[blk + j], b = v[blk + j + span];
+            v[blk + j] = cadd(a, b);
+            v[blk + j + span] = j == 0 ? csub(a, b) : cmul(csub(a, b), tw[j * (256 / span)]);
+          }
+        }
+#pragma unroll
+        for (int r = 1; r < MB; ++r) {              // W_B^{lane k1}, k1 = brev_MB(r)
+          const int k1 = brev(r, LM);
+          v[r] = cmul(v[r], tw[((lane * k1) & (B - 1)) << (9 - lgb)]);
+        }
+        int val = 0;
+#pragma unroll
+        for (int r = 0; r < MB; ++r) {
+          v[r] = warp_dif(v[r], lane, 5, stw);
+          val |= (v[r].x * v[r].x + v[r].y * v[r].y > gamma ? 1 : 0) << r;
+          if (sp) sp[brev(r, LM) + MB * brev(lane, 5)] = v[r];
+        }
+        uint32_t wd[MB];
+#pragma unroll
+        for (int t = 0; t < MB; ++t) {              // word t: bucket k = 32 t + lane
+          const int k = 32 * t + lane;
+          const int vq = __shfl_sync(0xffffffffu, val, brev(k >> LM, 5));
+          wd[t] = __ballot_sync(0xffffffffu, (vq >> brev(k & (MB - 1), LM)) & 1);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int t = 0; t < MB; t += 4)
+            *reinterpret_cast<uint4*>(bmw + t) = make_uint4(wd[t], wd[t + 1], wd[t + 2], wd[t + 3]);
+        }
+      } else if (B == 64) {
         const float2 a = cmul(acc[q][0], sh0), c = cmul(acc[q][1], sh1);
         float2 u = cadd(a, c), v = cmul(csub(a, c), w64);   // X[2k] <- u, X[2k+1] <- v
         u = warp_dif(u, lane, 5, stw);
@@ -1712,12 +1790,12 @@ static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch
 }
 
 
-template <int TAPS, int LPW, int VL = 0>
+template <int TAPS, int LPW, int VL = 0, int MB = 2>
 static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
                                      void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride,
                                      uint32_t* vdet = nullptr, unsigned long long* rcount = nullptr,
-                                     uint32_t* slots = nullptr, int list_cap = 0) {
-  auto kern = k_gather1d<TAPS, LPW, VL>;
+                                     uint32_t* slots = nullptr, int list_cap = 0, int seg = 0) {
+  auto kern = k_gather1d<TAPS, LPW, VL, MB>;
   const int ncw = (nl + LPW - 1) / LPW;
   const char* env_v = getenv("RSFT_G1_VOTE_WARPS");
   const int nv = VL ? (env_v && env_v[0] ? std::max(1, std::min(atoi(env_v), kG1BS)) : 8) : 0;   // 6-12 measured alike, 4 slower
@@ -1732,7 +1810,7 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
                            : 0;
   int S = env_s && env_s[0] ? atoi(env_s) : 0;
   if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048 - vbytes) / fbytes));
-  const size_t smem = 16 * S + 128 + 1024 + S * fbytes + vbytes;
+  const size_t smem = 16 * S + 128 + (MB > 2 ? 4096 : 1024) + S * fbytes + vbytes;
   const char* env_k = getenv("RSFT_G1_CHUNK");        // bytes per bulk copy (divides the frame)
   int chunk = env_k && env_k[0] ? atoi(env_k) : (int)std::min<size_t>(fbytes, 8192);
   if (chunk <= 0 || chunk % 16 || fbytes % chunk) chunk = (int)fbytes;
@@ -1747,22 +1825,46 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, (unsigned)threads, smem, st, p->dev,
                                    reinterpret_cast<const float2*>(d_x), batch, l0, nl, W, S, chunk, bm,
                                    reinterpret_cast<float2*>(spectra), bm_stride, sp_stride, nv, vdet, rcount, slots,
-                                   list_cap); le_ != cudaSuccess)
+                                   list_cap, seg); le_ != cudaSuccess)
     return check(le_, "k_gather1d launch");
   p->last_launches += 1;
   return check(cudaGetLastError(), "k_gather1d launch");
 }
 
 static rsft_status launch_gather1d(rsft_plan_s* p, const void* d_x, int64_t batch, int l0, int nl, uint32_t* bm,
-                                   void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride) {
+                                   void* spectra, cudaStream_t st, int64_t bm_stride, int64_t sp_stride, int seg = 0) {
   const int taps = gather1d_taps(p);
   const int lpw = nl > 16 ? 2 : 1;
-#define RSFT_G1(T) \
-  if (taps == T) return lpw == 1 ? launch_gather1d_t<T, 1>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride) \
-                                 : launch_gather1d_t<T, 2>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride);
-  RSFT_G1(4) RSFT_G1(8) RSFT_G1(16) RSFT_G1(32)
+  const int mb = p->b[0] <= 64 ? 2 : (int)(p->b[0] / 32);
+#define RSFT_G1(T, M) \
+  if (taps == T && mb == M) \
+    return lpw == 1 ? launch_gather1d_t<T, 1, 0, M>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride, nullptr, nullptr, nullptr, 0, seg) \
+                    : launch_gather1d_t<T, 2, 0, M>(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride, sp_stride, nullptr, nullptr, nullptr, 0, seg);
+  RSFT_G1(4, 2) RSFT_G1(8, 2) RSFT_G1(16, 2) RSFT_G1(32, 2)
+  RSFT_G1(4, 4) RSFT_G1(8, 4) RSFT_G1(16, 4) RSFT_G1(32, 4)
+  RSFT_G1(8, 8) RSFT_G1(16, 8) RSFT_G1(32, 8)
 #undef RSFT_G1
   return RSFT_E_UNSUPPORTED;
+}
+
+// Segment mode for D = 1 gather plans: one launch per <= 32 loops, loop l on segment l of every
+// frame (x [batch][L][N]); bitmaps [batch][L][wpl], spectra [batch][L][B].
+static rsft_status launch_gather1d_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm,
+                                            void* spectra, cudaStream_t st) {
+  const int L = p->L;
+  const int c = (L + kMaxLaunchLoops - 1) / kMaxLaunchLoops, per = (L + c - 1) / c;
+  int launches = 0;
+  for (int a = 0; a < L; a += per) {
+    const int m = std::min(per, L - a);
+    void* sp = spectra ? reinterpret_cast<char*>(spectra) + (size_t)a * p->btot * 8 : nullptr;
+    p->last_launches = 0;
+    rsft_status s = launch_gather1d(p, d_x, batch, a, m, bm + (size_t)a * p->dev.wpl, sp, st,
+                                    (int64_t)L * p->dev.wpl, (int64_t)L * p->btot, 1);
+    if (s) return s;
+    launches += p->last_launches;
+  }
+  p->last_launches = launches;
+  return RSFT_OK;
 }
 
 // rsft_run for D = 1 gather plans: the fold kernel with vote warps (first and second stage in one
@@ -1793,6 +1895,10 @@ static rsft_status launch_fused_t(rsft_plan_s* p, const void* d_x, int64_t batch
     if (p->D == 1 && (frame_stride == 0 || frame_stride == p->ntot) && gather1d_taps(p) && !(g1 && g1[0] && g1[0] != '0'))
       return launch_gather1d(p, d_x, batch, l0, nl, bm, spectra, st, bm_stride ? bm_stride : (int64_t)nl * p->dev.wpl,
                              sp_stride ? sp_stride : (int64_t)nl * p->btot);
+    if (p->D == 1 && p->b[0] > 64) {                 // the streaming 1-D form folds B <= 64 only
+      set_error("k_fused: D = 1 with B > 64 needs the gather form (support W <= 1024)");
+      return RSFT_E_UNSUPPORTED;
+    }
   }
   auto kern = p->D == 2 ? k_fused<LP, F2.u, F2.stages, F2.threads, F2.ctas> : k_fused<LP, F1.u, F1.stages, F1.threads, F1.ctas>;
   size_t smem = fused_smem_bytes(p, nl, LP);
@@ -2039,6 +2145,11 @@ static rsft_status launch_fused_lp(rsft_plan_s* p, int lp, const void* d_x, int6
 
 rsft_status launch_segments(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, void* spectra,
                             cudaStream_t st) {
+  {
+    const char* g1 = getenv("RSFT_NO_GATHER1D");      // read per launch
+    if (p->D == 1 && gather1d_taps(p) && !(g1 && g1[0] && g1[0] != '0'))
+      return launch_gather1d_segments(p, d_x, batch, bm, spectra, st);
+  }
   if (resolve_mode(p, batch) == RSFT_MODE_FUSED && loop_pad(1) == 2) {
     return launch_segments_fused_t<2>(p, d_x, batch, bm, spectra, st);
   }
@@ -2127,7 +2238,14 @@ rsft_status upload_twiddles(cudaStream_t st) {
     double a = -2.0 * M_PI * (double)k / 128.0;
     tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
-  return check(cudaMemcpyToSymbolAsync(c_tw128, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st), "twiddles");
+  rsft_status s = check(cudaMemcpyToSymbolAsync(c_tw128, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st), "twiddles");
+  if (s) return s;
+  float2 t5[512];
+  for (int k = 0; k < 512; ++k) {
+    double a = -2.0 * M_PI * (double)k / 512.0;
+    t5[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  return check(cudaMemcpyToSymbolAsync(c_tw512, t5, sizeof(t5), 0, cudaMemcpyHostToDevice, st), "twiddles");
 }
 
 }  // namespace rsft

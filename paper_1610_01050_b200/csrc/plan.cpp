@@ -135,7 +135,7 @@ rsft_status rebuild_tables(rsft_plan_s* p) {
     const int64_t n = p->n[ld], b = p->b[ld], W = n / 32;
     const size_t bytes = (size_t)L * b * W * 4;
     p->xmask.clear();
-    if (bytes <= kMaxXmaskBytes) {
+    if (bytes <= kMaxXmaskBytes && b <= kMaxB) {
       p->xmask.assign((size_t)L * b * W, 0u);
       for (int l = 0; l < L; ++l) {
         const int64_t s = p->sigma[l * D + ld];
@@ -209,7 +209,7 @@ void layout_workspace(rsft_plan_s* p) {
   {
     const int64_t n = p->n[p->D - 1], b = p->b[p->D - 1];
     w.xmask_bytes = (size_t)p->L * b * (n / 32) * 4;
-    if (w.xmask_bytes > kMaxXmaskBytes) w.xmask_bytes = 0;
+    if (w.xmask_bytes > kMaxXmaskBytes || b > kMaxB) w.xmask_bytes = 0;   // the vote's mask forms: B_last <= 64
   }
   w.xmask_off = off; off = align256(off + w.xmask_bytes);
   w.ntab_bytes = (w.xmask_bytes && p->b[p->D - 1] >= 4 && 4 * w.xmask_bytes <= kMaxNibbleBytes) ? 4 * w.xmask_bytes : 0;
@@ -368,7 +368,7 @@ rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out) {
     int64_t n = P.n[d], b = P.b[d], w = P.support[d];
     if (!is_pow2(n) || !is_pow2(b) || b > n) return RSFT_E_SHAPE;
     if (n > (int64_t(1) << 30)) return RSFT_E_UNSUPPORTED;
-    if (b > kMaxB) return RSFT_E_UNSUPPORTED;
+    if (b > (P.ndim == 1 ? kMaxB1d : kMaxB)) return RSFT_E_UNSUPPORTED;
     if (b < n) {
       if (w == 0) w = n;
       if (w < 0 || w > n || w % 2 || (w / 2) % b) return RSFT_E_SHAPE;
@@ -406,6 +406,8 @@ rsft_status rsft_plan_create(const rsft_params* params, rsft_plan_t* out) {
     p->prewin[d] = prewindow(P, p->n[d]);
     p->flatg[d] = flat_proto(p->n[d], p->b[d], p->W[d], P.flat_atten_db);
   }
+  // D = 1 with B > 64: only the gather-form fold (k_gather1d, support W <= 1024) folds it
+  if (p->D == 1 && p->b[0] > kMaxB && !gather1d_taps(p)) { delete p; return RSFT_E_UNSUPPORTED; }
   rebuild_tables(p);
   layout_workspace(p);
   if (resolve_mode(p, P.max_batch) < 0) { delete p; return RSFT_E_UNSUPPORTED; }

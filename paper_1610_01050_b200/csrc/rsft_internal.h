@@ -17,6 +17,7 @@ constexpr int kMaxLoops = 64;         // L <= 63: 6 bit planes of vote counts
 constexpr int kMaxLaunchLoops = 32;   // loops per fold launch (more loops: several passes)
 constexpr int kSizingSms = 148;     // host-only plan: workspace sized for a B200 (rsft.h)
 constexpr int kMaxB = 64;          // register FFT lines and lane folds support B_d <= 64
+constexpr int kMaxB1d = 256;       // D = 1 gather form (k_gather1d): B = 128, 256 as 4 / 8 buckets per lane
 constexpr int64_t kChunkWords = 8192;  // compaction chunk: words of the detection bitmap
 constexpr int kThreads = 256;          // CTA size of most kernels
 constexpr int kThreadsFft = 1024;      // split-mode outer FFT: one L2 round trip per thread

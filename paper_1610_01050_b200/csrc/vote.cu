@@ -1175,13 +1175,11 @@ static rsft_status launch_vote_mode(rsft_plan_s* p, const uint32_t* bm, int64_t 
 bool vote1d_usable(const rsft_plan_s* p) {
   const char* off = getenv("RSFT_NO_VOTE1D");
   if (off && off[0] && off[0] != '0') return false;
-  return p->D == 1 && p->n[0] >= 32 && p->n[0] <= 32768 && p->L <= 32;
+  return p->D == 1 && p->n[0] >= 32 && p->n[0] <= 32768 && p->L <= 32 && p->b[0] <= 64;
 }
 
-static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {
-  const char* off = getenv("RSFT_NO_VOTE1D");        // read per launch: tests select either kernel
-  if (off && off[0] && off[0] != '0') return false;
-  return p->D == 1 && !counts && p->n[0] >= 32 && p->n[0] <= 32768 && p->L <= 32;
+static bool vote1d_ok(const rsft_plan_s* p, uint8_t* counts) {   // RSFT_NO_VOTE1D read per launch
+  return !counts && vote1d_usable(p);             // the masks of one loop are 64-bit (B <= 64)
 }
 
 static rsft_status launch_vote1d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, uint32_t* det,

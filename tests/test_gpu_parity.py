@@ -47,6 +47,14 @@ CASES = [
     ("1d_g_B_eq_N", (64,), (64,), 4, dict(p_fa=1e-2), 3, "fused"),
     ("1d_g_B1", (256,), (1,), 3, dict(p_fa=1e-2), 3, "fused"),
     ("1d_g_b32_dense", (512,), (32,), 7, dict(p_fa=1e-3, random_tau=True), 4, "fused"),
+    # D = 1 with B = 128 / 256 (4 / 8 buckets per lane; P:558 B_opt = 128, Figs. ROC_K / ROC_CO
+    # B = 256): full support, short support, two loops per warp, B = N, > 32 loops (two passes)
+    ("1d_B128_full", (1024,), (128,), 6, dict(p_fa=1e-3, random_tau=True), 3, "fused"),
+    ("1d_B256_full", (1024,), (256,), 5, dict(p_fa=1e-3), 2, "fused"),
+    ("1d_B128_w512", (4096,), (128,), 8, dict(support=(512,), random_tau=True, p_fa=1e-3, mu=6), 3, "fused"),
+    ("1d_B256_w512_L20", (2048,), (256,), 20, dict(support=(512,), p_fa=1e-2, mu=14), 2, "fused"),
+    ("1d_B256_eq_N", (256,), (256,), 3, dict(p_fa=1e-2), 2, "fused"),
+    ("1d_B128_L40", (1024,), (128,), 40, dict(support=(256,), p_fa=1e-2, mu=30, random_tau=True), 2, "fused"),
     # D = 1 warp-per-frame vote (k_vote1d): candidate mode (mu near L) and dense mode (mu small)
     ("1d_v_mu_half", (4096,), (64,), 8, dict(support=(512,), random_tau=True, p_fa=1e-2, mu=4), 6, "fused"),
     ("1d_v_mu1", (2048,), (32,), 4, dict(support=(256,), p_fa=1e-2, mu=1), 5, "fused"),
@@ -117,7 +125,8 @@ def test_parity_ffma_fold_on_mma_shapes(case, monkeypatch):
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
-G1_CASES = [c for c in CASES if c[0].startswith("1d_") and c[0] != "1d_g_L20_w1024"]   # too big for the streaming kernel
+# the streaming kernel folds B <= 64 and frames whose tables fit (not 1d_g_L20_w1024)
+G1_CASES = [c for c in CASES if c[0].startswith("1d_") and c[0] != "1d_g_L20_w1024" and c[2][0] <= 64]
 
 
 @pytest.mark.parametrize("case", G1_CASES, ids=[c[0] for c in G1_CASES])
@@ -417,6 +426,9 @@ def test_variant_b_c5_full_cube():
     ((128, 64), (16, 8), 5, "fused"),
     ((1024,), (64,), 50, "fused"),                  # the paper's T = 50
     ((1024,), (32,), 4, "fused"),
+    ((1024,), (128,), 6, "fused"),                  # gather-form segments, 4 buckets per lane
+    ((1024,), (256,), 12, "fused"),                 # 8 buckets per lane
+    ((4096,), (64,), 3, "fused"),                   # W = N > 1024: the streaming 1-D fold, per loop
     ((32, 16, 64), (4, 4, 8), 3, "split"),
     ((64, 128, 32), (8, 16, 8), 4, "split"),          # c3-like: multi-a0 boxes, batched segments
     ((128, 64), (16, 16), 3, "split"),                # D = 2 split, batched segments

@@ -106,7 +106,9 @@ def test_set_schedule_roundtrip_and_errors():
 @pytest.mark.parametrize("kw,status", [
     (dict(n=(100,), b=(4,), loops=1), 2),                   # N not a power of two
     (dict(n=(64,), b=(128,), loops=1), 2),                  # B > N
-    (dict(n=(1024,), b=(128,), loops=1), 4),                # B > 64 unsupported
+    (dict(n=(4096,), b=(128,), loops=1), 4),                # D = 1, B > 64 needs the gather form (W <= 1024)
+    (dict(n=(2048,), b=(512,), loops=1, support=(1024,)), 4),   # D = 1, B > 256
+    (dict(n=(256, 256), b=(128, 8), loops=1), 4),           # D = 2, B_d > 64
     (dict(n=(64,), b=(8,), loops=1, support=(24,)), 2),     # 2B does not divide W
     (dict(n=(64,), b=(8,), loops=0), 1),
     (dict(n=(64,), b=(8,), loops=64), 4),                   # L > 63 (6 vote bit planes)
@@ -122,6 +124,25 @@ def test_plan_argument_errors(kw, status):
     with pytest.raises(B.RsftError) as e:
         B.Plan(n, b, loops, **kw)
     assert e.value.status == status
+
+
+@pytest.mark.parametrize("n,b,w", [((1024,), (128,), 0), ((1024,), (256,), 0), ((4096,), (256,), 1024),
+                                   ((256,), (256,), 0)])
+def test_plan_1d_large_b(n, b, w):
+    """D = 1 with B = 128 / 256 (the paper's B_opt = 128 at K = 100; B = 256 in Figs.
+    ROC_K / ROC_CO): planned in the gather form (support W <= 1024); the schedule,
+    windows and thresholds match the oracle's tables."""
+    kw = dict(support=(w,)) if w else {}
+    p = B.Plan(n, b, 4, seed=5, random_tau=True, **kw)
+    assert p.mode == 1
+    op = R.Params(n=n, b=b, loops=4, seed=5, random_tau=True, **kw)
+    tb = R.make_tables(op)
+    sig, _, tau = p.schedule()
+    np.testing.assert_array_equal(sig, tb.sigma)
+    np.testing.assert_array_equal(tau, tb.tau)
+    be, ga = p.thresholds()
+    for l in range(4):
+        assert math.isclose(be[l], R.beta(op, tb, l), rel_tol=1e-9)
 
 
 def test_device_calls_require_bind():
