@@ -631,18 +631,20 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
 
   if (warp == ncw) {                                // ---- producer: whole frames (segments), S-deep ring
     if (lane == 0) {
-      int s = 0;
+      int s = 0, j = 0;
+      uint32_t ph = 0;                              // empty-barrier parity of slot s's previous use
+      int64_t fi = 0;
       const int64_t nit = seg ? nfr * nl : nfr;
-      for (int64_t g = 0; g < nit; ++g) {
-        if (g >= S) mbar_wait(&empty[s], (uint32_t)(((g / S) - 1) & 1));   // use u + 1 waits for parity u & 1
+      for (int64_t g = 0; g < nit; ++g) {           // item g = (frame fi, segment j)
+        if (g >= S) mbar_wait(&empty[s], ph);
         mbar_expect_tx(&full[s], fbytes);
-        const int64_t fi = seg ? g / nl : g;
         const int64_t frame = blockIdx.x + fi * gridDim.x;
-        const int64_t row = seg ? frame * pd.L + l0 + (g - fi * nl) : frame;
+        const int64_t row = seg ? frame * pd.L + l0 + j : frame;
         const char* src = reinterpret_cast<const char*>(x + (size_t)row * N);
         for (uint32_t o = 0; o < fbytes; o += (uint32_t)chunk)
           tma_load_1d(ring + (size_t)s * fbytes + o, src + o, (uint32_t)chunk, &full[s]);
-        if (++s == S) s = 0;
+        if (++s == S) { s = 0; if (g >= 2 * S - 1) ph ^= 1u; }   // use u + 1 waits for parity u & 1
+        if (!seg || ++j == nl) { j = 0; ++fi; }
       }
     }
     return;
