@@ -6,8 +6,10 @@ as a fraction of the B200 peak, at 1/2/4/8 GPUs).
                     [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...         (one rank per GPU, NCCL)
 
-A step is one pass of the whole hot path (execute = fused fold+FFT+threshold; detect_compact =
-vote + second stage + sorted index list) over one batch of synthetic frames resident in HBM.  Default
+A step is one pass of the whole hot path (fold + FFT + threshold, vote + second stage, sorted index
+list) over one batch of synthetic frames resident in HBM: ONE rsft_run call for fused-mode plans
+(c4 / c2: k_fused2v folds and votes in one kernel; c1: k_gather1d with vote warps), rsft_execute +
+rsft_detect_compact for split-mode plans (c3, c5) or with --two-calls.  Default
 workload: c4 (BASELINE configs[3]: 1024x256 complex64 frames, B=32x16, L=6, P_fa=1e-6),
 4096 frames per GPU (weak scaling: frames shard across GPUs, no collective in the data path).
 `--workload c5_cube` runs the single 512 MiB cube with its L=16 loops sharded across ranks
@@ -308,8 +310,13 @@ def main_gpu(a):
     idx = torch.empty(cap, dtype=torch.int64, device=dev)
     cnt = torch.empty(1, dtype=torch.int64, device=dev)
 
+    # fused-mode plans: rsft_run is ONE fold kernel that also votes (D = 1 gather form, D = 2
+    # warp-specialised k_fused2v) + the scan / index writer; split-mode plans: the fold, outer-FFT
+    # and vote kernels, timed as two ABI calls so that the fold is the "dominant kernel"
+    use_run = a.run or (plan.mode == 1 and not a.two_calls)
+
     def step(events=None):
-        if a.run:
+        if use_run:
             # one rsft_run call (D = 1 gather plans: fold + vote in one kernel); the "dominant
             # kernel" events then bracket the whole call (conservative)
             if events is not None:
@@ -375,6 +382,8 @@ def main_gpu(a):
     peak, peak_src = load_peaks()
     k1_avg = statistics.mean(k1_ms)
     algo_bytes = frames * (8 * plan.ntot + plan.loops * plan.bitmap_words * 4)
+    if use_run:     # the whole call also writes the detection words (N/8 B per frame, §8(d)) + the index list
+        algo_bytes += frames * plan.detect_words * 4 + 8 * min(detections, cap)
     achieved = algo_bytes / (k1_avg / 1000.0) / 1e9
     step_ms = elapsed_ms / a.steps
     value = world * frames / (step_ms / 1000.0)
@@ -383,8 +392,8 @@ def main_gpu(a):
         cpu = cpu_baseline(wl, a.cpu_budget)
     cfg = workload_config(wl, frames)
     cfg["mode"] = {1: "fused", 2: "split"}.get(plan.mode, plan.mode)
-    if a.run:
-        cfg["step_call"] = "rsft_run (one call; roofline times the whole call)"
+    cfg["step_call"] = ("rsft_run (one call; roofline times the whole call)" if use_run
+                        else "rsft_execute + rsft_detect_compact (roofline times rsft_execute)")
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "step_ms": step_stats(per_step),
@@ -393,7 +402,7 @@ def main_gpu(a):
         "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(wl.name),
-                     "kernel": fold_kernel_label(plan, wl) + (" [whole rsft_run call]" if a.run else ""),
+                     "kernel": fold_kernel_label(plan, wl, use_run) + (" [whole rsft_run call]" if use_run else ""),
                      "algorithmic_bytes_per_launch": algo_bytes,
                      "avg_launch_ms": k1_avg, "share_of_step": k1_avg / step_ms, "peak_source": peak_src},
         "gpu_launches": launches,
@@ -410,14 +419,18 @@ def main_gpu(a):
     return 0
 
 
-def fold_kernel_label(plan, wl):
-    """The first-stage kernel(s) rsft_execute launches for this plan (librsft's dispatch rules)."""
+def fold_kernel_label(plan, wl, run=False):
+    """The first-stage kernel(s) rsft_execute (run: rsft_run) launches for this plan (librsft's
+    dispatch rules)."""
     if plan.mode == 2:
         mma = (len(wl.n) == 3 and wl.n[2] == 64 and not os.environ.get("RSFT_NO_MMA"))
         return ("k_split_mma (3xTF32 tcgen05)" if mma else "k_split_fold") + " + k_split_fft (fold + outer FFT + threshold)"
     w = (wl.support[0] if wl.support else 0) or wl.n[0]
     if len(wl.n) == 1 and w % 32 == 0 and w <= 1024 and not os.environ.get("RSFT_NO_GATHER1D"):
         return "k_gather1d (gather-form fold + FFT + threshold)"
+    if run and len(wl.n) == 2 and max(wl.loops, 1) <= 8 and wl.b[0] <= 32 and wl.b[1] in (8, 16, 32) \
+            and wl.n[1] in (128, 256) and wl.n[0] <= 1024 and not os.environ.get("RSFT_NO_FUSED2V"):
+        return "k_fused2v (fold warps + FFT/threshold/vote warps) + k_scan_tiles/k_scan_apply + k_region_write"
     return "k_fused (pre-window+permute+flat window+fold+FFT+threshold)"
 
 
@@ -642,8 +655,10 @@ def main():
     ap.add_argument("--segments", action="store_true", help="time the RSFT in segment mode (P:204)")
     ap.add_argument("--c5-variant", default="B", choices=["A", "B"], help="c5 multi-GPU scheme (DESIGN.md §8)")
     ap.add_argument("--run", action="store_true",
-                    help="issue each step as ONE rsft_run call (D = 1: fold and vote fused in one kernel); the "
-                         "roofline then times the whole call")
+                    help="issue each step as ONE rsft_run call (the default for fused-mode plans, where the fold "
+                         "kernel also votes); the roofline then times the whole call")
+    ap.add_argument("--two-calls", action="store_true",
+                    help="issue each step as rsft_execute + rsft_detect_compact (the fold kernel timed alone)")
     ap.add_argument("--force-collectives", action="store_true",
                     help="initialise an NCCL process group even with one rank, so the multi-GPU code path "
                          "(barriers, max-over-ranks timing, c5 reduce-scatter + all-gather) runs on a 1-GPU lease")

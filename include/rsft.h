@@ -214,10 +214,15 @@ rsft_status rsft_detect_compact(rsft_plan_t plan, const uint32_t* d_bitmaps, int
                                 uint32_t* d_detect, int64_t* d_idx, int64_t capacity,
                                 int64_t* d_count, void* stream);
 
-/* Whole hot path on device buffers: rsft_execute (all loops) + rsft_detect_compact, issued
- * back to back on `stream` (programmatic dependent launches), with the same outputs (d_bitmaps
- * [batch][L][bitmap_words], d_detect [batch][detect_words], sorted indices, *d_count).
- * (Voting inside the fold kernel's per-frame epilogue was measured slower and is not done.)
+/* Whole hot path on device buffers (Alg. 1 l.5-14), with the outputs of rsft_execute
+ * (all loops) + rsft_detect_compact (d_bitmaps [batch][L][bitmap_words], d_detect
+ * [batch][detect_words], sorted indices, *d_count).  Fused-mode plans run first and second stage
+ * in ONE warp-specialised kernel: D = 1 with a flat-window support <= 1024 (k_gather1d with vote
+ * warps) and D = 2 with L <= 8, B_0 <= 32, B_1 in {8, 16, 32}, N_1 in {128, 256}, N_0 <= 1024
+ * (k_fused2v: fold warps stream the frame while epilogue warps FFT, threshold and vote the
+ * previous one); then the region scan + index writer of rsft_detect_compact.  Other plans issue
+ * rsft_execute + rsft_detect_compact back to back on `stream` (programmatic dependent launches).
+ * Bucket values come from a different FFT order than rsft_execute's (equal to fp32 rounding).
  * Errors: as rsft_execute and rsft_detect_compact. */
 rsft_status rsft_run(rsft_plan_t plan, const void* d_x, int64_t batch, uint32_t* d_bitmaps, uint32_t* d_detect,
                      int64_t* d_idx, int64_t capacity, int64_t* d_count, void* stream);

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsft.so")
-SOURCES = ["plan.cpp", "design.cpp", "api.cu", "kernels.cu", "vote.cu", "synth.cu", "bartlett.cu"]
+SOURCES = ["plan.cpp", "design.cpp", "api.cu", "kernels.cu", "fused2v.cu", "vote.cu", "synth.cu", "bartlett.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr",

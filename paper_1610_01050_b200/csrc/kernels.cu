@@ -26,6 +26,7 @@
 #include "kcommon.cuh"
 #include "hcommon.h"
 #include "vote1d.cuh"
+#include "fold.cuh"
 
 namespace rsft {
 
@@ -106,50 +107,6 @@ __device__ __forceinline__ void load_twiddles(float2* tw) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
 }
 
-// Column weights + lane fold.  Lane owns columns c = base + 2*lane_col + e (e = 0,1); its
-// residues (2*lane + e) mod B_last (B_last <= 64 divides 64).  Lanes whose index agrees
-// mod B_last/2 share residues and are summed with xor shuffles.  After the call lanes
-// < max(B_last/2,1) hold residue sums for residues 2*lane + e (e < min(B_last,2)).
-template <int LP>
-__device__ __forceinline__ void colweight(float2 (&acc)[LP][2], const float* __restrict__ hlast,
-                                          int l0, int nl, int nlast, int col) {
-#pragma unroll
-  for (int l = 0; l < LP; ++l) {
-    float2 hc = make_float2(0.f, 0.f);
-    if (l < nl) hc = __ldg(reinterpret_cast<const float2*>(hlast + (size_t)(l0 + l) * nlast + col));
-    acc[l][0].x *= hc.x; acc[l][0].y *= hc.x;
-    acc[l][1].x *= hc.y; acc[l][1].y *= hc.y;
-  }
-}
-
-template <int LP>
-__device__ __forceinline__ void colweight_plain(float2 (&acc)[LP][2], const float* hl, int nlast, int col) {
-#pragma unroll
-  for (int l = 0; l < LP; ++l) {
-    const float2 hc = *reinterpret_cast<const float2*>(hl + (size_t)l * nlast + col);
-    acc[l][0].x *= hc.x; acc[l][0].y *= hc.x;
-    acc[l][1].x *= hc.y; acc[l][1].y *= hc.y;
-  }
-}
-
-template <int LP>
-__device__ __forceinline__ void lane_fold(float2 (&acc)[LP][2], int blast) {
-  for (int off = blast >= 2 ? blast / 2 : 1; off < 32; off <<= 1) {
-#pragma unroll
-    for (int l = 0; l < LP; ++l)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, acc[l][e].x, off),
-                                     __shfl_xor_sync(0xffffffffu, acc[l][e].y, off));
-        acc[l][e] = __fadd2_rn(acc[l][e], o);
-      }
-  }
-  if (blast == 1) {
-#pragma unroll
-    for (int l = 0; l < LP; ++l) acc[l][0] = __fadd2_rn(acc[l][0], acc[l][1]);
-  }
-}
-
 // Residue fold through shared memory (reduce over the lanes that share residues, written
 // to slot[l][r]; segments add).  Same sums as lane_fold, a quarter of its instructions at
 // B_last = 8: every lane stores its LP float4 (acc[l][0], acc[l][1]) to scr[l][lane] (odd l
@@ -192,61 +149,6 @@ __device__ __forceinline__ void colweight_fold(float2 (&acc)[LP][2], const float
                                                int l0, int nl, int nlast, int col, int blast) {
   colweight<LP>(acc, hlast, l0, nl, nlast, col);
   lane_fold<LP>(acc, blast);
-}
-
-// ------------------------------------------------------------------------------------
-// TMA bulk-copy pipeline (per warp): lane 0 streams row segments of x global -> shared
-// with cp.async.bulk (SASS UBLKCP) into an S-deep ring, completion tracked by one
-// mbarrier per stage (expect_tx / complete_tx); all lanes wait on the stage's phase, read
-// their 16 B with LDS.128 and run the FFMA2 fold.  Bytes in flight per warp are explicit
-// ((S-1) x U x 512 B), independent of registers and of ptxas scheduling.
-// One row group: U row-loads of 32 float4 (512 B) per warp, already in the stage buffer.
-// acc[l] += w_row[l] * x for each row.  Rows past the end of a class are zero-filled by
-// the TMA (out-of-bounds box rows) and carry the zero weight row, so they add nothing.
-template <int LP, int U, bool INIT = false>
-__device__ __forceinline__ void fold_group(float2 (&acc)[LP][2], const float4* __restrict__ buf, int lane,
-                                           const float* const (&wrow)[U]) {
-  float4 v[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) v[u] = buf[u * 32 + lane];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if constexpr (LP % 4 == 0) {                   // 16-B weight loads (rows are 16-B aligned)
-      const float4* wr = reinterpret_cast<const float4*>(wrow[u]);
-#pragma unroll
-      for (int l4 = 0; l4 < LP / 4; ++l4) {
-        const float4 w = wr[l4];
-        const float wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (INIT && u == 0) {                    // first row of the group: acc = w * v
-            acc[4 * l4 + i][0] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].x, v[u].y));
-            acc[4 * l4 + i][1] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].z, v[u].w));
-          } else {
-            mac(acc[4 * l4 + i][0], wv[i], v[u].x, v[u].y);
-            mac(acc[4 * l4 + i][1], wv[i], v[u].z, v[u].w);
-          }
-        }
-      }
-    } else {
-      const float2* wr = reinterpret_cast<const float2*>(wrow[u]);
-#pragma unroll
-      for (int l2 = 0; l2 < LP / 2; ++l2) {
-        const float2 w = wr[l2];
-        const float wv[2] = {w.x, w.y};
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (INIT && u == 0) {
-            acc[2 * l2 + i][0] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].x, v[u].y));
-            acc[2 * l2 + i][1] = __fmul2_rn(make_float2(wv[i], wv[i]), make_float2(v[u].z, v[u].w));
-          } else {
-            mac(acc[2 * l2 + i][0], wv[i], v[u].x, v[u].y);
-            mac(acc[2 * l2 + i][1], wv[i], v[u].z, v[u].w);
-          }
-        }
-      }
-    }
-  }
 }
 
 // fold_group with per-row weights formed on the fly: w[l] = h0v[l] * wrow[u][l] (D == 3,
@@ -529,23 +431,6 @@ __global__ void __launch_bounds__(T, C) k_fused(PlanDev pd, const __grid_constan
 // shuffles, no barrier), |.|^2 > gamma_l and the ballot to bitmap words in registers
 // (Alg. 1 l.9-10; Eq. tpd).  No CTA barrier after the prologue.
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ float2 shfl_xor2(float2 v, int m) {
-  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
-}
-
-// 2^lgb-point DIF across lanes (x = element lane mod 2^lgb, lgb <= 5): lane p ends with
-// X[brev(p mod 2^lgb)].  stw[q] = W_{2h}^{lane & (h-1)} for h = 16 >> q.
-__device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const float2 (&stw)[5]) {
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    const int h = 16 >> q;
-    if ((2 * h) > (1 << lgb)) continue;           // warp-uniform
-    const float2 p = shfl_xor2(x, h);
-    x = (lane & h) ? cmul(csub(p, x), stw[q]) : cadd(x, p);
-  }
-  return x;
-}
-
 // Fused c1 path (VL > 0; rsft_run): `nv` vote warps per CTA vote the frames the loop warps just
 // finished -- each loop warp also drops its bitmap words into a BS-slot shared ring (mbarriers
 // bfull / bempty), a vote warp takes frame fi = v, v + nv, ... and runs the per-frame D = 1 vote
@@ -1770,7 +1655,7 @@ __global__ void k_chunk_sum(const float2* __restrict__ F, int nchunk, int64_t bo
 // count (rcount[region]) for the offset scan of rsft_detect_compact.
 // smem: bm [L][lw] | E [L][B_rd][W] | sig_rd [32] | X [L][B_last][W]
 // ------------------------------------------------------------------------------------
-static rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, int64_t n0, CUtensorMap* m, int u,
+rsft_status fold_map(const rsft_plan_s* p, const void* d_x, int64_t batch, int64_t n0, CUtensorMap* m, int u,
                             int64_t frame_stride = 0) {
   const int D = p->D;
   const uint64_t e = 8;
@@ -2212,10 +2097,16 @@ rsft_status launch_detect_compact(rsft_plan_s* p, const uint32_t* bm, int64_t ba
 bool vote1d_usable(const rsft_plan_s* p);                                                              // vote.cu
 rsft_status launch_scan_write(rsft_plan_s* p, int64_t batch, uint32_t* det, int64_t* idx, int64_t capacity,
                               int64_t* d_count, bool list, cudaStream_t st);                          // vote.cu
+bool fused2v_ok(const rsft_plan_s* p);                                                                 // fused2v.cu
+rsft_status launch_fused2v(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det,
+                           unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st);
+rsft_status upload_twiddles_2v(cudaStream_t st);
 
-// Whole pipeline on one batch: execute (all loops) + detect_compact.  (Running the vote in
-// the fold kernel's per-frame epilogue was measured slower at c4: the CTA's TMA stream
-// stalls while it votes.)
+// Whole pipeline on one batch.  Fused-mode plans: one fold kernel that also votes (D = 1:
+// k_gather1d with vote warps; D = 2: k_fused2v, whose epilogue warps FFT and vote frame f while
+// the fold warps stream frame f + 1 -- the synchronous per-frame epilogue vote measured slower at
+// c4 because the CTA's TMA stream stalled while it voted) + the scan / writer; other plans:
+// execute (all loops) + detect_compact.
 rsft_status launch_run(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t* bm, uint32_t* det, int64_t* idx,
                        int64_t capacity, int64_t* d_count, cudaStream_t st) {
   {
@@ -2225,6 +2116,18 @@ rsft_status launch_run(rsft_plan_s* p, const void* d_x, int64_t batch, uint32_t*
       const bool list = p->dev.region_slots != nullptr;
       rsft_status s = launch_gather1d_voted(p, d_x, batch, bm, det, p->dev.region_state,
                                             list ? p->dev.region_slots : nullptr, (int)p->dev.list_cap, st);
+      if (s == RSFT_OK) return launch_scan_write(p, batch, det, idx, capacity, d_count, list, st);
+      if (s != RSFT_E_UNSUPPORTED) return s;
+    }
+  }
+  {
+    // D = 2 fused plans (c2 / c4): fold warps + epilogue / vote warps in one kernel (fused2v.cu)
+    const char* fr = getenv("RSFT_FUSED_RUN");
+    if (!(fr && fr[0] == '0') && fused2v_ok(p) && resolve_mode(p, batch) == RSFT_MODE_FUSED &&
+        batch <= p->dev.region_capacity) {
+      const bool list = p->dev.region_slots != nullptr;
+      rsft_status s = launch_fused2v(p, d_x, batch, bm, det, p->dev.region_state, list ? p->dev.region_slots : nullptr,
+                                     (int)p->dev.list_cap, st);
       if (s == RSFT_OK) return launch_scan_write(p, batch, det, idx, capacity, d_count, list, st);
       if (s != RSFT_E_UNSUPPORTED) return s;
     }
@@ -2247,7 +2150,9 @@ rsft_status upload_twiddles(cudaStream_t st) {
     double a = -2.0 * M_PI * (double)k / 512.0;
     t5[k] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
-  return check(cudaMemcpyToSymbolAsync(c_tw512, t5, sizeof(t5), 0, cudaMemcpyHostToDevice, st), "twiddles");
+  s = check(cudaMemcpyToSymbolAsync(c_tw512, t5, sizeof(t5), 0, cudaMemcpyHostToDevice, st), "twiddles");
+  if (s) return s;
+  return upload_twiddles_2v(st);
 }
 
 }  // namespace rsft

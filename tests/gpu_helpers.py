@@ -32,12 +32,26 @@ def gpu_run(plan, x_np, spectra=True, counts=True, capacity=None):
     bm_r, det_r, idx_r, cnt_r = plan.run(x, cap)             # whole path (fused vote in fused mode)
     torch.cuda.synchronize()
     count = int(cnt.item())
-    assert int(cnt_f.item()) == count and int(cnt_r.item()) == count
+    assert int(cnt_f.item()) == count
     np.testing.assert_array_equal(det_f.cpu().numpy(), det.cpu().numpy())
-    np.testing.assert_array_equal(det_r.cpu().numpy(), det.cpu().numpy())
-    np.testing.assert_array_equal(bm_r.cpu().numpy(), bm.cpu().numpy())
     np.testing.assert_array_equal(idx_f.cpu().numpy()[:min(count, cap)], idx.cpu().numpy()[:min(count, cap)])
-    np.testing.assert_array_equal(idx_r.cpu().numpy()[:min(count, cap)], idx.cpu().numpy()[:min(count, cap)])
+    # rsft_run: fused-mode plans fold + FFT + vote in one kernel whose FFT order differs from
+    # rsft_execute's (equal to fp32 rounding).  Its bits must equal execute's except inside the
+    # 1e-3 near-threshold band; with equal bits, every output must be identical.
+    bm_np, bmr_np = bm.cpu().numpy(), bm_r.cpu().numpy()
+    if not np.array_equal(bmr_np, bm_np):
+        assert sp is not None, "rsft_run bitmaps differ from rsft_execute's (no spectra to check the band)"
+        _, gam = plan.thresholds()
+        diff = B.bitmap_to_bool((bmr_np ^ bm_np).reshape(-1), bm_np.size * 32).reshape(batch, plan.loops, -1)
+        diff = diff[:, :, :plan.btot]
+        f_, l_, k_ = np.nonzero(diff)
+        pw = np.abs(sp.cpu().numpy()[f_, l_, k_].astype(np.complex128)) ** 2
+        rel = np.abs(pw / gam[l_] - 1.0)
+        assert (rel < 1e-3).all(), ("rsft_run bits outside the near-threshold band", rel.max())
+    else:
+        assert int(cnt_r.item()) == count
+        np.testing.assert_array_equal(det_r.cpu().numpy(), det.cpu().numpy())
+        np.testing.assert_array_equal(idx_r.cpu().numpy()[:min(count, cap)], idx.cpu().numpy()[:min(count, cap)])
     return {
         "bm": bm.cpu().numpy(),
         "spectra": sp.cpu().numpy() if sp is not None else None,
