@@ -1581,14 +1581,18 @@ __global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2*
     const int r0 = (lp.sig[0] * lane + lp.tau[0]) & 31;             // b0 = lane
     float2 y[B1];
 #pragma unroll
-    for (int q = 0; q < B1; q += 2) {
-      float4 a = __ldg(reinterpret_cast<const float4*>(src + r0 * B1 + q));
-      for (int c = 1; c < nchunk; ++c) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(src + (size_t)c * bouter + r0 * B1 + q));
-        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-      }
+    for (int q = 0; q < B1; q += 2) {                  // the row's loads all in flight
+      const float4 a = __ldg(reinterpret_cast<const float4*>(src + r0 * B1 + q));
       y[q] = make_float2(a.x, a.y);
       y[q + 1] = make_float2(a.z, a.w);
+    }
+    for (int c = 1; c < nchunk; ++c) {
+#pragma unroll
+      for (int q = 0; q < B1; q += 2) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src + (size_t)c * bouter + r0 * B1 + q));
+        y[q] = cadd(y[q], make_float2(a.x, a.y));
+        y[q + 1] = cadd(y[q + 1], make_float2(a.z, a.w));
+      }
     }
     const float2* Tl = T + (size_t)lg * B1 * B1;
     const float2 t0 = sh0 ? tw[lane << 1] : make_float2(1.f, 0.f);  // e^{-j pi b0 / 32}
@@ -1625,6 +1629,87 @@ __global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2*
       if (X[k1].x * X[k1].x + X[k1].y * X[k1].y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
       if (sp) sp[k] = X[k1];
     }
+  }
+}
+
+// Split mode, kernel 2, warp-register form for B_0 = 64 outer grids (D == 3, c5: 64 x 32): a
+// 256-thread CTA per (frame, loop, k_last) line, two barriers.  Rows: warp w takes bucket rows
+// b0 = w, w + 8, ...; lane j = bucket b1 gathers residue (sigma_0 b0 + tau_0, sigma_1 b1 + tau_1)
+// (mod B) of the summed folded spectra (I3), applies both half-bucket twiddles (L1) and the warp
+// runs the B1-point dim-1 DIF across its lanes (xor shuffles; 8 rows in flight per warp).
+// Columns: warp w takes columns k1 = w, w + 8, ...; lane j holds rows j and j + 32, the first
+// radix-2 stage of the 64-point dim-0 DIF runs in-lane and the two 32-point halves across the
+// lanes: lane p then holds k0 = 2 brev5(p) (+1).  |.|^2 > gamma_l -> atomicOr into the bitmap
+// words (zeroed by the fold kernel).  Alg. 1 l.9-10; Eq. tpd.
+template <int B1>
+__global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2* __restrict__ F, int rl0, int rnl,
+                                                        int nchunk, int l0, int nl, int64_t batch,
+                                                        uint32_t* __restrict__ bitmaps, float2* __restrict__ spectra,
+                                                        int seg_L) {
+  pdl_enter();
+  constexpr int LB1 = B1 == 32 ? 5 : B1 == 16 ? 4 : 3;
+  __shared__ float2 tw[128];
+  __shared__ float2 V[64][B1 + 1];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int blast = pd.blast, bouter = pd.bouter;
+  const bool sh0 = pd.shift[0] != 0, sh1 = pd.shift[1] != 0;
+  float2 stw[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int h = 16 >> q;
+    stw[q] = tw[((lane & (h - 1)) * 64) / h];          // W_{2h}^{lane mod h}
+  }
+  const float2 w64 = tw[2 * lane];                      // W_64^j (first dim-0 stage)
+  const int b1 = lane & (B1 - 1);                       // lanes >= B1 duplicate
+  const float2 t1 = sh1 ? tw[b1 * (64 / B1)] : make_float2(1.f, 0.f);   // e^{-j pi b1 / B1}
+  const int k1_of_lane = brev(b1, LB1);
+  const int64_t lines = batch * nl * blast;
+  for (int64_t li = blockIdx.x; li < lines; li += gridDim.x) {
+    const int64_t frame = li / (nl * blast);
+    const int rem = (int)(li - frame * nl * blast), l = rem / blast, kl = rem - l * blast;
+    const int lg = seg_L > 0 ? (int)(frame % seg_L) : l;
+    const LoopDev lp = pd.loops[l0 + lg];
+    const float2* src = F + ((((size_t)frame * rnl + (l0 + l - rl0)) * blast + kl) * nchunk) * bouter;
+    const int r1 = (lp.sig[1] * b1 + lp.tau[1]) & (B1 - 1);
+    float2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {                      // rows b0 = warp + 8 q: all gathers in flight
+      const int b0 = warp + 8 * q;
+      v[q] = __ldg(src + ((lp.sig[0] * b0 + lp.tau[0]) & 63) * B1 + r1);
+    }
+    for (int c = 1; c < nchunk; ++c) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b0 = warp + 8 * q;
+        v[q] = cadd(v[q], __ldg(src + (size_t)c * bouter + ((lp.sig[0] * b0 + lp.tau[0]) & 63) * B1 + r1));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int b0 = warp + 8 * q;
+      float2 x = cmul(v[q], t1);
+      if (sh0) x = cmul(x, tw[b0]);                    // e^{-j pi b0 / 64}
+      x = warp_dif(x, lane, LB1, stw);
+      if (lane < B1) V[b0][k1_of_lane] = x;
+    }
+    __syncthreads();
+    const float gamma = lp.gamma;
+    uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
+    float2* sp = spectra ? spectra + ((size_t)frame * nl + l) * pd.btot : nullptr;
+    const int k0e = 2 * brev(lane, 5);
+#pragma unroll
+    for (int k1 = warp; k1 < B1; k1 += 8) {
+      const float2 a = V[lane][k1], b = V[lane + 32][k1];
+      const float2 u = warp_dif(cadd(a, b), lane, 5, stw);
+      const float2 t = warp_dif(cmul(csub(a, b), w64), lane, 5, stw);
+      const int64_t ke = (int64_t)(k0e * B1 + k1) * blast + kl, ko = ke + (int64_t)B1 * blast;
+      if (u.x * u.x + u.y * u.y > gamma) atomicOr(bm + (ke >> 5), 1u << (ke & 31));
+      if (t.x * t.x + t.y * t.y > gamma) atomicOr(bm + (ko >> 5), 1u << (ko & 31));
+      if (sp) { sp[ke] = u; sp[ko] = t; }
+    }
+    __syncthreads();                                     // V reused by the next line
   }
 }
 
@@ -1936,6 +2021,20 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
         return check(le_, "k_split_fft_w32 launch");
       p->last_launches += 1;
       return check(cudaGetLastError(), "k_split_fft_w32 launch");
+    }
+  }
+  {
+    // two-warp form for 64 x B1 outer grids (c5); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
+    const char* ew = getenv("RSFT_FFT_WARP");
+    if (D == 3 && p->b[0] == 64 && (b1 == 8 || b1 == 16 || b1 == 32) && !(ew && ew[0] == '0')) {
+      auto kw = b1 == 8 ? k_split_fft_w64<8> : b1 == 16 ? k_split_fft_w64<16> : k_split_fft_w64<32>;
+      const int64_t lines = batch * nl * blast;
+      const int64_t grid = std::min<int64_t>(lines, 8 * (int64_t)p->num_sms);
+      if (cudaError_t le_ = pdl_launch(kw, (unsigned)grid, 256, 0, st, p->dev, F, rl0, rnl, nchunk, l0, nl, batch, bm,
+                                       reinterpret_cast<float2*>(spectra), seg_L); le_ != cudaSuccess)
+        return check(le_, "k_split_fft_w64 launch");
+      p->last_launches += 1;
+      return check(cudaGetLastError(), "k_split_fft_w64 launch");
     }
   }
   size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;

@@ -74,6 +74,10 @@ CASES = [
     # warp-form outer FFT (B_0 = 32, B_1 in {8, 16})
     ("3d_w32_b16", (64, 32, 32), (32, 16, 8), 6, dict(p_fa=1e-3, random_tau=True), 2, "split"),
     ("3d_w32_b8_mu", (128, 64, 32), (32, 8, 4), 5, dict(p_fa=1e-2, mu=3), 2, "split"),
+    # two-warp outer FFT (B_0 = 64, B_1 in {8, 16, 32}; c5's outer grid is 64 x 32)
+    ("3d_w64_b32", (128, 64, 32), (64, 32, 8), 6, dict(p_fa=1e-3, random_tau=True), 2, "split"),
+    ("3d_w64_b16_mma", (64, 256, 64), (64, 16, 8), 8, dict(p_fa=1e-3), 1, "split"),
+    ("3d_w64_b8_mu", (64, 32, 64), (64, 8, 8), 5, dict(p_fa=1e-2, mu=3, random_tau=True), 2, "split"),
     # more than 32 loops (up to 63, the paper's T = 50 design point P:640): several fold passes
     ("2d_L40", (128, 64), (16, 8), 40, dict(p_fa=1e-2, mu=30, random_tau=True), 2, "fused"),
     ("1d_L50_w256", (1024,), (32,), 50, dict(support=(256,), p_fa=1e-2, mu=40), 2, "fused"),
@@ -160,6 +164,62 @@ def test_parity_3d_region_vote_forced(case, monkeypatch):
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
+def _votes_all_kernels(plan, bm, cap, monkeypatch, envs):
+    import torch
+    outs = []
+    for env in envs:
+        for k in ("RSFT_VOTE3D", "RSFT_NO_VOTE3D"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        det = plan.detect(bm)
+        det_c, idx, cnt = plan.detect_compact(bm, cap)
+        torch.cuda.synchronize()
+        c = int(cnt.item())
+        outs.append((det.cpu().numpy(), det_c.cpu().numpy(), idx.cpu().numpy()[:min(c, cap)], c))
+    return outs
+
+
+V3_ENVS = [{}, {"RSFT_NO_VOTE3D": "1"}]
+
+
+@pytest.mark.parametrize("case", V3_CASES[:8], ids=[c[0] for c in V3_CASES[:8]])
+def test_3d_votes_bit_identical(case, monkeypatch):
+    """The 3-D votes (k_vote3d, warp per plane on the k_etab expansions; k_vote, CTA per region)
+    are integer work on the same bitmaps: their detection words, counts and index lists must be
+    bit-identical."""
+    import torch
+    name, n, b, loops, kw, batch, mode = case
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
+    x = torch.from_numpy(frames(wl, batch)).cuda()
+    plan = make_plan(op, max_batch=batch, mode=mode).bind()
+    bm = plan.execute(x)
+    outs = _votes_all_kernels(plan, bm, batch * plan.ntot, monkeypatch, V3_ENVS)
+    for o in outs[1:]:
+        for a_, b_ in zip(outs[0], o):
+            np.testing.assert_array_equal(np.asarray(a_), np.asarray(b_))
+
+
+@pytest.mark.parametrize("name", ["c3_3d", "c5_cube"])
+def test_3d_votes_bit_identical_full_size(name, monkeypatch):
+    """c3 (batched) and the c5 cube at full size: the 3-D votes bit-identical (the c5 planes of
+    1024 words exceed k_vote3d's default limit; RSFT_VOTE3D=1 forces it there)."""
+    import torch
+    wl = synth.WORKLOADS[name]
+    batch = 8 if name == "c3_3d" else 1
+    x = torch.from_numpy(frames(wl.with_(batch=batch), batch)).cuda()
+    op = wl_params(wl)
+    plan = make_plan(op, max_batch=batch).bind()
+    bm = plan.execute(x)
+    envs = [{}, {"RSFT_VOTE3D": "1"}, {"RSFT_NO_VOTE3D": "1"}]
+    outs = _votes_all_kernels(plan, bm, 1 << 22, monkeypatch, envs)
+    assert outs[0][3] > 0
+    for o in outs[1:]:
+        for a_, b_ in zip(outs[0], o):
+            np.testing.assert_array_equal(np.asarray(a_), np.asarray(b_))
+
+
 V2_CASES = [c for c in CASES if c[0].startswith("2d_") and c[6] == "fused"]
 
 
@@ -177,7 +237,7 @@ def test_parity_2d_frame_vote_forced(case, force, monkeypatch):
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
-W32_CASES = [c for c in CASES if c[0].startswith("3d_w32")]
+W32_CASES = [c for c in CASES if c[0].startswith(("3d_w32", "3d_w64"))]
 
 
 @pytest.mark.parametrize("case", W32_CASES, ids=[c[0] for c in W32_CASES])
