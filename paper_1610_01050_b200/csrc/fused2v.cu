@@ -38,8 +38,9 @@ namespace rsft {
 __constant__ float2 c_tw2v[128];   // e^{-j 2 pi k / 128} (fp64-rounded at bind)
 
 constexpr int kF2vFold = 8;        // fold warps: 4 of the 32 residue classes of c4 each
-// epilogue (FFT + threshold + vote) warps NE: 8 by default, 4 selectable (launch_fused2v)
+constexpr int kF2vEpi = 8;         // epilogue (FFT + threshold + vote) warps: one per loop (L <= 8)
 constexpr int kF2vU = 8;           // rows per TMA box (4 KiB)
+constexpr int kF2vFB = 2;          // residue-sum slots F (one slot + 5 ring stages measured slower)
 constexpr int kF2vMaxRows = 8;     // vote rows per epilogue thread at NE = 4 (32 / NE: N0 <= 1024)
 
 template <int NE>
@@ -59,7 +60,7 @@ RSFT_HD inline F2vLayout f2v_layout(int S, int L, int LP, int N0, int B0, int B1
   o.bars = off; off += (kF2vFold * S + 4) * 8;
   off = f2v_align(off, 16);
   o.fslot = L * B0 * (B1 + 1);                       // float2 per buffer
-  o.F = off; off += 2 * f2v_align(o.fslot, 2) * 8;
+  o.F = off; off += kF2vFB * f2v_align(o.fslot, 2) * 8;
   o.tw = off; off += 128 * 8;
   // row weights class-major [B0][A0 rounded up to U][LP] (zero rows pad the last group): the U
   // rows of a box are contiguous, so the fold addresses them with immediate offsets
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
   const F2vLayout lay = f2v_layout(S, L, LP, N0, B0, NB1, W, wpl);
   float4* ring = reinterpret_cast<float4*>(smem + lay.ring);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bars);
-  uint64_t* Ffull = bars + NF * S;                   // [2], NF x 32 arrivals per frame
-  uint64_t* Fempty = Ffull + 2;                      // [2], NE x 32 arrivals per frame
+  uint64_t* Ffull = bars + NF * S;                   // [FB], NF x 32 arrivals per frame
+  uint64_t* Fempty = Ffull + 2;                      // [FB], NE x 32 arrivals per frame
   float2* Fbuf = reinterpret_cast<float2*>(smem + lay.F);
   const int fslot = f2v_align(lay.fslot, 2);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
@@ -114,8 +115,7 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
   for (int i = tid; i < L * NB1 * W; i += blockDim.x) Xs[i] = __ldg(pd.xmask + i);
   if (tid == 0) {
     for (int i = 0; i < NF * S; ++i) mbar_init(&bars[i], 1);
-    mbar_init(&Ffull[0], NF * 32); mbar_init(&Ffull[1], NF * 32);
-    mbar_init(&Fempty[0], NE * 32); mbar_init(&Fempty[1], NE * 32);
+    for (int i = 0; i < kF2vFB; ++i) { mbar_init(&Ffull[i], NF * 32); mbar_init(&Fempty[i], NE * 32); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
     const int fold_lanes = NB1 / 2;
     float2 racc[LP][2];
     for (int64_t fi = 0; fi < nfr; ++fi) {
-      const int fb = (int)(fi & 1);
+      const int fb = (int)(fi % kF2vFB);
+      const uint32_t use = (uint32_t)(fi / kF2vFB);   // this slot's use count
       float2* F = Fbuf + (size_t)fb * fslot;
       bool waited = false;
       for (int unit = 0; unit < units; ++unit) {
@@ -186,8 +187,8 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
         }
         if (seg == spt - 1) {
           lane_fold<LP>(racc, NB1);
-          if (!waited) {                             // slot fb free: the epilogue of frame fi - 2 is done
-            mbar_wait(&Fempty[fb], (uint32_t)(((fi >> 1) & 1) ^ 1));
+          if (!waited) {                             // slot fb free: the epilogue gathered frame fi - FB
+            mbar_wait(&Fempty[fb], (use & 1u) ^ 1u);
             waited = true;
           }
           if (lane < fold_lanes) {
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
           }
         }
       }
-      if (!waited) mbar_wait(&Fempty[fb], (uint32_t)(((fi >> 1) & 1) ^ 1));   // keeps the Ffull phases in step
+      if (!waited) mbar_wait(&Fempty[fb], (use & 1u) ^ 1u);   // keeps the Ffull phases in step
       __syncwarp();
       mbar_arrive(&Ffull[fb]);
     }
@@ -231,18 +232,24 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
 
   for (int64_t fi = 0; fi < nfr; ++fi) {
     const int64_t frame = blockIdx.x + fi * gridDim.x;
-    const int fb = (int)(fi & 1);
+    const int fb = (int)(fi % kF2vFB);
     const float2* F = Fbuf + (size_t)fb * fslot;
-    mbar_wait(&Ffull[fb], (uint32_t)((fi >> 1) & 1));
-    for (int l = ew; l < L; l += NE) {
-      const LoopDev lp = pd.loops[l];
+    mbar_wait(&Ffull[fb], (uint32_t)((fi / kF2vFB) & 1));
+    // one loop per epilogue warp (L <= 8 = NE): gather its bucket rows, then free the slot
+    const int l = ew;
+    const LoopDev lp = pd.loops[l < L ? l : 0];
+    float2 v[NB1];
+    if (l < L) {
       const int r0 = (lp.sig[0] * b0 + lp.tau[0]) & (B0 - 1);
       const float2* Fr = F + ((size_t)l * B0 + r0) * fstride;
-      float2 v[NB1];
 #pragma unroll
-      for (int b1 = 0; b1 < NB1; ++b1) {             // residue -> bucket (I3) + half-bucket twiddles (L1)
-        const int r1 = (lp.sig[1] * b1 + lp.tau[1]) & (NB1 - 1);
-        float2 x = Fr[r1];
+      for (int b1 = 0; b1 < NB1; ++b1) v[b1] = Fr[(lp.sig[1] * b1 + lp.tau[1]) & (NB1 - 1)];   // residue -> bucket (I3)
+    }
+    mbar_arrive(&Fempty[fb]);                        // F[fb] consumed (values in registers)
+    if (l < L) {
+#pragma unroll
+      for (int b1 = 0; b1 < NB1; ++b1) {             // half-bucket twiddles (L1)
+        float2 x = v[b1];
         if (shift1) x = cmul(x, c_tw2v[b1 * (64 / NB1)]);
         v[b1] = cmul(x, h0tw);
       }
@@ -276,7 +283,6 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
         bitmaps[(size_t)frame * L * wpl + (size_t)l * wpl + lane] = word;
       }
     }
-    mbar_arrive(&Fempty[fb]);                        // F[fb] consumed
     epi_sync<NE>();
     // E[l][k0][w] = OR of the last-dim masks X[l][k1] of the set buckets (k0, k1) of loop l (I1)
     const int lgW = __ffs(W) - 1;
@@ -460,14 +466,11 @@ rsft_status launch_fused2v(rsft_plan_s* p, const void* d_x, int64_t batch, uint3
                            unsigned long long* rcount, uint32_t* slots, int list_cap, cudaStream_t st) {
   const int lp = p->L <= 6 ? 6 : 8;
   const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
-  // 8 epilogue warps (c4: 1.404 vs 1.420 ms per step with 4; c2: 0.757 vs 1.054 ms, where 4 warps
-  // take longer per frame than the fold); RSFT_F2V_EPI=4 (read per launch) selects 4
-  const char* ee = getenv("RSFT_F2V_EPI");
-  const int ne = ee && ee[0] == '4' ? 4 : 8;
+  // 8 epilogue warps, one loop each (4 measured slower: c4 1.420 vs 1.404 ms per step; c2 1.054 vs
+  // 0.757 ms, where 4 warps took longer per frame than the fold)
 #define RSFT_F2V(LPV, B1V, MV) \
   if (lp == LPV && p->b[1] == B1V && mode == MV) \
-    return ne == 8 ? launch_f2v_t<LPV, B1V, MV, 8>(p, d_x, batch, bm, det, rcount, slots, list_cap, st) \
-                   : launch_f2v_t<LPV, B1V, MV, 4>(p, d_x, batch, bm, det, rcount, slots, list_cap, st);
+    return launch_f2v_t<LPV, B1V, MV, kF2vEpi>(p, d_x, batch, bm, det, rcount, slots, list_cap, st);
 #define RSFT_F2V_M(LPV, B1V) RSFT_F2V(LPV, B1V, 0) RSFT_F2V(LPV, B1V, 1) RSFT_F2V(LPV, B1V, 2)
   RSFT_F2V_M(6, 8) RSFT_F2V_M(6, 16) RSFT_F2V_M(6, 32)
   RSFT_F2V_M(8, 8) RSFT_F2V_M(8, 16) RSFT_F2V_M(8, 32)

@@ -402,14 +402,11 @@ def test_parity_c2_shape_fused_batch(batch):
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
 
-@pytest.mark.parametrize("epi", ["4", "8"])
-def test_fused2v_epilogue_widths_many_frames(epi, monkeypatch):
-    """rsft_run's D = 2 warp-specialised kernel (k_fused2v) with 4 and 8 epilogue warps (env
-    RSFT_F2V_EPI, read per launch) on c2's shape with more frames than CTAs: every CTA cycles
-    its double-buffered residue slot many times (Ffull / Fempty phases).  gpu_run compares its
-    bitmaps, detections and index list with rsft_execute + rsft_detect_compact; sampled frames
-    (CTA boundaries 147/148, the last frame) against the oracle."""
-    monkeypatch.setenv("RSFT_F2V_EPI", epi)
+def test_fused2v_many_frames():
+    """rsft_run's D = 2 warp-specialised kernel (k_fused2v) on c2's shape with more frames than
+    CTAs: every CTA cycles its residue-sum slot(s) many times (Ffull / Fempty phases).  gpu_run
+    compares its bitmaps, detections and index list with rsft_execute + rsft_detect_compact;
+    sampled frames (CTA boundaries 147/148, the last frame) against the oracle."""
     wl = synth.C2.with_(batch=400)
     x = frames(wl, 400)
     plan, _, reps = run_case(wl_params(wl), x, mode="fused", check=[0, 1, 147, 148, 149, 296, 399])
