@@ -245,42 +245,71 @@ __device__ __forceinline__ int bart_pos(int r, int lane) {
   return bart_brev_c(r, bart_lg(M)) + M * (int)(__brev((unsigned)lane) >> 27);
 }
 
-// Pass 1, D == 2: one warp per (frame, segment, row): window on load, row FFT (n1 = 32 M),
-// natural order through the warp's shared line buffer, coalesced store to the scratch.
+// RW = 32 / M lines of n = 32 M points per warp, no cross-lane shuffle stages (the four-step FFT
+// through a transpose): lane l holds a[j M + k] = x_j[l + 32 k] (k < M) on entry.  In-lane M-point
+// DIF over k, twiddles W_n^{l q1} (q1 = brev_M(r); w1 = W_n^l), a transpose through the warp's
+// [32][33] scratch xs so that lane L = j M + q1 holds a[l] = Y_j[l][q1] for l < 32, and an in-lane
+// 32-point DIF over l.  On return lane L = j M + q1 holds a[r2] = X_j[q1 + M brev5(r2)].
+// (X[q1 + M q2] = sum_l W_n^{l q1} W_32^{l q2} sum_k x[l + 32 k] W_M^{k q1}.)
+template <int M>
+__device__ __forceinline__ void bart_warp_fft_t(float2 (&a)[32], int lane, float2 w1, float2* __restrict__ xs) {
+  constexpr int RW = 32 / M, LM = bart_lg(M);
+#pragma unroll
+  for (int j = 0; j < RW; ++j) {
+    float2 (&v)[M] = *reinterpret_cast<float2 (*)[M]>(&a[j * M]);
+    bart_lane_dif<M>(v, 5 + LM);
+    float2 cur = w1;
+#pragma unroll
+    for (int q1 = 1; q1 < M; ++q1) {
+      const int r = bart_brev_c(q1, LM);
+      v[r] = bart_cmul(v[r], cur);
+      cur = bart_cmul(cur, w1);
+    }
+#pragma unroll
+    for (int r = 0; r < M; ++r) xs[(j * M + bart_brev_c(r, LM)) * 33 + lane] = v[r];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; ++l) a[l] = xs[lane * 33 + l];
+  __syncwarp();
+  bart_lane_dif<32>(a, 10);
+}
+
+// Pass 1, D == 2: a warp takes RW = 32 / M rows (frame, segment, row) at a time: window on load,
+// row FFTs (n1 = 32 M) through the transpose form (bart_warp_fft_t), stores to the scratch in
+// natural order (lane (j, q1) writes elements q1 + M q2: M-element runs per row).
 template <int M>
 __global__ void __launch_bounds__(256) k_bart_rows(PlanDev pd, const float2* __restrict__ x, int64_t nrows, int n0,
                                                    int lgn1, const float* __restrict__ w0, const float* __restrict__ w1,
                                                    float2* __restrict__ scratch) {
   extern __shared__ __align__(16) float2 br[];
-  float2* t = br;                                      // [2048]
-  float2 (*line)[32 * M] = reinterpret_cast<float2 (*)[32 * M]>(br + 2048);   // [8][n1]
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
-  __syncthreads();
+  constexpr int RW = 32 / M, n1 = 32 * M;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float2 stw[5];
-  bart_stw(stw, lane, t);
-  constexpr int n1 = 32 * M;
+  float2* xs = br + warp * (32 * 33);
+  const float2 tw1 = bart_twn(pd.btw, lane, lgn1);     // W_n1^lane
   float wc[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) wc[k] = w1[lane + 32 * k];
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < nrows; row += (int64_t)gridDim.x * 8) {
-    const float2* src = x + (size_t)row * n1;
-    const float wr = w0[(int)(row % n0)];
-    float2 v[M];
+  const int L = lane / M, q1 = lane % M;               // output line / column phase of this lane
+  const int64_t groups = nrows / RW;                   // nrows = batch T n0, n0 % RW == 0
+  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g < groups; g += (int64_t)gridDim.x * 8) {
+    const int64_t row0 = g * RW;
+    const float2* src = x + (size_t)row0 * n1;
+    float2 a[32];
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      const float2 a = src[lane + 32 * k];
-      const float w = wr * wc[k];
-      v[k] = make_float2(a.x * w, a.y * w);
+    for (int j = 0; j < RW; ++j) {
+      const float wr = w0[(int)((row0 + j) % n0)];
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const float2 v = src[(size_t)j * n1 + lane + 32 * k];
+        const float w = wr * wc[k];
+        a[j * M + k] = make_float2(v.x * w, v.y * w);
+      }
     }
-    bart_warp_fft<M>(v, lane, lgn1, t, stw);
+    bart_warp_fft_t<M>(a, lane, tw1, xs);
+    float2* dst = scratch + (size_t)(row0 + L) * n1 + q1;
 #pragma unroll
-    for (int r = 0; r < M; ++r) line[warp][bart_pos<M>(r, lane)] = v[r];
-    __syncwarp();
-    float2* dst = scratch + (size_t)row * n1;
-#pragma unroll
-    for (int k = 0; k < M; ++k) dst[lane + 32 * k] = line[warp][lane + 32 * k];
-    __syncwarp();
+    for (int r2 = 0; r2 < 32; ++r2) dst[M * bart_brev_c(r2, 5)] = a[r2];
   }
 }
 
@@ -340,68 +369,76 @@ __global__ void __launch_bounds__(256) k_bart_planes(PlanDev pd, const float2* _
   }
 }
 
-// Pass 2 (D >= 2): one CTA per (frame, tile of 8 adjacent inner columns); per segment the
-// [n0][8] tile is staged in shared memory (padded rows), warp w transforms column w along dim 0
-// and accumulates |.|^2 in registers over the T segments; power (natural order) and the
-// detection bits are written once.
-template <int M0>
-__global__ void __launch_bounds__(256) k_bart_cols(PlanDev pd, const float2* __restrict__ scratch, int64_t batch, int T,
-                                                   int64_t inner, int lgn0, float* __restrict__ power, float scale,
-                                                   float gamma, uint32_t* __restrict__ det) {
+// Pass 2 (D >= 2): one CTA of CW warps per (frame, tile of C = CW RW adjacent inner columns), RW =
+// 32 / M0 columns per warp; per segment the [n0][C] tile is staged in shared memory (padded rows),
+// the NEXT segment's tile loads are issued before this one's FFTs (registers), each warp transforms
+// its RW columns along dim 0 (bart_warp_fft_t) and accumulates |.|^2 in registers over the T
+// segments; power (natural order) and the detection bits are written once.
+// CW warps per CTA: 8 for 1024-point columns (c4: one CTA per SM, 3.14 vs 3.68 ms per step with
+// 4), 4 below (two CTAs per SM; c2: 0.94 vs 1.02 ms with 8).
+template <int M0> struct BartColCfg { static constexpr int CW = M0 == 32 ? 8 : 4; };
+template <int M0, int CW = BartColCfg<M0>::CW>
+__global__ void __launch_bounds__(32 * CW, 8 / CW) k_bart_cols(PlanDev pd, const float2* __restrict__ scratch,
+                                                                     int64_t batch, int T, int64_t inner, int lgn0,
+                                                                     float* __restrict__ power, float scale,
+                                                                     float gamma, uint32_t* __restrict__ det) {
   extern __shared__ __align__(16) float2 bc[];
-  float2* t = bc;                                      // [2048]
-  float2* tile = t + 2048;                             // [n0][9]
-  constexpr int n0 = 32 * M0, C = 8, st = C + 1;
-  float2* xs = tile + n0 * st + (threadIdx.x >> 5) * (32 * 33);   // M0 == 32: transpose scratch
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) t[i] = pd.btw[i];
-  __syncthreads();
+  constexpr int n0 = 32 * M0, RW = 32 / M0, C = RW * CW, st = C + 1;
+  constexpr int NT = 32 * CW;
+  constexpr int NQ = n0 * C / 2 / NT;                   // 16-B chunks per thread per segment
+  float2* tile = bc;                                   // [n0][C + 1]
+  float2* xs = tile + n0 * st + (threadIdx.x >> 5) * (32 * 33);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float2 stw[5];
-  bart_stw(stw, lane, t);
+  const float2 tw1 = bart_twn(pd.btw, lane, lgn0);     // W_n0^lane
   const int64_t ctiles = inner / C, ntot = (int64_t)n0 * inner, words = (ntot + 31) >> 5;
   float* ptile = reinterpret_cast<float*>(tile);       // reused for the power transpose: [n0][C]
+  const int L = lane / M0, q1 = lane % M0;             // output column (of the warp's RW) / phase
   for (int64_t u = blockIdx.x; u < batch * ctiles; u += gridDim.x) {
     const int64_t frame = u / ctiles;
     const int64_t c0 = (u - frame * ctiles) * C;
-    float acc[M0];
+    float acc[32];
 #pragma unroll
-    for (int r = 0; r < M0; ++r) acc[r] = 0.f;
+    for (int r = 0; r < 32; ++r) acc[r] = 0.f;
+    const float2* base = scratch + (size_t)frame * T * ntot + c0;
+    float4 q[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {                      // segment 0's tile
+      const int qi = threadIdx.x + NT * j, r = qi / (C / 2), c2 = (qi % (C / 2)) * 2;
+      q[j] = __ldcs(reinterpret_cast<const float4*>(base + (size_t)r * inner + c2));
+    }
     for (int s = 0; s < T; ++s) {
-      __syncthreads();
-      const float2* src = scratch + ((size_t)frame * T + s) * ntot + c0;
-      // 16-B loads (two adjacent columns of one row), all of a thread's loads in flight at once
-      constexpr int NQ = n0 * C / 2 / 256;             // 16-B chunks per thread (blockDim 256)
-      float4 q[NQ > 0 ? NQ : 1];
+      __syncthreads();                                 // previous tile's readers done
 #pragma unroll
       for (int j = 0; j < NQ; ++j) {
-        const int qi = threadIdx.x + 256 * j, r = qi >> 2, c2 = (qi & 3) * 2;
-        q[j] = __ldcs(reinterpret_cast<const float4*>(src + (size_t)r * inner + c2));
-      }
-#pragma unroll
-      for (int j = 0; j < NQ; ++j) {
-        const int qi = threadIdx.x + 256 * j, r = qi >> 2, c2 = (qi & 3) * 2;
+        const int qi = threadIdx.x + NT * j, r = qi / (C / 2), c2 = (qi % (C / 2)) * 2;
         tile[r * st + c2] = make_float2(q[j].x, q[j].y);
         tile[r * st + c2 + 1] = make_float2(q[j].z, q[j].w);
       }
-      if (NQ == 0)
-        for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) tile[(e >> 3) * st + (e & 7)] = src[(size_t)(e >> 3) * inner + (e & 7)];
       __syncthreads();
-      float2 v[M0];
+      if (s + 1 < T) {                                 // next segment's loads in flight during the FFTs
+        const float2* src = base + (size_t)(s + 1) * ntot;
 #pragma unroll
-      for (int k = 0; k < M0; ++k) v[k] = tile[(lane + 32 * k) * st + warp];
-      if constexpr (M0 == 32) bart_warp_fft1024(reinterpret_cast<float2 (&)[32]>(v), lane, t, xs);
-      else bart_warp_fft<M0>(v, lane, lgn0, t, stw);
+        for (int j = 0; j < NQ; ++j) {
+          const int qi = threadIdx.x + NT * j, r = qi / (C / 2), c2 = (qi % (C / 2)) * 2;
+          q[j] = __ldcs(reinterpret_cast<const float4*>(src + (size_t)r * inner + c2));
+        }
+      }
+      float2 a[32];
 #pragma unroll
-      for (int r = 0; r < M0; ++r) acc[r] += v[r].x * v[r].x + v[r].y * v[r].y;
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < M0; ++k) a[j * M0 + k] = tile[(lane + 32 * k) * st + warp * RW + j];
+      bart_warp_fft_t<M0>(a, lane, tw1, xs);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) acc[r] += a[r].x * a[r].x + a[r].y * a[r].y;
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < M0; ++r)
-      ptile[(M0 == 32 ? lane + 32 * bart_brev_c(r, 5) : bart_pos<M0>(r, lane)) * C + warp] = acc[r];
+    for (int r2 = 0; r2 < 32; ++r2) ptile[(q1 + M0 * bart_brev_c(r2, 5)) * C + warp * RW + L] = acc[r2];
     __syncthreads();
     float* pdst = power + (size_t)frame * ntot + c0;
     for (int e = threadIdx.x; e < n0 * C; e += blockDim.x) {
-      const int r = e >> 3, c = e & 7;
+      const int r = e / C, c = e % C;
       const float p = ptile[e];
       pdst[(size_t)r * inner + c] = p;
       if (det && p * scale > gamma) {
@@ -560,10 +597,11 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
           m == 1 ? k_bart_rows<1> : m == 2 ? k_bart_rows<2> : m == 4 ? k_bart_rows<4> : m == 8 ? k_bart_rows<8>
         : m == 16 ? k_bart_rows<16> : m == 32 ? k_bart_rows<32> : nullptr;
       if (!k1) return RSFT_E_UNSUPPORTED;
-      const size_t smem = (2048 + 8 * (size_t)nn[1]) * 8;
+      if (nn[0] % (32 / m)) return RSFT_E_UNSUPPORTED;   // whole row groups per warp
+      const size_t smem = (size_t)8 * 32 * 33 * 8;     // per-warp transpose scratch
       if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return RSFT_E_CUDA;
-      const int64_t grid = std::min<int64_t>((nlines + 7) / 8, 8 * (int64_t)p->num_sms);
+      const int64_t grid = std::min<int64_t>((nlines / (32 / m) + 7) / 8, 6 * (int64_t)p->num_sms);
       k1<<<(unsigned)grid, 256, smem, st>>>(p->dev, xin, nlines, nn[0], g.lg1, wr[0], wr[1], scr);
     } else {
       const int m2 = mof(nn[2]), m1 = mof(nn[1]);
@@ -586,15 +624,17 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
     void (*k2)(PlanDev, const float2*, int64_t, int, int64_t, int, float*, float, float, uint32_t*) =
         m0 == 1 ? k_bart_cols<1> : m0 == 2 ? k_bart_cols<2> : m0 == 4 ? k_bart_cols<4> : m0 == 8 ? k_bart_cols<8>
       : m0 == 16 ? k_bart_cols<16> : m0 == 32 ? k_bart_cols<32> : nullptr;
-    if (!k2 || inner % 8) return RSFT_E_UNSUPPORTED;
-    const size_t smem2 = (2048 + (size_t)nn[0] * 9 + (m0 == 32 ? 8 * 32 * 33 : 0)) * 8;
+    const int cw = m0 == 32 ? BartColCfg<32>::CW : BartColCfg<1>::CW;
+    const int64_t ccols = (int64_t)cw * (32 / std::max(m0, 1));   // columns per CTA
+    if (!k2 || inner % ccols) return RSFT_E_UNSUPPORTED;
+    const size_t smem2 = ((size_t)nn[0] * (ccols + 1) + (size_t)cw * 32 * 33) * 8;
     if (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess)
       return RSFT_E_CUDA;
     int nb = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2, 256, smem2);
-    const int64_t units2 = batch * (inner / 8);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2, 32 * cw, smem2);
+    const int64_t units2 = batch * (inner / ccols);
     const int64_t grid2 = std::min<int64_t>(units2, (int64_t)std::max(nb, 1) * p->num_sms);
-    k2<<<(unsigned)grid2, 256, smem2, st>>>(p->dev, scr, batch, segments, inner, g.lg0, d_power, scale, gam, d_detect);
+    k2<<<(unsigned)grid2, 32 * cw, smem2, st>>>(p->dev, scr, batch, segments, inner, g.lg0, d_power, scale, gam, d_detect);
     p->last_launches = 2;
   }
   const cudaError_t e = cudaGetLastError();

@@ -63,7 +63,10 @@ def test_roc_monotone():
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,batch", [((1024,), 3), ((256, 128), 2), ((64, 32, 32), 2), ((4096,), 3), ((128, 64), 3),
                                      ((2048,), 2), ((512,), 2),
-                                     ((1024, 256), 2), ((512, 128, 32), 1)])
+                                     ((1024, 256), 2), ((512, 128, 32), 1),
+                                     # two-pass 2-D shapes for every transpose-FFT width: rows of 32 M
+                                     # points (RW = 32 / M rows per warp), columns of 32 M0 points
+                                     ((256, 256), 2), ((512, 64), 2), ((1024, 32), 2), ((128, 512), 2)])
 def test_bartlett_gpu_parity(n, batch):
     """Single-pass (<= 8192 samples) and two-pass frames, several frames per call, against the
     oracle's literal Alg. 2 (numpy fftn) frame by frame."""
