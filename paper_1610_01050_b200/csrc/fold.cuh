@@ -108,15 +108,48 @@ __device__ __forceinline__ float2 shfl_xor2(float2 v, int m) {
   return make_float2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
 
-// 2^lgb-point DIF across lanes (x = element lane mod 2^lgb, lgb <= 5): lane p ends with
-// X[brev(p mod 2^lgb)].  stw[q] = W_{2h}^{lane & (h-1)} for h = 16 >> q.
-__device__ __forceinline__ float2 warp_dif(float2 x, int lane, int lgb, const float2 (&stw)[5]) {
+// Select form of warp_dif below (no per-lane constants beyond stw: for register-capped kernels).
+__device__ __forceinline__ float2 warp_dif_sel(float2 x, int lane, int lgb, const float2 (&stw)[5]) {
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
     const int h = 16 >> q;
     if ((2 * h) > (1 << lgb)) continue;           // warp-uniform
     const float2 p = shfl_xor2(x, h);
     x = (lane & h) ? cmul(csub(p, x), stw[q]) : cadd(x, p);
+  }
+  return x;
+}
+
+// 2^lgb-point DIF across lanes (x = element lane mod 2^lgb, lgb <= 5): lane p ends with
+// X[brev(p mod 2^lgb)].  Stage q (h = 16 >> q) pairs lanes p, p ^ h: the lower one keeps x + p,
+// the upper one (p - x) W_{2h}^{lane mod h}.  Written branch-free with per-lane constants (DifTw):
+// y = sg x + partner, then y w with w = 1 on the lower lane -- one FFMA2 + one FMUL2 + one FFMA2
+// per stage and value in SASS (the select form issued 4 FADD + 4 FMUL/FFMA + 4 moves).
+struct DifTw {
+  float2 cd[5], mdc[5];                              // w = (c, d) and (-d, c)
+  float sg[5];                                       // +1 lower lane, -1 upper lane
+};
+// stw[q] = W_{2h}^{lane & (h-1)} for h = 16 >> q
+__device__ __forceinline__ DifTw dif_tw(int lane, const float2 (&stw)[5]) {
+  DifTw t;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const bool up = (lane & (16 >> q)) != 0;
+    const float2 w = up ? stw[q] : make_float2(1.f, 0.f);
+    t.cd[q] = w;
+    t.mdc[q] = make_float2(-w.y, w.x);
+    t.sg[q] = up ? -1.f : 1.f;
+  }
+  return t;
+}
+__device__ __forceinline__ float2 warp_dif(float2 x, int lgb, const DifTw& t) {
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int h = 16 >> q;
+    if ((2 * h) > (1 << lgb)) continue;           // warp-uniform
+    const float2 p = shfl_xor2(x, h);
+    const float2 y = __ffma2_rn(make_float2(t.sg[q], t.sg[q]), x, p);
+    x = __ffma2_rn(make_float2(y.y, y.y), t.mdc[q], __fmul2_rn(make_float2(y.x, y.x), t.cd[q]));
   }
   return x;
 }

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
     const int h = 16 >> q;
     stw[q] = tw[(lane & (h - 1)) * (64 / h)];
   }
+  const DifTw dt = dif_tw(lane, stw);
   const float2 h0tw = pd.shift[0] ? tw[b0 * (64 >> lgb0)] : make_float2(1.f, 0.f);   // e^{-j pi b0 / B0}
   const bool shift1 = pd.shift[1] != 0;
   const int rpw = 32 / NB1;                          // bucket rows per bitmap word
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
       uint32_t mask = 0u;
 #pragma unroll
       for (int s = 0; s < NB1; ++s) {
-        const float2 x = warp_dif(v[s], lane, lgb0, stw);
+        const float2 x = warp_dif(v[s], lgb0, dt);
         if (x.x * x.x + x.y * x.y > lp.gamma) mask |= 1u << brev(s, LB1);
       }
       // bitmap words: word w holds bucket rows w rpw .. w rpw + rpw - 1 (flat k = k0 B1 + k1)

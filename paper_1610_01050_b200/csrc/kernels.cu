@@ -564,6 +564,13 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
     const int hh = 16 >> q;
     stw[q] = tw[((lane & (hh - 1)) * (TWN / 2)) / hh];
   }
+  const DifTw dt = dif_tw(lane, stw);
+  // the fused-vote build (VL > 0, 96 registers) keeps the select-form DIF: the packed form's per-lane
+  // constants spill there (c1 rsft_run 0.92 vs 0.85 ms)
+  auto dif = [&](float2 x, int lg) -> float2 {
+    if constexpr (VL > 0) return warp_dif_sel(x, lane, lg, stw);
+    else return warp_dif(x, lg, dt);
+  };
   // half-bucket twiddles e^{-j pi b / B} of the lane's buckets (L1), stage-1 twiddle (B = 64)
   const float2 sh0 = MB > 2 ? make_float2(1.f, 0.f) : shift ? tw[(lane & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
   const float2 sh1 = MB > 2 ? make_float2(1.f, 0.f) : shift ? tw[((lane + 32) & (B - 1)) << (6 - lgb)] : make_float2(1.f, 0.f);
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
         int val = 0;
 #pragma unroll
         for (int r = 0; r < MB; ++r) {
-          v[r] = warp_dif(v[r], lane, 5, stw);
+          v[r] = dif(v[r], 5);
           val |= (v[r].x * v[r].x + v[r].y * v[r].y > gamma ? 1 : 0) << r;
           if (sp) sp[brev(r, LM) + MB * brev(lane, 5)] = v[r];
         }
@@ -670,8 +677,8 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
       } else if (B == 64) {
         const float2 a = cmul(acc[q][0], sh0), c = cmul(acc[q][1], sh1);
         float2 u = cadd(a, c), v = cmul(csub(a, c), w64);   // X[2k] <- u, X[2k+1] <- v
-        u = warp_dif(u, lane, 5, stw);
-        v = warp_dif(v, lane, 5, stw);
+        u = dif(u, 5);
+        v = dif(v, 5);
         const int kb = 2 * brev(lane, 5);                   // lane p holds X[kb], X[kb + 1]
         if (sp) { sp[kb] = u; sp[kb + 1] = v; }
         const int val = (u.x * u.x + u.y * u.y > gamma ? 1 : 0) | (v.x * v.x + v.y * v.y > gamma ? 2 : 0);
@@ -687,7 +694,7 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
         for (int o = 1; o < 32; o <<= 1)
           if (o >= B) a = cadd(a, shfl_xor2(a, o));         // lanes with equal lane mod B
         a = cmul(a, sh0);
-        a = warp_dif(a, lane, lgb, stw);
+        a = dif(a, lgb);
         const int kb = brev(lane & (B - 1), lgb);
         if (sp && lane < B) sp[kb] = a;
         const int val = a.x * a.x + a.y * a.y > gamma ? 1 : 0;
@@ -1571,6 +1578,7 @@ __global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2*
     const int h = 16 >> q;
     stw[q] = tw[((lane & (h - 1)) * 64) / h];          // W_{2h}^{lane mod h}
   }
+  const DifTw dt = dif_tw(lane, stw);
   const int64_t lines = batch * nl * blast;
   for (int64_t li = (int64_t)blockIdx.x * nw + warp; li < lines; li += (int64_t)gridDim.x * nw) {
     const int64_t frame = li / (nl * blast);
@@ -1609,16 +1617,7 @@ __global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2*
       X[k1] = cmul(acc, t0);
     }
 #pragma unroll
-    for (int k1 = 0; k1 < B1; ++k1) {                  // dim-0 DFT across the lanes (DIF)
-      float2 x = X[k1];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        const int h = 16 >> q;
-        const float2 p = make_float2(__shfl_xor_sync(0xffffffffu, x.x, h), __shfl_xor_sync(0xffffffffu, x.y, h));
-        x = (lane & h) ? cmul(csub(p, x), stw[q]) : cadd(x, p);
-      }
-      X[k1] = x;
-    }
+    for (int k1 = 0; k1 < B1; ++k1) X[k1] = warp_dif(X[k1], 5, dt);   // dim-0 DFT across the lanes (DIF)
     const int k0 = brev(lane, 5);
     const float gamma = lp.gamma;
     uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
@@ -1661,6 +1660,7 @@ __global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2*
     const int h = 16 >> q;
     stw[q] = tw[((lane & (h - 1)) * 64) / h];          // W_{2h}^{lane mod h}
   }
+  const DifTw dt = dif_tw(lane, stw);
   const float2 w64 = tw[2 * lane];                      // W_64^j (first dim-0 stage)
   const int b1 = lane & (B1 - 1);                       // lanes >= B1 duplicate
   const float2 t1 = sh1 ? tw[b1 * (64 / B1)] : make_float2(1.f, 0.f);   // e^{-j pi b1 / B1}
@@ -1691,7 +1691,7 @@ __global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2*
       const int b0 = warp + 8 * q;
       float2 x = cmul(v[q], t1);
       if (sh0) x = cmul(x, tw[b0]);                    // e^{-j pi b0 / 64}
-      x = warp_dif(x, lane, LB1, stw);
+      x = warp_dif(x, LB1, dt);
       if (lane < B1) V[b0][k1_of_lane] = x;
     }
     __syncthreads();
@@ -1702,8 +1702,8 @@ __global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2*
 #pragma unroll
     for (int k1 = warp; k1 < B1; k1 += 8) {
       const float2 a = V[lane][k1], b = V[lane + 32][k1];
-      const float2 u = warp_dif(cadd(a, b), lane, 5, stw);
-      const float2 t = warp_dif(cmul(csub(a, b), w64), lane, 5, stw);
+      const float2 u = warp_dif(cadd(a, b), 5, dt);
+      const float2 t = warp_dif(cmul(csub(a, b), w64), 5, dt);
       const int64_t ke = (int64_t)(k0e * B1 + k1) * blast + kl, ko = ke + (int64_t)B1 * blast;
       if (u.x * u.x + u.y * u.y > gamma) atomicOr(bm + (ke >> 5), 1u << (ke & 31));
       if (t.x * t.x + t.y * t.y > gamma) atomicOr(bm + (ko >> 5), 1u << (ko & 31));
