@@ -94,6 +94,10 @@ CASES = [
     ("2d_v_mu1_dense", (512, 128), (16, 8), 4, dict(p_fa=0.05, mu=1), 2, "fused"),
     ("2d_v_L12_B64", (256, 256), (64, 8), 12, dict(p_fa=1e-2, mu=9, random_tau=True), 2, "fused"),
     ("2d_v_B1_64", (128, 256), (8, 64), 5, dict(p_fa=1e-2), 2, "fused"),
+    # k_fused2v corners (rsft_run on D = 2 fused plans): B_1 = 32 (one bucket row per bitmap word),
+    # B_0 = 4 (lanes duplicate rows), L = 7 < LP = 8 with mu = 5 (bit-sliced counts)
+    ("2d_f2v_b1_32", (128, 256), (8, 32), 5, dict(p_fa=1e-3, random_tau=True), 3, "fused"),
+    ("2d_f2v_b0_4_mu", (64, 128), (4, 8), 7, dict(p_fa=1e-2, mu=5), 3, "fused"),
     ("3d_B_eq_N_last", (16, 32, 32), (4, 8, 32), 3, dict(p_fa=1e-3), 1, "split"),
     # tensor-core split fold (k_split_mma: N_last = 64, A_1 % 16 == 0, L <= 16, L % 4 == 0)
     ("3d_mma_A16", (16, 128, 64), (4, 8, 8), 8, dict(p_fa=1e-3, random_tau=True), 2, "split"),
