@@ -119,6 +119,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// mbar_wait for warps that usually wait long (nothing else to do meanwhile): test the phase, then
+// sleep `ns` before the next test, so the waiting warp does not take issue slots from the warps
+// doing the work (try_wait returns long before its suspend-time hint and its loop re-issues).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
+
 constexpr int kStageIdx = 2048;          // indices staged per CTA for coalesced writes
 
 // Block-wide exclusive scan of one int per thread; returns the prefix, *total = sum.

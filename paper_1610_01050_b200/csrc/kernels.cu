@@ -496,7 +496,11 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
       const int L = pd.L, wpl = pd.wpl;
       for (int64_t fi = vw; fi < nfr; fi += nv) {
         const int slot = (int)(fi & (kG1BS - 1));
-        mbar_wait(&bfull[slot], (uint32_t)((fi / kG1BS) & 1));
+#ifndef RSFT_G1_SLEEP
+#define RSFT_G1_SLEEP 0
+#endif
+        if (RSFT_G1_SLEEP) mbar_wait_backoff(&bfull[slot], (uint32_t)((fi / kG1BS) & 1), RSFT_G1_SLEEP);
+        else mbar_wait(&bfull[slot], (uint32_t)((fi / kG1BS) & 1));
         const uint32_t* b = bslot + slot * bsw;
         uint32_t mlo[VL], mhi[VL];
 #pragma unroll
@@ -521,7 +525,10 @@ __global__ void __launch_bounds__(VL ? 672 : 544, 1) k_gather1d(PlanDev pd, cons
       int64_t fi = 0;
       const int64_t nit = seg ? nfr * nl : nfr;
       for (int64_t g = 0; g < nit; ++g) {           // item g = (frame fi, segment j)
-        if (g >= S) mbar_wait(&empty[s], ph);
+        if (g >= S) {
+          if (RSFT_G1_SLEEP) mbar_wait_backoff(&empty[s], ph, RSFT_G1_SLEEP);
+          else mbar_wait(&empty[s], ph);
+        }
         mbar_expect_tx(&full[s], fbytes);
         const int64_t frame = blockIdx.x + fi * gridDim.x;
         const int64_t row = seg ? frame * pd.L + l0 + j : frame;
@@ -1631,24 +1638,26 @@ __global__ void __launch_bounds__(256) k_split_fft_w32(PlanDev pd, const float2*
   }
 }
 
-// Split mode, kernel 2, warp-register form for B_0 = 64 outer grids (D == 3, c5: 64 x 32): a
-// 256-thread CTA per (frame, loop, k_last) line, two barriers.  Rows: warp w takes bucket rows
-// b0 = w, w + 8, ...; lane j = bucket b1 gathers residue (sigma_0 b0 + tau_0, sigma_1 b1 + tau_1)
-// (mod B) of the summed folded spectra (I3), applies both half-bucket twiddles (L1) and the warp
-// runs the B1-point dim-1 DIF across its lanes (xor shuffles; 8 rows in flight per warp).
-// Columns: warp w takes columns k1 = w, w + 8, ...; lane j holds rows j and j + 32, the first
-// radix-2 stage of the 64-point dim-0 DIF runs in-lane and the two 32-point halves across the
-// lanes: lane p then holds k0 = 2 brev5(p) (+1).  |.|^2 > gamma_l -> atomicOr into the bitmap
+// Split mode, kernel 2, warp-register form for B_0 = 32 / 64 outer grids (D == 3; c3: 32 x 16,
+// c5: 64 x 32): a 256-thread CTA per (frame, loop, k_last) line, two barriers.  Rows: warp w takes
+// bucket rows b0 = w, w + 8, ...; lane j = bucket b1 gathers residue (sigma_0 b0 + tau_0,
+// sigma_1 b1 + tau_1) (mod B) of the summed folded spectra (I3), applies both half-bucket
+// twiddles (L1) and the warp runs the B1-point dim-1 DIF across its lanes (B0 / 8 rows in flight
+// per warp).  Columns: warp w takes columns k1 = w, w + 8, ...; lane j holds row j (B0 = 32: one
+// 32-point lane DIF, lane p then holds k0 = brev5(p)) or rows j and j + 32 (B0 = 64: the first
+// radix-2 stage of the 64-point dim-0 DIF in-lane, the two 32-point halves across the lanes:
+// lane p then holds k0 = 2 brev5(p) (+1)).  |.|^2 > gamma_l -> atomicOr into the bitmap
 // words (zeroed by the fold kernel).  Alg. 1 l.9-10; Eq. tpd.
-template <int B1>
-__global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2* __restrict__ F, int rl0, int rnl,
+template <int B0, int B1>
+__global__ void __launch_bounds__(256) k_split_fft_wr(PlanDev pd, const float2* __restrict__ F, int rl0, int rnl,
                                                         int nchunk, int l0, int nl, int64_t batch,
                                                         uint32_t* __restrict__ bitmaps, float2* __restrict__ spectra,
                                                         int seg_L) {
   pdl_enter();
   constexpr int LB1 = B1 == 32 ? 5 : B1 == 16 ? 4 : 3;
   __shared__ float2 tw[128];
-  __shared__ float2 V[64][B1 + 1];
+  constexpr int RQ = B0 / 8;                            // rows per warp
+  __shared__ float2 V[B0][B1 + 1];
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tw[i] = c_tw128[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1673,24 +1682,24 @@ __global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2*
     const LoopDev lp = pd.loops[l0 + lg];
     const float2* src = F + ((((size_t)frame * rnl + (l0 + l - rl0)) * blast + kl) * nchunk) * bouter;
     const int r1 = (lp.sig[1] * b1 + lp.tau[1]) & (B1 - 1);
-    float2 v[8];
+    float2 v[RQ];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {                      // rows b0 = warp + 8 q: all gathers in flight
+    for (int q = 0; q < RQ; ++q) {                     // rows b0 = warp + 8 q: all gathers in flight
       const int b0 = warp + 8 * q;
-      v[q] = __ldg(src + ((lp.sig[0] * b0 + lp.tau[0]) & 63) * B1 + r1);
+      v[q] = __ldg(src + ((lp.sig[0] * b0 + lp.tau[0]) & (B0 - 1)) * B1 + r1);
     }
     for (int c = 1; c < nchunk; ++c) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < RQ; ++q) {
         const int b0 = warp + 8 * q;
-        v[q] = cadd(v[q], __ldg(src + (size_t)c * bouter + ((lp.sig[0] * b0 + lp.tau[0]) & 63) * B1 + r1));
+        v[q] = cadd(v[q], __ldg(src + (size_t)c * bouter + ((lp.sig[0] * b0 + lp.tau[0]) & (B0 - 1)) * B1 + r1));
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < RQ; ++q) {
       const int b0 = warp + 8 * q;
       float2 x = cmul(v[q], t1);
-      if (sh0) x = cmul(x, tw[b0]);                    // e^{-j pi b0 / 64}
+      if (sh0) x = cmul(x, tw[b0 * (64 / B0)]);       // e^{-j pi b0 / B0}
       x = warp_dif(x, LB1, dt);
       if (lane < B1) V[b0][k1_of_lane] = x;
     }
@@ -1698,16 +1707,27 @@ __global__ void __launch_bounds__(256) k_split_fft_w64(PlanDev pd, const float2*
     const float gamma = lp.gamma;
     uint32_t* bm = bitmaps + ((size_t)frame * nl + l) * pd.wpl;
     float2* sp = spectra ? spectra + ((size_t)frame * nl + l) * pd.btot : nullptr;
-    const int k0e = 2 * brev(lane, 5);
+    if constexpr (B0 == 64) {
+      const int k0e = 2 * brev(lane, 5);
 #pragma unroll
-    for (int k1 = warp; k1 < B1; k1 += 8) {
-      const float2 a = V[lane][k1], b = V[lane + 32][k1];
-      const float2 u = warp_dif(cadd(a, b), 5, dt);
-      const float2 t = warp_dif(cmul(csub(a, b), w64), 5, dt);
-      const int64_t ke = (int64_t)(k0e * B1 + k1) * blast + kl, ko = ke + (int64_t)B1 * blast;
-      if (u.x * u.x + u.y * u.y > gamma) atomicOr(bm + (ke >> 5), 1u << (ke & 31));
-      if (t.x * t.x + t.y * t.y > gamma) atomicOr(bm + (ko >> 5), 1u << (ko & 31));
-      if (sp) { sp[ke] = u; sp[ko] = t; }
+      for (int k1 = warp; k1 < B1; k1 += 8) {
+        const float2 a = V[lane][k1], b = V[lane + 32][k1];
+        const float2 u = warp_dif(cadd(a, b), 5, dt);
+        const float2 t = warp_dif(cmul(csub(a, b), w64), 5, dt);
+        const int64_t ke = (int64_t)(k0e * B1 + k1) * blast + kl, ko = ke + (int64_t)B1 * blast;
+        if (u.x * u.x + u.y * u.y > gamma) atomicOr(bm + (ke >> 5), 1u << (ke & 31));
+        if (t.x * t.x + t.y * t.y > gamma) atomicOr(bm + (ko >> 5), 1u << (ko & 31));
+        if (sp) { sp[ke] = u; sp[ko] = t; }
+      }
+    } else {
+      const int k0 = brev(lane, 5);
+#pragma unroll
+      for (int k1 = warp; k1 < B1; k1 += 8) {
+        const float2 u = warp_dif(V[lane][k1], 5, dt);
+        const int64_t k = (int64_t)(k0 * B1 + k1) * blast + kl;
+        if (u.x * u.x + u.y * u.y > gamma) atomicOr(bm + (k >> 5), 1u << (k & 31));
+        if (sp) sp[k] = u;
+      }
     }
     __syncthreads();                                     // V reused by the next line
   }
@@ -2006,11 +2026,14 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
   const int64_t blast = p->b[D - 1];
   const int64_t b1 = D == 3 ? p->b[1] : 1;
   {
-    // warp form for 32 x B1 outer grids (c3); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
+    // warp form with a direct dim-1 DFT for 32 x B1 outer grids (RSFT_FFT_W32DFT=1; the register
+    // form below is the default); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
     const char* ew = getenv("RSFT_FFT_WARP");
+    const char* eo = getenv("RSFT_FFT_W32DFT");
     const int LT = seg_L > 0 ? seg_L : nl;
     const size_t smw = ((size_t)LT * b1 * b1 + 128) * 8;
-    if (D == 3 && p->b[0] == 32 && (b1 == 8 || b1 == 16) && smw <= 64 * 1024 && !(ew && ew[0] == '0')) {
+    if (eo && eo[0] == '1' && D == 3 && p->b[0] == 32 && (b1 == 8 || b1 == 16) && smw <= 64 * 1024 &&
+        !(ew && ew[0] == '0')) {
       auto kw = b1 == 8 ? k_split_fft_w32<8> : k_split_fft_w32<16>;
       rsft_status s = check(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw), "smem attr");
       if (s) return s;
@@ -2024,17 +2047,21 @@ static rsft_status launch_split_fft(rsft_plan_s* p, const float2* F, int rl0, in
     }
   }
   {
-    // two-warp form for 64 x B1 outer grids (c5); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
+    // register form for 32 / 64 x B1 outer grids (c3, c5); RSFT_FFT_WARP=0 (read per launch) keeps the CTA form
     const char* ew = getenv("RSFT_FFT_WARP");
-    if (D == 3 && p->b[0] == 64 && (b1 == 8 || b1 == 16 || b1 == 32) && !(ew && ew[0] == '0')) {
-      auto kw = b1 == 8 ? k_split_fft_w64<8> : b1 == 16 ? k_split_fft_w64<16> : k_split_fft_w64<32>;
+    const char* eo = getenv("RSFT_FFT_W32DFT");         // 1: B_0 = 32 grids use k_split_fft_w32 (direct dim-1 DFT)
+    const bool w32dft = eo && eo[0] == '1';
+    if (D == 3 && (p->b[0] == 64 || (p->b[0] == 32 && !w32dft)) && (b1 == 8 || b1 == 16 || b1 == 32) &&
+        !(ew && ew[0] == '0')) {
+      auto kw = p->b[0] == 64 ? (b1 == 8 ? k_split_fft_wr<64, 8> : b1 == 16 ? k_split_fft_wr<64, 16> : k_split_fft_wr<64, 32>)
+                              : (b1 == 8 ? k_split_fft_wr<32, 8> : b1 == 16 ? k_split_fft_wr<32, 16> : k_split_fft_wr<32, 32>);
       const int64_t lines = batch * nl * blast;
       const int64_t grid = std::min<int64_t>(lines, 8 * (int64_t)p->num_sms);
       if (cudaError_t le_ = pdl_launch(kw, (unsigned)grid, 256, 0, st, p->dev, F, rl0, rnl, nchunk, l0, nl, batch, bm,
                                        reinterpret_cast<float2*>(spectra), seg_L); le_ != cudaSuccess)
-        return check(le_, "k_split_fft_w64 launch");
+        return check(le_, "k_split_fft_wr launch");
       p->last_launches += 1;
-      return check(cudaGetLastError(), "k_split_fft_w64 launch");
+      return check(cudaGetLastError(), "k_split_fft_wr launch");
     }
   }
   size_t smem2 = 128 * 8 + (size_t)p->b[0] * (b1 + 1) * 8;

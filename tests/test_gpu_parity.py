@@ -246,8 +246,9 @@ W32_CASES = [c for c in CASES if c[0].startswith(("3d_w32", "3d_w64"))]
 
 @pytest.mark.parametrize("case", W32_CASES, ids=[c[0] for c in W32_CASES])
 def test_outer_fft_warp_vs_cta_forms(case, monkeypatch):
-    """The warp-form outer FFT (k_split_fft_w32) and the CTA form (RSFT_FFT_WARP=0, read per
-    launch) on the same input: both within the oracle tolerance, bits equal outside the band."""
+    """The register-form outer FFT (k_split_fft_wr, default for B_0 = 32 / 64), the CTA form
+    (RSFT_FFT_WARP=0) and, for B_0 = 32, the direct-DFT warp form (k_split_fft_w32,
+    RSFT_FFT_W32DFT=1; env read per launch) on the same input: each within the oracle tolerance."""
     name, n, b, loops, kw, batch, mode = case
     op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
     wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=77)
@@ -256,6 +257,11 @@ def test_outer_fft_warp_vs_cta_forms(case, monkeypatch):
     _, res_cta, reps = run_case(op, x, mode=mode)
     assert max(r["max_ratio"] for r in reps) < 1e-4
     monkeypatch.delenv("RSFT_FFT_WARP")
+    if b[0] == 32:
+        monkeypatch.setenv("RSFT_FFT_W32DFT", "1")
+        _, _, reps = run_case(op, x, mode=mode)
+        assert max(r["max_ratio"] for r in reps) < 1e-4
+        monkeypatch.delenv("RSFT_FFT_W32DFT")
     _, res_w, reps = run_case(op, x, mode=mode)
     assert max(r["max_ratio"] for r in reps) < 1e-4
 
