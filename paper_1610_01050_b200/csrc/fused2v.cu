@@ -41,7 +41,7 @@ constexpr int kF2vFold = 8;        // fold warps: 4 of the 32 residue classes of
 constexpr int kF2vEpi = 8;         // epilogue (FFT + threshold + vote) warps: one per loop (L <= 8)
 constexpr int kF2vU = 8;           // rows per TMA box (4 KiB)
 constexpr int kF2vFB = 2;          // residue-sum slots F (one slot + 5 ring stages measured slower)
-constexpr int kF2vMaxRows = 8;     // vote rows per epilogue thread at NE = 4 (32 / NE: N0 <= 1024)
+constexpr int kF2vMaxN0 = 1024;    // vote rows per epilogue thread: 32 / NE (N0 <= 1024)
 
 template <int NE>
 __device__ __forceinline__ void epi_sync() {
@@ -407,19 +407,13 @@ __global__ void __launch_bounds__(32 * (kF2vFold + NE), 1) k_fused2v(PlanDev pd,
   }
 }
 
-static rsft_status check2v(cudaError_t e, const char* what) {
-  if (e == cudaSuccess) return RSFT_OK;
-  set_error(std::string(what) + ": " + cudaGetErrorString(e));
-  return RSFT_E_CUDA;
-}
-
 rsft_status upload_twiddles_2v(cudaStream_t st) {
   float2 tw[128];
   for (int k = 0; k < 128; ++k) {
     const double a = -2.0 * M_PI * (double)k / 128.0;
     tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
   }
-  return check2v(cudaMemcpyToSymbolAsync(c_tw2v, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st), "twiddles (2v)");
+  return check(cudaMemcpyToSymbolAsync(c_tw2v, tw, sizeof(tw), 0, cudaMemcpyHostToDevice, st), "twiddles (2v)");
 }
 
 // Shapes the kernel covers: D = 2, all L <= 8 loops, B0 <= 32, B1 in {8, 16, 32}, N1 in {128, 256},
@@ -430,7 +424,7 @@ bool fused2v_ok(const rsft_plan_s* p) {
   if (p->D != 2 || p->L > 8 || !p->dev.xmask) return false;
   const int64_t B0 = p->b[0], B1 = p->b[1], N0 = p->n[0], N1 = p->n[1];
   if (B0 < 2 || B0 > 32 || !(B1 == 8 || B1 == 16 || B1 == 32)) return false;
-  if (N1 < 128 || N1 > 256 || N0 > 32 * 4 * kF2vMaxRows) return false;   // W = N1 / 32 in {4, 8}: 16-B E rows
+  if (N1 < 128 || N1 > 256 || N0 > kF2vMaxN0) return false;   // W = N1 / 32 in {4, 8}: 16-B E rows
   return true;
 }
 
@@ -452,14 +446,14 @@ static rsft_status launch_f2v_t(rsft_plan_s* p, const void* d_x, int64_t batch, 
   CUtensorMap tmap;
   rsft_status s = fold_map(p, d_x, batch, p->n[0], &tmap, kF2vU, 0);
   if (s) return s;
-  s = check2v(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr (2v)");
+  s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr (2v)");
   if (s) return s;
   const int64_t grid = std::min<int64_t>(batch, p->num_sms);
   if (cudaError_t e = pdl_launch(kern, (unsigned)grid, 32 * (kF2vFold + NE), smem, st, p->dev, tmap, batch, S, bm, det, rcount,
                                  slots, list_cap); e != cudaSuccess)
-    return check2v(e, "k_fused2v launch");
+    return check(e, "k_fused2v launch");
   p->last_launches += 1;
-  return check2v(cudaGetLastError(), "k_fused2v launch");
+  return check(cudaGetLastError(), "k_fused2v launch");
 }
 
 // rsft_run on a fused2v_ok plan: bitmaps, detection words, per-frame counts + local lists.
