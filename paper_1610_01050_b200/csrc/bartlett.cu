@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "rsft_internal.h"
@@ -515,6 +516,84 @@ __global__ void __launch_bounds__(256) k_bart_1d(PlanDev pd, const float2* __res
   }
 }
 
+// Single pass for 1-D frames of N = 4096 = 64 x 64 samples (c1) with the transpose-form warp FFTs
+// (no shuffle stages, bart_warp_fft_t): n = 64 r + c; warp w owns columns c = 16 w .. 16 w + 15 and,
+// after the barrier, rows k1 = 16 w .. 16 w + 15.  Per segment: the warp loads its 16 columns
+// straight from global memory (lane l: rows l and l + 32, 16 contiguous samples each; window on
+// load), runs the 64-point DFTs down them, applies W_N^{c k1} and stores the tile [k1][c]; then
+// the 64-point DFTs along its 16 rows, |X|^2 accumulated in registers over the T segments.
+// X[k1 + 64 k2] = sum_c W_64^{c k2} W_N^{c k1} sum_r x[64 r + c] W_64^{r k1}.  Power and detection
+// words are written once per frame (natural order through the tile).
+__global__ void __launch_bounds__(128) k_bart_1d4096(PlanDev pd, const float2* __restrict__ x, int64_t batch, int T,
+                                                     const float* __restrict__ w0, float* __restrict__ power,
+                                                     float scale, float gamma, uint32_t* __restrict__ det) {
+  extern __shared__ __align__(16) float2 b4[];
+  constexpr int N = 4096, R = 64, C = 64, st = C + 1;
+  float2* tile = b4;                                   // [R][C + 1]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2* xs = tile + R * st + warp * (32 * 33);
+  const float2 tw1 = bart_twn(pd.btw, lane, 6);        // W_64^lane
+  const int c0 = 16 * warp;
+  const int L = lane >> 1, q1 = lane & 1;              // output line (of 16) / phase after the transpose
+  float wcol[2][16];                                   // window of this lane's samples (registers: 4.8 M
+#pragma unroll                                         // frames/s against 2.8 M with L1 loads, 3 CTAs/SM)
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) wcol[k][j] = w0[C * (lane + 32 * k) + c0 + j];
+  for (int64_t frame = blockIdx.x; frame < batch; frame += gridDim.x) {
+    float acc[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) acc[r] = 0.f;
+    for (int s = 0; s < T; ++s) {
+      const float2* src = x + ((size_t)frame * T + s) * N + c0;
+      float2 a[32];                                    // a[j M + k] = col_j[lane + 32 k], M = 2
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float4* p4 = reinterpret_cast<const float4*>(src + C * (lane + 32 * k));
+#pragma unroll
+        for (int j2 = 0; j2 < 8; ++j2) {
+          const float4 v = __ldcs(p4 + j2);
+          const float wa = wcol[k][2 * j2], wb = wcol[k][2 * j2 + 1];
+          a[(2 * j2) * 2 + k] = make_float2(v.x * wa, v.y * wa);
+          a[(2 * j2 + 1) * 2 + k] = make_float2(v.z * wb, v.w * wb);
+        }
+      }
+      bart_warp_fft_t<2>(a, lane, tw1, xs);            // lane (L, q1): col c0 + L, k1 = q1 + 2 brev5(r2)
+      __syncthreads();                                 // previous segment's row readers done
+      {
+        const int c = c0 + L;
+#pragma unroll
+        for (int r2 = 0; r2 < 32; ++r2) {
+          const int k1 = q1 + 2 * bart_brev_c(r2, 5);
+          tile[k1 * st + c] = bart_cmul(a[r2], bart_twn(pd.btw, (c * k1) & (N - 1), 12));
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)                     // rows k1 = c0 + j: a[j M + k] = row[lane + 32 k]
+#pragma unroll
+        for (int k = 0; k < 2; ++k) a[j * 2 + k] = tile[(c0 + j) * st + lane + 32 * k];
+      bart_warp_fft_t<2>(a, lane, tw1, xs);            // lane (L, q1): k1 = c0 + L, k2 = q1 + 2 brev5(r2)
+#pragma unroll
+      for (int r2 = 0; r2 < 32; ++r2) acc[r2] += a[r2].x * a[r2].x + a[r2].y * a[r2].y;
+    }
+    __syncthreads();
+    float* pt = reinterpret_cast<float*>(tile);        // power in natural order k = k1 + 64 k2
+#pragma unroll
+    for (int r2 = 0; r2 < 32; ++r2) pt[(c0 + L) + R * (q1 + 2 * bart_brev_c(r2, 5))] = acc[r2];
+    __syncthreads();
+    float* pdst = power + (size_t)frame * N;
+    uint32_t* ddst = det ? det + (size_t)frame * (N >> 5) : nullptr;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+      const float p = pt[k];
+      pdst[k] = p;
+      const unsigned word = __ballot_sync(0xffffffffu, p * scale > gamma);
+      if (ddst && lane == 0) ddst[k >> 5] = word;
+    }
+    __syncthreads();
+  }
+}
+
 rsft_status upload_bartlett_twiddles(cudaStream_t st) {
   float2 tw[2048];
   for (int k = 0; k < 2048; ++k)
@@ -557,7 +636,18 @@ rsft_status rsft_bartlett(rsft_plan_t p, const void* d_x, int64_t batch, int32_t
   const bool single = ntot <= kBartTile;
   if (!single && (inner > kBartTile || !d_scratch)) return RSFT_E_UNSUPPORTED;
   const size_t tw_bytes = 2048 * 8;
-  if (p->D == 1 && ntot >= 1024 && ntot <= 4096) {   // four-step warp FFTs, one pass
+  const char* e1 = getenv("RSFT_BART_1D_SHFL");       // 1: the shuffle-form four-step kernel for N = 4096
+  if (p->D == 1 && ntot == 4096 && !(e1 && e1[0] == '1')) {   // transpose-form four-step, one pass
+    const size_t smem = ((size_t)64 * 65 + 4 * 32 * 33) * 8;
+    if (cudaFuncSetAttribute(k_bart_1d4096, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return RSFT_E_CUDA;
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_bart_1d4096, 128, smem);
+    const int64_t grid = std::min<int64_t>(batch, (int64_t)std::max(nb, 1) * p->num_sms);
+    k_bart_1d4096<<<(unsigned)grid, 128, smem, st>>>(p->dev, reinterpret_cast<const float2*>(d_x), batch, segments,
+                                                     wr[0], d_power, scale, gam, d_detect);
+    p->last_launches = 1;
+  } else if (p->D == 1 && ntot >= 1024 && ntot <= 4096) {   // four-step warp FFTs, one pass
     const int lg = __builtin_ctzll(ntot), lr = lg / 2, lc = lg - lr;
     void (*k)(PlanDev, const float2*, int64_t, int, const float*, float*, float, float, uint32_t*) = nullptr;
     if (lr == 5 && lc == 5) k = k_bart_1d<1, 1>;
