@@ -323,6 +323,69 @@ __global__ void __launch_bounds__(kThreads) k_etab(PlanDev pd, const uint32_t* _
   }
 }
 
+// cp.async (LDGSTS) helpers of the software-pipelined E copies (k_vote, k_vote3d)
+__device__ __forceinline__ void v3_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void v3_cp4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void v3_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void v3_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// k_etab for B_last = 8 with the plan-constant nibble tables (c3, c5): one thread per first-stage
+// bitmap word = 4 bucket rows (k0, k1) of 8 last-dim buckets each; every E word is two nibble
+// lookups, NT[l][0][bits 0-3][w] | NT[l][1][bits 4-7][w], and the 4 W words of the thread's rows
+// are contiguous in etab (row index = 4 x word index: B_tot = 32 wpl).  One coalesced load per
+// thread, issued before the table staging, no per-bit loop.
+template <int W>
+__global__ void __launch_bounds__(256) k_etab8(PlanDev pd, const uint32_t* __restrict__ bitmaps, int64_t nwords) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint32_t nts[];    // [L][2][16][W]
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t bw = i < nwords ? __ldg(bitmaps + i) : 0u;
+  const int L = pd.L, wpl = pd.wpl;
+  for (int j = threadIdx.x; j < L * 8 * W; j += blockDim.x)
+    reinterpret_cast<uint4*>(nts)[j] = __ldg(reinterpret_cast<const uint4*>(pd.ntab) + j);
+  __syncthreads();
+  if (i >= nwords) return;
+  const int l = (int)((i / wpl) % L);
+  const uint32_t* NT = nts + l * 32 * W;
+  uint32_t out[4 * W];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t lo = (bw >> (8 * q)) & 15u, hi = (bw >> (8 * q + 4)) & 15u;
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[q * W + w] = NT[lo * W + w] | NT[(16 + hi) * W + w];
+  }
+  uint4* dst = reinterpret_cast<uint4*>(pd.etab + (size_t)i * 4 * W);
+#pragma unroll
+  for (int v = 0; v < W; ++v) dst[v] = make_uint4(out[4 * v], out[4 * v + 1], out[4 * v + 2], out[4 * v + 3]);
+}
+
+// E words of every dim-0 bucket for the batch (D == 3): k_etab8 where it applies, else k_etab.
+static rsft_status launch_etab(rsft_plan_s* p, const uint32_t* bm, int64_t batch, cudaStream_t st) {
+  const int W = (int)(p->n[2] / 32);
+  const char* off = getenv("RSFT_NO_ETAB8");         // read per launch: tests select either kernel
+  const bool e8 = !(off && off[0] && off[0] != '0') && p->b[2] == 8 && p->dev.ntab && (p->b[0] * p->b[1]) % 4 == 0 &&
+                  (W == 1 || W == 2 || W == 4) && p->dev.wpl * 32 == p->b[0] * p->b[1] * p->b[2];
+  if (e8) {
+    const int64_t nw = batch * p->L * p->dev.wpl;
+    const size_t smem = (size_t)p->L * 32 * W * 4;
+    auto kern = W == 1 ? k_etab8<1> : W == 2 ? k_etab8<2> : k_etab8<4>;
+    if (cudaError_t le_ = pdl_launch(kern, (unsigned)((nw + 255) / 256), 256, smem, st, p->dev, bm, nw); le_ != cudaSuccess)
+      return check(le_, "k_etab8 launch");
+  } else {
+    const int64_t ne = batch * p->L * p->b[0] * p->b[1];
+    const int64_t eg = (ne + kThreads - 1) / kThreads;
+    if (cudaError_t le_ = pdl_launch(k_etab, (unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st,
+                                     p->dev, bm, batch); le_ != cudaSuccess)
+      return check(le_, "k_etab launch");
+  }
+  p->last_launches += 1;
+  return RSFT_OK;
+}
+
 template <int CW, int MODE, bool COUNT, bool LIST>
 #ifndef RSFT_VOTE_CTAS
 #define RSFT_VOTE_CTAS 4
@@ -591,17 +654,48 @@ __global__ void __launch_bounds__(32 * kVote1dWarps, MINB) k_vote1d(PlanDev pd, 
 // (Alg. 1 l.11-14).  The L loads of a word are independent (all in flight).
 // Outputs: detection words, and (list mode) the region count + ascending local index list.
 // ------------------------------------------------------------------------------------
-template <int LP, int MODE>
+
+// Issue the copies of region r's E blocks (one dim-0 bucket per loop, rw words each) into the
+// warp's shared buffer dst (cp.async: no registers held, completion by commit group).
+__device__ __forceinline__ void v3_issue(const PlanDev& pd, const int* s0, int64_t r, int64_t slab, int64_t d0b,
+                                         int L, int B0, int rw, int lgrw, uint32_t n0m, int lga0, int lane,
+                                         uint32_t dst) {
+  const int64_t frame = r / slab, i0 = d0b + (r - frame * slab);
+  const uint32_t* et = pd.etab + (size_t)frame * L * B0 * rw;
+  if ((rw & 3) == 0) {                               // 16-B pieces: one per lane at c3 (L rw = 128)
+    const int lg4 = lgrw - 2;
+    for (int j = lane; j < (L * rw) >> 2; j += 32) {
+      const int l = j >> lg4, q = j & ((rw >> 2) - 1);
+      const int k0 = (int)((((uint32_t)s0[l] * (uint32_t)i0) & n0m) >> lga0);
+      v3_cp16(dst + 16u * j, et + ((size_t)l * B0 + k0) * rw + 4 * q);
+    }
+  } else {
+    for (int j = lane; j < L * rw; j += 32) {
+      const int l = j >> lgrw, q = j & (rw - 1);
+      const int k0 = (int)((((uint32_t)s0[l] * (uint32_t)i0) & n0m) >> lga0);
+      v3_cp4(dst + 4u * j, et + ((size_t)l * B0 + k0) * rw + q);
+    }
+  }
+}
+
+// IT > 0: the region's items fit IT passes of 32 (c3: 4 passes).  The word offset of every
+// (pass, loop) lookup, l rw + k1_l(i1) W + w, does not depend on the region (sigma_{l,1} is per
+// loop), so each lane computes its IT x LP byte offsets once per kernel and keeps them in
+// registers: a lookup is then an add + a shared load, with no per-lookup branch (the index
+// arithmetic was 53 % of the kernel's instructions, ncu `profiles/r02c_c3_k_vote3d_before.lines.txt`).
+template <int LP, int MODE, int IT>
 __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64_t d0b, int64_t d0e,
                                                  uint32_t* __restrict__ detect, unsigned long long* __restrict__ rcount,
                                                  uint32_t* __restrict__ slots, int list_cap) {
   pdl_enter();
   __shared__ int s0[LP], s1[LP];
-  extern __shared__ __align__(16) uint32_t v3s[];    // per warp: the region's E rows [L][B1][W]
+  extern __shared__ __align__(16) uint32_t v3s[];    // per warp: two buffers of the region's E rows [L][B1][W]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int L = pd.L, B0 = pd.b[0], B1 = pd.b[1], W = pd.n[2] >> 5, N1 = pd.n[1];
   const int rw = B1 * W, lgrw = __ffs(rw) - 1;       // words per (loop, k0) E block
-  uint32_t* es = v3s + (size_t)warp * L * rw;
+  const int ew = L * rw;                             // words per buffer
+  uint32_t* es0 = v3s + (size_t)warp * 2 * ew;
+  const uint32_t sa0 = smem_u32(es0);
   const uint32_t n0m = (uint32_t)(pd.n[0] - 1), n1m = (uint32_t)(N1 - 1);
   const int lga0 = pd.lga[0], lga1 = pd.lga[1];
   for (int l = threadIdx.x; l < LP; l += blockDim.x) {
@@ -618,81 +712,123 @@ __global__ void __launch_bounds__(256) k_vote3d(PlanDev pd, int64_t batch, int64
   const int lgW = __ffs(W) - 1;
   const int64_t slab_words = slab * items;
   const int mu = pd.mu;
-  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, TW = (int64_t)gridDim.x * nwarps;
-  for (int64_t r = gw; r < nregions; r += TW) {
-    const int64_t frame = r / slab, i0 = d0b + (r - frame * slab);
-    // this region's E blocks (one dim-0 bucket per loop) into the warp's shared copy: coalesced
-    // rw-word runs, then every detection word reads its L words from shared memory
-    __syncwarp();
-    for (int j = lane; j < L * rw; j += 32) {
-      const int l = j >> lgrw, q = j & (rw - 1);
-      const int k0 = (int)((((uint32_t)s0[l] * (uint32_t)i0) & n0m) >> lga0);
-      es[j] = __ldg(pd.etab + (((size_t)frame * L + l) * B0 + k0) * (size_t)rw + q);
-    }
-    __syncwarp();
-    const uint32_t* et[LP];
+  // byte offsets of the (pass, loop) lookups in the warp's E buffer, constant over regions;
+  // loops l >= L read word 0 and are neutralised by pad masks (no per-lookup branch)
+  uint32_t offs[IT > 0 ? IT : 1][LP];
+  uint32_t pad[LP];
 #pragma unroll
-    for (int l = 0; l < LP; ++l) et[l] = es + (l < L ? l : 0) * rw;
+  for (int l = 0; l < LP; ++l) pad[l] = l < L ? 0u : 0xffffffffu;
+  if constexpr (IT > 0) {
+#pragma unroll
+    for (int iq = 0; iq < IT; ++iq) {
+      const uint32_t it = (uint32_t)(iq * 32 + lane), i1 = it >> lgW, w = it & (uint32_t)(W - 1);
+#pragma unroll
+      for (int l = 0; l < LP; ++l)
+        offs[iq][l] = l < L ? 4u * ((uint32_t)(l * rw) + ((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w) : 0u;
+    }
+  }
+  // the L words of detection word it (and the second stage on them)
+  auto vote_word = [&](const uint32_t* es, const uint32_t (&e)[LP], bool padded) -> uint32_t {
+    (void)es;
+    uint32_t word = 0u;
+    if (MODE == 0) {
+      word = 0xffffffffu;
+#pragma unroll
+      for (int l = 0; l < LP; ++l) if (padded || l < L) word &= e[l];
+    } else if (MODE == 1) {
+#pragma unroll
+      for (int l = 0; l < LP; ++l) word |= e[l];
+    } else {
+      uint32_t pl[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int l = 0; l < LP; ++l) {
+        uint32_t carry = e[l];
+#pragma unroll
+        for (int b = 0; b < 6; ++b) { const uint32_t t = pl[b] & carry; pl[b] ^= carry; carry = t; }
+      }
+      uint32_t gt = 0u, eq = 0xffffffffu;            // bit-sliced count >= mu
+#pragma unroll
+      for (int b = 5; b >= 0; --b) {
+        const uint32_t mb = ((mu >> b) & 1) ? 0xffffffffu : 0u;
+        gt |= eq & pl[b] & ~mb;
+        eq &= ~(pl[b] ^ mb);
+      }
+      word = gt | eq;
+    }
+    return word;
+  };
+  // detection word store + region-local index list (ascending), run = detections so far
+  auto emit = [&](int it, uint32_t word, uint32_t* det, uint32_t* sl, int& run) {
+    if (it < items) det[it] = word;
+    if (__ballot_sync(0xffffffffu, word != 0u) == 0u) return;   // no detection in these 32 words
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (sl) {
+      int q = run + incl - c;
+      uint32_t v = word;
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1;
+        if (q < list_cap) sl[q] = (uint32_t)((it << 5) + bit);
+        ++q;
+      }
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  };
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, TW = (int64_t)gridDim.x * nwarps;
+  // software pipeline: region r + TW's E blocks are in flight (cp.async) while region r votes
+  if (gw < nregions) v3_issue(pd, s0, gw, slab, d0b, L, B0, rw, lgrw, n0m, lga0, lane, sa0);
+  v3_commit();
+  int buf = 0;
+  for (int64_t r = gw; r < nregions; r += TW, buf ^= 1) {
+    const int64_t frame = r / slab, i0 = d0b + (r - frame * slab);
+    if (r + TW < nregions)
+      v3_issue(pd, s0, r + TW, slab, d0b, L, B0, rw, lgrw, n0m, lga0, lane, sa0 + 4u * (uint32_t)((buf ^ 1) * ew));
+    v3_commit();
+    v3_wait1();                                      // this region's group has landed (own copies)
+    __syncwarp();                                    // ... and every lane's
+    const uint32_t* es = es0 + buf * ew;
     uint32_t* det = detect + (size_t)frame * slab_words + (size_t)(i0 - d0b) * items;
     uint32_t* sl = slots ? slots + (size_t)r * list_cap : nullptr;
     int run = 0;
-    for (int it0 = 0; it0 < items; it0 += 32) {
-      const int it = it0 + lane;
-      uint32_t word = 0u;
-      if (it < items) {
-        const uint32_t i1 = (uint32_t)(it >> lgW), w = (uint32_t)(it & (W - 1));
+    if constexpr (IT > 0) {
+#pragma unroll
+      for (int iq = 0; iq < IT; ++iq) {
+        const int it = iq * 32 + lane;
+        const uint32_t sb = sa0 + 4u * (uint32_t)(buf * ew);
         uint32_t e[LP];
 #pragma unroll
-        for (int l = 0; l < LP; ++l)
-          e[l] = l < L ? et[l][((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w] : 0u;
-        if (MODE == 0) {
-          word = 0xffffffffu;
-#pragma unroll
-          for (int l = 0; l < LP; ++l) if (l < L) word &= e[l];
-        } else if (MODE == 1) {
-#pragma unroll
-          for (int l = 0; l < LP; ++l) word |= e[l];
-        } else {
-          uint32_t pl[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-          for (int l = 0; l < LP; ++l) {
-            uint32_t carry = e[l];
-#pragma unroll
-            for (int b = 0; b < 6; ++b) { const uint32_t t = pl[b] & carry; pl[b] ^= carry; carry = t; }
-          }
-          uint32_t gt = 0u, eq = 0xffffffffu;          // bit-sliced count >= mu
-#pragma unroll
-          for (int b = 5; b >= 0; --b) {
-            const uint32_t mb = ((mu >> b) & 1) ? 0xffffffffu : 0u;
-            gt |= eq & pl[b] & ~mb;
-            eq &= ~(pl[b] ^ mb);
-          }
-          word = gt | eq;
+        for (int l = 0; l < LP; ++l) {
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e[l]) : "r"(sb + offs[iq][l]));
+          e[l] = MODE == 0 ? (e[l] | pad[l]) : (e[l] & ~pad[l]);
         }
-        det[it] = word;
+        const uint32_t word = it < items ? vote_word(es, e, true) : 0u;
+        emit(it, word, det, sl, run);
       }
-      if (__ballot_sync(0xffffffffu, word != 0u) == 0u) continue;   // no detection in these 32 words
-      const int c = __popc(word);
-      int incl = c;
+    } else {
+      for (int it0 = 0; it0 < items; it0 += 32) {
+        const int it = it0 + lane;
+        uint32_t word = 0u;
+        if (it < items) {
+          const uint32_t i1 = (uint32_t)(it >> lgW), w = (uint32_t)(it & (W - 1));
+          uint32_t e[LP];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (sl) {
-        int q = run + incl - c;
-        uint32_t v = word;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          if (q < list_cap) sl[q] = (uint32_t)((it << 5) + bit);
-          ++q;
+          for (int l = 0; l < LP; ++l)
+            e[l] = l < L ? es[l * rw + (int)(((((uint32_t)sg1[l] * i1) & n1m) >> lga1) * W + w)] : 0u;
+          word = vote_word(es, e, false);
         }
+        emit(it, word, det, sl, run);
       }
-      run += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (rcount && lane == 0) rcount[r] = (unsigned long long)run;
+    __syncwarp();                                    // every lane done reading buf before it is refilled
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------
@@ -1126,6 +1262,10 @@ template <int CW, int MODE, bool COUNT, bool LIST>
 static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                                  uint32_t* det, uint8_t* counts, cudaStream_t st) {
   int lw = 0;
+  // D == 3: E words of every dim-0 bucket once per frame (k_etab), copied per region (a
+  // double-buffered cp.async copy of the next region's rows measured slower at c5: 20 vs 17 us)
+  const int use_etab = p->D == 3 && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
+                       (d0e - d0b) > p->b[0];
   const size_t smem = vote_smem(p, &lw);
   auto kern = k_vote<CW, MODE, COUNT, LIST>;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -1139,16 +1279,8 @@ static rsft_status launch_vote_t(rsft_plan_s* p, const uint32_t* bm, int64_t bat
   if (nb < 1) { set_error("k_vote: zero occupancy"); return RSFT_E_UNSUPPORTED; }
   int64_t grid = (int64_t)nb * p->num_sms;
   if (grid > nregions) grid = nregions;
-  // D == 3: E words of every dim-0 bucket once per frame (k_etab), copied per region
-  const int use_etab = p->D == 3 && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
-                       (d0e - d0b) > p->b[0];
-  if (use_etab) {
-    const int64_t ne = batch * p->L * p->b[0] * p->b[1];
-    const int64_t eg = (ne + kThreads - 1) / kThreads;
-    if (cudaError_t le_ = pdl_launch(k_etab, (unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st, p->dev, bm, batch); le_ != cudaSuccess)
-      return check(le_, "k_etab launch");
-    p->last_launches += 1;
-  }
+  if (use_etab)
+    if ((s = launch_etab(p, bm, batch, st))) return s;
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, kThreads, smem, st, p->dev, bm, d0b, d0e, lw, np, nregions, det, counts,
                                                p->dev.region_state, use_etab); le_ != cudaSuccess)
     return check(le_, "kern launch");
@@ -1214,29 +1346,33 @@ static bool vote3d_ok(const rsft_plan_s* p, int64_t batch, int64_t d0b, int64_t 
   const int64_t lim = on && on[0] == '1' ? (int64_t)1 << 20 : 256;
   return p->D == 3 && !counts && p->dev.etab && p->dev.xmask && batch <= p->dev.etab_frames &&
          (d0e - d0b) > p->b[0] && p->n[1] * (p->n[2] / 32) <= lim && p->L <= 32 &&
-         8 * p->L * p->b[1] * (p->n[2] / 32) * 4 <= 96 * 1024;
+         16 * p->L * p->b[1] * (p->n[2] / 32) * 4 <= 192 * 1024;
 }
 
 static rsft_status launch_vote3d(rsft_plan_s* p, const uint32_t* bm, int64_t batch, int64_t d0b, int64_t d0e,
                                  uint32_t* det, unsigned long long* rcount, uint32_t* slots, int list_cap,
                                  cudaStream_t st) {
-  const int64_t ne = batch * p->L * p->b[0] * p->b[1];
-  const int64_t eg = (ne + kThreads - 1) / kThreads;
-  if (cudaError_t le_ = pdl_launch(k_etab, (unsigned)(eg < 4 * p->num_sms ? eg : 4 * p->num_sms), kThreads, 0, st,
-                                   p->dev, bm, batch); le_ != cudaSuccess)
-    return check(le_, "k_etab launch");
-  p->last_launches += 1;
+  if (rsft_status es = launch_etab(p, bm, batch, st)) return es;
   const int mode = p->mu == p->L ? 0 : p->mu == 1 ? 1 : 2;
   const int lp = p->L <= 8 ? 8 : p->L <= 16 ? 16 : 32;
   void (*kern)(PlanDev, int64_t, int64_t, int64_t, uint32_t*, unsigned long long*, uint32_t*, int) = nullptr;
-#define RSFT_V3(LPV, MV) if (lp == LPV && mode == MV) kern = k_vote3d<LPV, MV>;
-  RSFT_V3(8, 0) RSFT_V3(8, 1) RSFT_V3(8, 2) RSFT_V3(16, 0) RSFT_V3(16, 1) RSFT_V3(16, 2)
-  RSFT_V3(32, 0) RSFT_V3(32, 1) RSFT_V3(32, 2)
+  // precomputed-offset passes (IT) when a region's words fit IT passes of 32 (IT L <= 32 offsets
+  // per lane); RSFT_VOTE3D_PK=0 (read per launch) keeps the per-lookup index arithmetic
+  const int64_t items = p->n[1] * (p->n[2] / 32);
+  const char* pke = getenv("RSFT_VOTE3D_PK");
+  const bool pk = !(pke && pke[0] == '0') && (lp == 8 ? items <= 128 : lp == 16 && items <= 64);   // <= 32 offsets per lane
+  const int it = !pk ? 0 : items <= 32 ? 1 : items <= 64 ? 2 : 4;
+#define RSFT_V3(LPV, MV, ITV) if (lp == LPV && mode == MV && it == ITV) kern = k_vote3d<LPV, MV, ITV>;
+  RSFT_V3(8, 0, 0) RSFT_V3(8, 1, 0) RSFT_V3(8, 2, 0) RSFT_V3(16, 0, 0) RSFT_V3(16, 1, 0) RSFT_V3(16, 2, 0)
+  RSFT_V3(32, 0, 0) RSFT_V3(32, 1, 0) RSFT_V3(32, 2, 0)
+  RSFT_V3(8, 0, 1) RSFT_V3(8, 1, 1) RSFT_V3(8, 2, 1) RSFT_V3(16, 0, 1) RSFT_V3(16, 1, 1) RSFT_V3(16, 2, 1)
+  RSFT_V3(8, 0, 2) RSFT_V3(8, 1, 2) RSFT_V3(8, 2, 2) RSFT_V3(16, 0, 2) RSFT_V3(16, 1, 2) RSFT_V3(16, 2, 2)
+  RSFT_V3(8, 0, 4) RSFT_V3(8, 1, 4) RSFT_V3(8, 2, 4)
 #undef RSFT_V3
   const int64_t nregions = batch * (d0e - d0b);
   int64_t grid = (nregions + 7) / 8;
   if (grid > 16 * (int64_t)p->num_sms) grid = 16 * (int64_t)p->num_sms;
-  const size_t smem = (size_t)8 * p->L * p->b[1] * (p->n[2] / 32) * 4;
+  const size_t smem = (size_t)8 * 2 * p->L * p->b[1] * (p->n[2] / 32) * 4;   // 8 warps x 2 buffers
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
   if (cudaError_t le_ = pdl_launch(kern, (unsigned)grid, 256, smem, st, p->dev, batch, d0b, d0e, det, rcount, slots,

@@ -172,7 +172,7 @@ def _votes_all_kernels(plan, bm, cap, monkeypatch, envs):
     import torch
     outs = []
     for env in envs:
-        for k in ("RSFT_VOTE3D", "RSFT_NO_VOTE3D"):
+        for k in ("RSFT_VOTE3D", "RSFT_NO_VOTE3D", "RSFT_NO_ETAB8", "RSFT_VOTE3D_PK"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -184,12 +184,15 @@ def _votes_all_kernels(plan, bm, cap, monkeypatch, envs):
     return outs
 
 
-V3_ENVS = [{}, {"RSFT_NO_VOTE3D": "1"}]
+V3_ENVS = [{}, {"RSFT_NO_VOTE3D": "1"}, {"RSFT_NO_ETAB8": "1"}, {"RSFT_NO_ETAB8": "1", "RSFT_NO_VOTE3D": "1"},
+           {"RSFT_VOTE3D_PK": "0"}]
 
 
 @pytest.mark.parametrize("case", V3_CASES[:8], ids=[c[0] for c in V3_CASES[:8]])
 def test_3d_votes_bit_identical(case, monkeypatch):
-    """The 3-D votes (k_vote3d, warp per plane on the k_etab expansions; k_vote, CTA per region)
+    """The 3-D votes (k_vote3d, warp per plane on the k_etab expansions; k_vote, CTA per region),
+    each on the expansions of k_etab8 (nibble form, B_last = 8) and of k_etab (per-bit form),
+    k_vote3d with packed per-lane offsets and with per-lookup index arithmetic,
     are integer work on the same bitmaps: their detection words, counts and index lists must be
     bit-identical."""
     import torch
@@ -216,7 +219,7 @@ def test_3d_votes_bit_identical_full_size(name, monkeypatch):
     op = wl_params(wl)
     plan = make_plan(op, max_batch=batch).bind()
     bm = plan.execute(x)
-    envs = [{}, {"RSFT_VOTE3D": "1"}, {"RSFT_NO_VOTE3D": "1"}]
+    envs = [{}, {"RSFT_VOTE3D": "1"}, {"RSFT_NO_VOTE3D": "1"}, {"RSFT_NO_ETAB8": "1"}, {"RSFT_VOTE3D_PK": "0"}]
     outs = _votes_all_kernels(plan, bm, 1 << 22, monkeypatch, envs)
     assert outs[0][3] > 0
     for o in outs[1:]:
