@@ -128,7 +128,7 @@ def main():
         old["_source"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per step of the roofline's kernels (the "
                           f"whole rsft_run call for fused plans, the fold + outer-FFT kernels for split plans), mean "
                           f"per launch, from the launch lists in {src} (ncu --metrics, --clock-control none); "
-                          f"committed as profiles/r02b_launches_*.csv")
+                          f"committed as profiles/r02d_launches_*.csv")
         json.dump(old, open(traffic_path, "w"), indent=1)
     print("\n".join(L))
 
