@@ -206,9 +206,11 @@ rsft_status rsft_compact(rsft_plan_t plan, const uint32_t* d_detect, int64_t bat
  * the same index list / count as rsft_compact.  Runs the vote kernel for the frame shape
  * (D = 1: a warp per frame; D = 2 with N_0 <= 256: a CTA per frame; D = 3 with small planes: a
  * warp per dim-0 plane; else a CTA per vote region), which also writes per-region detection
- * counts and region-local sorted index lists into the workspace; then a two-pass parallel scan
- * of the region counts (offsets, total -> *d_count) and a writer that copies each region's
- * list to its offset (re-reading the region's detection words if its list overflowed).
+ * counts and region-local sorted index lists into the workspace; then, for up to 8192 vote
+ * regions, ONE launch in which every CTA sums the counts of the preceding regions itself and
+ * copies its regions' lists to their offsets (total -> *d_count); for more regions a two-pass
+ * parallel scan of the region counts and a separate writer.  A region whose list overflowed is
+ * re-read from its detection words.  Both forms give the same list (integer work).
  * Errors: E_ARG, E_STATE, E_WORKSPACE, E_CUDA. */
 rsft_status rsft_detect_compact(rsft_plan_t plan, const uint32_t* d_bitmaps, int64_t batch,
                                 uint32_t* d_detect, int64_t* d_idx, int64_t capacity,

@@ -1116,6 +1116,88 @@ __global__ void __launch_bounds__(256) k_region_write_warp(const uint32_t* __res
   }
 }
 
+// Few regions with region-local lists (c4 / c2: one region per frame, nregions <= kDirectRegions):
+// the scan and the writer in ONE launch.  A CTA of 8 warps takes G = 8 / WPR consecutive regions
+// (WPR warps per region: 4 for frames of >= 4096 detection words, 1 otherwise); it sums the raw
+// counts of every preceding region itself (block reduce over <= 64 KiB that sit in L2; counts
+// stay counts), each region's warps add the counts of the CTA's earlier regions and copy the
+// region's list with 4 independent loads in flight per thread (or, after a list overflow, one
+// warp re-reads the detection words in order); the last region writes *d_count.  Positions
+// depend only on the counts: same output as the two-pass scan + writer (bit-identity test:
+// RSFT_NO_SCANWRITE=1 selects that path).
+constexpr int64_t kDirectRegions = 8192;
+template <int WPR>
+__global__ void __launch_bounds__(256) k_region_scan_write(const uint32_t* __restrict__ det, int64_t rwords,
+                                                            const unsigned long long* __restrict__ counts,
+                                                            long long* __restrict__ d_count, int64_t nregions,
+                                                            const uint32_t* __restrict__ slots,
+                                                            long long* __restrict__ idx, int64_t capacity,
+                                                            int list_cap) {
+  constexpr int G = 8 / WPR;                          // regions per CTA (even)
+  pdl_enter();
+  __shared__ long long red[8];
+  __shared__ long long own[G];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * G;
+  long long s = 0;
+  const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(counts);     // r0 is even
+  for (int64_t i = t; i < (r0 >> 1); i += 256) {
+    const ulonglong2 v = __ldcg(c2 + i);
+    s += (long long)v.x + (long long)v.y;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[wid] = s;
+  if (t < G) own[t] = r0 + t < nregions ? (long long)__ldcg(counts + r0 + t) : 0ll;
+  __syncthreads();
+  const int q = wid / WPR, sub = (wid % WPR) * 32 + lane;
+  long long run0 = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) run0 += red[i];
+#pragma unroll
+  for (int i = 0; i < G; ++i) run0 += i < q ? own[i] : 0ll;
+  const int64_t r = r0 + q;
+  if (r >= nregions) return;
+  const long long n = own[q];
+  if (r == nregions - 1 && sub == 0) *d_count = run0 + n;
+  const long long g0 = r * rwords * 32;
+  if (n <= list_cap) {
+    constexpr int S = 32 * WPR;
+    const uint32_t* sl = slots + (size_t)r * list_cap;
+    for (long long i = sub; i < n; i += 4 * S) {
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = i + u * S < n ? __ldcs(sl + i + u * S) : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u * S < n && run0 + i + u * S < capacity) idx[run0 + i + u * S] = g0 + (long long)v[u];
+    }
+    return;
+  }
+  if (wid % WPR) return;                             // list overflow: one warp re-reads the words
+  const uint32_t* src = det + r * rwords;
+  long long run = run0;
+  for (int64_t w0 = 0; w0 < rwords; w0 += 32) {
+    const int64_t w = w0 + lane;
+    uint32_t v = w < rwords ? src[w] : 0u;
+    const int c = __popc(v);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    long long qo = run + incl - c;
+    while (v) {
+      const int bit = __ffs(v) - 1;
+      v &= v - 1;
+      if (qo < capacity) idx[qo] = g0 + (w << 5) + bit;
+      ++qo;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // K4 compaction: detection bitmap -> ascending flat indices, single pass.  Chunks of
 // kChunkWords words are taken in ticket order (atomic counter), so a chunk's predecessors
@@ -1505,6 +1587,22 @@ rsft_status launch_scan_write(rsft_plan_s* p, int64_t batch, uint32_t* det, int6
   const int64_t np = vote_regions_per_frame(p, 0, n0);
   const int64_t nregions = np * batch;
   const int64_t rwords = ((p->ntot + 31) / 32) / np;
+  const char* nsw = getenv("RSFT_NO_SCANWRITE");     // read per launch: tests select either path
+  if (list && nregions <= kDirectRegions && !(nsw && nsw[0] == '1')) {
+    // 4 warps per region list for large frames (c4: 15 vs 20 us); at c2's 2048-word frames one warp
+    // per region measured faster (17 vs 21 us)
+    const bool wide = rwords >= 4096;
+    cudaError_t le_ = wide
+        ? pdl_launch(k_region_scan_write<4>, (unsigned)((nregions + 1) / 2), 256, 0, st, det, rwords,
+                     p->dev.region_state, reinterpret_cast<long long*>(d_count), nregions, p->dev.region_slots,
+                     reinterpret_cast<long long*>(idx), capacity, (int)p->dev.list_cap)
+        : pdl_launch(k_region_scan_write<1>, (unsigned)((nregions + 7) / 8), 256, 0, st, det, rwords,
+                     p->dev.region_state, reinterpret_cast<long long*>(d_count), nregions, p->dev.region_slots,
+                     reinterpret_cast<long long*>(idx), capacity, (int)p->dev.list_cap);
+    if (le_ != cudaSuccess) return check(le_, "k_region_scan_write launch");
+    p->last_launches += 1;
+    return check(cudaGetLastError(), "k_region_scan_write launch");
+  }
   {
     const int64_t ntiles = (nregions + kScanTile - 1) / kScanTile;
     if (ntiles > p->dev.chunk_capacity) return RSFT_E_WORKSPACE;

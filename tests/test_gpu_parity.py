@@ -227,6 +227,48 @@ def test_3d_votes_bit_identical_full_size(name, monkeypatch):
             np.testing.assert_array_equal(np.asarray(a_), np.asarray(b_))
 
 
+SW_CASES = [c for c in CASES if c[0] in ("1d_g_c1like", "1d_v_dense_pfa", "2d_fused", "2d_v_c4like", "2d_v_dense_mu",
+                                          "2d_v_mu1_dense", "2d_split_rpw1", "3d_c3like_mu")]
+
+
+@pytest.mark.parametrize("case", SW_CASES, ids=[c[0] for c in SW_CASES])
+def test_scan_write_one_launch_vs_two_pass(case, monkeypatch):
+    """The sorted index list through k_region_scan_write (scan + writer in one launch, default for
+    <= 8192 vote regions) and through the two-pass scan + region writer (RSFT_NO_SCANWRITE=1, read
+    per launch): integer work on the same counts, so count and list must be bit-identical -- with
+    batches that span several writer CTAs and a ragged tail, dense spectra whose region lists
+    overflow (the writer re-reads the detection words), and a capacity below the count."""
+    import torch
+    name, n, b, loops, kw, batch, mode = case
+    batch = 37 if len(n) < 3 else 5
+    op = oracle_params(n, b, loops, seed=zlib.crc32(name.encode()) % 1000, noise_var=1.0, **kw)
+    wl = synth.Workload(name, n, b, loops, op.p_fa, 1.0, (3, 8), (0.0, 20.0), batch, data_seed=78)
+    x = torch.from_numpy(frames(wl, batch)).cuda()
+    plan = make_plan(op, max_batch=batch, mode=mode).bind()
+    full = batch * plan.ntot
+    outs = []
+    for env in (None, "1"):
+        monkeypatch.delenv("RSFT_NO_SCANWRITE", raising=False)
+        if env:
+            monkeypatch.setenv("RSFT_NO_SCANWRITE", env)
+        for cap in (full, 7):
+            idx0 = torch.full((cap + 5,), -1, dtype=torch.int64, device="cuda")
+            _, det, idx, cnt = plan.run(x, cap, idx=idx0)
+            _, idx2, cnt2 = plan.detect_compact(plan.execute(x), cap)
+            torch.cuda.synchronize()
+            c = int(cnt.item())
+            assert int(cnt2.item()) == c
+            assert (idx0[cap:] == -1).all()                # nothing written past the capacity
+            outs.append((c, idx.cpu().numpy()[:min(c, cap)], idx2.cpu().numpy()[:min(c, cap)], det.cpu().numpy()))
+    assert outs[0][0] > 0
+    for k in (0, 1):
+        for a_, b_ in zip(outs[k], outs[k + 2]):
+            np.testing.assert_array_equal(np.asarray(a_), np.asarray(b_))
+    c, idx, _, det = outs[0]
+    bits = np.unpackbits(det.view(np.uint8), bitorder="little")
+    np.testing.assert_array_equal(np.flatnonzero(bits), idx)   # ascending flat indices == the set bits
+
+
 V2_CASES = [c for c in CASES if c[0].startswith("2d_") and c[6] == "fused"]
 
 
