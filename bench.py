@@ -430,7 +430,8 @@ def fold_kernel_label(plan, wl, run=False):
         return "k_gather1d (gather-form fold + FFT + threshold)"
     if run and len(wl.n) == 2 and max(wl.loops, 1) <= 8 and wl.b[0] <= 32 and wl.b[1] in (8, 16, 32) \
             and wl.n[1] in (128, 256) and wl.n[0] <= 1024 and not os.environ.get("RSFT_NO_FUSED2V"):
-        return "k_fused2v (fold warps + FFT/threshold/vote warps) + k_scan_tiles/k_scan_apply + k_region_write"
+        return ("k_fused2v (fold warps + FFT/threshold/vote warps) + scan / index writer "
+                "(k_region_scan_write for <= 8192 frames, else k_scan_tiles/k_scan_apply + k_region_write)")
     return "k_fused (pre-window+permute+flat window+fold+FFT+threshold)"
 
 

@@ -438,7 +438,10 @@ static rsft_status launch_f2v_t(rsft_plan_s* p, const void* d_x, int64_t batch, 
   const int W = (int)(p->n[1] / 32);
   int S = 0;
   const char* es = getenv("RSFT_F2V_STAGES");
-  const int smax = es && es[0] ? std::max(2, atoi(es)) : 8;
+  // ring depth per fold warp: 3 stages (2 boxes = 8 KiB ahead per warp, 64 KiB in flight per SM) measured
+  // best -- c4 1.379 ms per step vs 1.399 (4 stages, the most that fit) and 1.436 (2); c2 0.728 vs 0.764
+  // and 0.794 (DESIGN 6.7); the read-only TMA microbenchmark peaks at ~49 KiB in flight per SM too
+  const int smax = es && es[0] ? std::max(2, atoi(es)) : 3;
   for (int s = smax; s >= 2; --s)
     if (f2v_layout(s, p->L, LP, (int)p->n[0], (int)p->b[0], NB1, W, p->dev.wpl).total <= 227 * 1024) { S = s; break; }
   if (!S) return RSFT_E_UNSUPPORTED;
