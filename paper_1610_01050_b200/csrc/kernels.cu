@@ -1804,8 +1804,9 @@ static rsft_status launch_gather1d_t(rsft_plan_s* p, const void* d_x, int64_t ba
   if (S <= 0) S = (int)std::min<size_t>(8, std::max<size_t>(2, (200 * 1024 / ctas - 2048 - vbytes) / fbytes));
   const size_t smem = 16 * S + 128 + (MB > 2 ? 4096 : 1024) + S * fbytes + vbytes;
   const char* env_k = getenv("RSFT_G1_CHUNK");        // bytes per bulk copy (divides the frame)
-  // c1 (32-KiB frames), whole rsft_run step: 2048-B copies 0.901 ms, 4096 0.861, 8192 0.849, 16384 0.842
-  int chunk = env_k && env_k[0] ? atoi(env_k) : (int)std::min<size_t>(fbytes, 16384);
+  // c1 (32-KiB frames), whole rsft_run step: 2048-B copies 0.901 ms, 4096 0.861, 8192 0.849, 16384 0.842,
+  // 32768 (one copy per frame) 0.840
+  int chunk = env_k && env_k[0] ? atoi(env_k) : (int)std::min<size_t>(fbytes, 32768);
   if (chunk <= 0 || chunk % 16 || fbytes % chunk) chunk = (int)fbytes;
   rsft_status s = check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
   if (s) return s;
