@@ -39,7 +39,10 @@ __constant__ float2 c_tw2v[128];   // e^{-j 2 pi k / 128} (fp64-rounded at bind)
 
 constexpr int kF2vFold = 8;        // fold warps: 4 of the 32 residue classes of c4 each
 constexpr int kF2vEpi = 8;         // epilogue (FFT + threshold + vote) warps: one per loop (L <= 8)
-constexpr int kF2vU = 8;           // rows per TMA box (4 KiB)
+#ifndef RSFT_F2V_U
+#define RSFT_F2V_U 8
+#endif
+constexpr int kF2vU = RSFT_F2V_U;   // rows per TMA box (8: 4 KiB; 4 / 16 are tuning builds)
 constexpr int kF2vFB = 2;          // residue-sum slots F (one slot + 5 ring stages measured slower)
 constexpr int kF2vMaxN0 = 1024;    // vote rows per epilogue thread: 32 / NE (N0 <= 1024)
 
