@@ -40,9 +40,9 @@ __constant__ float2 c_tw2v[128];   // e^{-j 2 pi k / 128} (fp64-rounded at bind)
 constexpr int kF2vFold = 8;        // fold warps: 4 of the 32 residue classes of c4 each
 constexpr int kF2vEpi = 8;         // epilogue (FFT + threshold + vote) warps: one per loop (L <= 8)
 #ifndef RSFT_F2V_U
-#define RSFT_F2V_U 8
+#define RSFT_F2V_U 16
 #endif
-constexpr int kF2vU = RSFT_F2V_U;   // rows per TMA box (8: 4 KiB; 4 / 16 are tuning builds)
+constexpr int kF2vU = RSFT_F2V_U;   // rows per TMA box (16: 8 KiB; -DRSFT_F2V_U=4 / 8 are tuning builds, DESIGN 6.7)
 constexpr int kF2vFB = 2;          // residue-sum slots F (one slot + 5 ring stages measured slower)
 constexpr int kF2vMaxN0 = 1024;    // vote rows per epilogue thread: 32 / NE (N0 <= 1024)
 
@@ -444,7 +444,9 @@ static rsft_status launch_f2v_t(rsft_plan_s* p, const void* d_x, int64_t batch, 
   // ring depth per fold warp: 3 stages (2 boxes = 8 KiB ahead per warp, 64 KiB in flight per SM) measured
   // best -- c4 1.379 ms per step vs 1.399 (4 stages, the most that fit) and 1.436 (2); c2 0.728 vs 0.764
   // and 0.794 (DESIGN 6.7); the read-only TMA microbenchmark peaks at ~49 KiB in flight per SM too
-  const int smax = es && es[0] ? std::max(2, atoi(es)) : 3;
+  // With 16-row (8-KiB) boxes, 2 stages (one box ahead per warp, the same 64 KiB in flight, half the box issues
+  // and waits): c4 1.378 ms, c2 0.710 ms (4-row boxes: 1.50 / 0.89 ms).
+  const int smax = es && es[0] ? std::max(2, atoi(es)) : (kF2vU >= 16 ? 2 : 3);
   for (int s = smax; s >= 2; --s)
     if (f2v_layout(s, p->L, LP, (int)p->n[0], (int)p->b[0], NB1, W, p->dev.wpl).total <= 227 * 1024) { S = s; break; }
   if (!S) return RSFT_E_UNSUPPORTED;
